@@ -1,0 +1,76 @@
+"""ORACLE (test infrastructure only) — end-to-end reference solves.
+
+monolithic_solve: the plain definition of the result — u solves K(rho) u = f
+on the free dofs (Eq.(4)), by SuperLU.
+dd_solve: the method step by step in the paper's order (PAPER.md:137-146
+Eq.(7)): interior factorisations -> condensed rhs -> interface PCG with
+H^_theta -> back-substitution.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+import numpy as np
+import scipy.sparse.linalg as spla
+
+from .fem import free_system, true_relres
+from .topology import build_topology
+from .dd import subdomain_blocks, factor_subdomains, schur_apply, condensed_rhs, back_substitute
+from .precond import build_components, apply_precond
+from .krylov import pcg
+
+
+def monolithic_solve(prob):
+    K, f, free = free_system(prob)
+    u = np.zeros(prob.ndof)
+    if len(free):
+        u[free] = spla.splu(K.tocsc()).solve(f)
+    return u
+
+
+@dataclass
+class DDResult:
+    u: np.ndarray
+    iterations: int
+    converged: bool
+    relres: float
+    uG: np.ndarray
+    history: list = field(default_factory=list)
+
+
+class DDOracle:
+    """Setup/factor/solve split mirroring de_setup / de_factor / de_solve."""
+
+    def __init__(self, prob, mode="lanczos", theta=0.5, k=10, inner="X", beta="FR"):
+        self.prob = prob
+        self.topo = build_topology(prob)
+        self.comps = build_components(prob, self.topo) if mode != "identity" else []
+        self.mode, self.theta, self.k, self.inner, self.beta = mode, theta, k, inner, beta
+        self.blocks = None
+        self.uG_prev = None
+
+    def factor(self, prob=None):
+        if prob is not None:
+            self.prob = prob
+        self.blocks = factor_subdomains(subdomain_blocks(self.prob, self.topo))
+
+    def S(self, x):
+        return schur_apply(self.blocks, self.topo.n_G, x)
+
+    def P(self, r):
+        return apply_precond(self.comps, r, self.mode, self.theta, self.k, self.inner)
+
+    def solve(self, rtol=None, maxit=20000, warm=False):
+        prob = self.prob
+        rtol = prob.rtol if rtol is None else rtol
+        if self.blocks is None:
+            self.factor()
+        free = prob.fixed == 0
+        nf = np.linalg.norm(prob.rhs[free])
+        if nf == 0:
+            return DDResult(np.zeros(prob.ndof), 0, True, 0.0, np.zeros(self.topo.n_G))
+        g = condensed_rhs(prob, self.topo, self.blocks)
+        x0 = self.uG_prev if (warm and self.uG_prev is not None) else None
+        uG, its, conv, hist = pcg(self.S, g, self.P, rtol * nf, maxit, x0=x0, beta=self.beta)
+        self.uG_prev = uG
+        u = back_substitute(prob, self.topo, self.blocks, uG)
+        return DDResult(u, its, conv, true_relres(prob, u), uG, hist)
