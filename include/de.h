@@ -1,0 +1,182 @@
+/*
+ * de.h — C ABI of the B200-native interface-PCG solver for SIMP-weighted Q1
+ * linear elasticity by non-overlapping domain decomposition
+ * (arXiv 1501.06211; citations are /root/reference/PAPER.md line numbers).
+ *
+ * The method (Eq. (7)):
+ *   1. K_IiIi u1_Ii = f_Ii                       (interior Dirichlet solves)
+ *   2. S u_Gamma = f_Gamma - sum_i K_GammaIi u1_Ii, S = sum_i R_i^T (A_GG,i - A_GI,i A_II,i^-1 A_IG,i) R_i,
+ *      solved by PCG preconditioned with H^_theta = (+)_c M_c (M_c^-1 L_c)^(1-theta)
+ *      (Eqs. (8)-(9)) applied by inverse Lanczos
+ *   3. K_IiIi u2_Ii = -K_IiGamma u_Gamma,   u = (u1_I, 0) + (u2_I, u_Gamma)
+ * Material (R1/R2): E_e = Emin + rho_e^p (E0 - Emin); 2D plane stress, 3D isotropic,
+ * Hooke's law sigma = 2 mu eps + lambda tr(eps) I. Q1 elements of edge h.
+ *
+ * Conventions (R4):
+ *   node = i + (nx+1)*(j + (ny+1)*k)   (x fastest, k = 0 in 2D)
+ *   dof  = dim*node + c                (component fastest)
+ *   element e = ex + nx*(ey + ny*ez), density[] in that order
+ *   subdomain s = sx + px*(sy + py*sz), each subdomain an axis-aligned box of sub[] elements
+ *
+ * Ownership: the caller owns every host array passed in; the library copies what it needs
+ * during the call and keeps no pointer afterwards. A de_ctx_t owns all device memory it
+ * allocates (cudaMalloc on options.device) until de_destroy. Device pointers passed to the
+ * *_device entry points are borrowed for the duration of the call only.
+ *
+ * Errors: every call returns de_status_t (DE_OK = 0). On failure, de_last_error() returns a
+ * thread-local message. There is no CPU fallback: without a usable CUDA device, de_setup
+ * returns DE_ECUDA.
+ *
+ * Threading: a context is not thread-safe; distinct contexts are independent.
+ * Multi-GPU (nranks > 1): every call is collective over ranks with identical host inputs;
+ * every rank returns the full u. Rank r owns subdomain columns sx in
+ * [floor(r*px/nranks), floor((r+1)*px/nranks)); interface vectors are replicated and the
+ * partial interface sums are combined with one ncclAllReduce per PCG iteration.
+ */
+#ifndef DE_H_
+#define DE_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    DE_OK = 0,
+    DE_EINVAL = -1,      /* invalid argument (partition does not divide mesh, dim not 2/3,
+                            rho <= 0 or non-finite, nu not in (-1, 1/2), E0 <= 0, Emin < 0,
+                            no Dirichlet dof, unsupported option)                          */
+    DE_ENOTSPD = -2,     /* non-positive pivot in an interior factorisation (subdomain id in message) */
+    DE_ENOCONV = -3,     /* max_iter reached; u holds the last iterate        */
+    DE_EBREAKDOWN = -4,  /* p^T S p <= 0, or a non-positive Ritz value (R9)       */
+    DE_ESTATE = -5,      /* de_solve before de_factor                                      */
+    DE_ENOMEM = -6,
+    DE_ECUDA = -7,
+    DE_ENCCL = -8
+} de_status_t;
+
+typedef struct de_ctx de_ctx_t;   /* opaque */
+
+typedef struct {
+    int32_t dim;             /* 2 or 3 */
+    int32_t nel[3];          /* elements per axis; nel[2] ignored when dim == 2 */
+    double h;                /* element edge length (BASELINE: 1.0); 2D thickness 1 */
+    const uint8_t* fixed;    /* host, ndof = dim * prod_a (nel[a]+1) flags; 1 = homogeneous Dirichlet */
+} de_mesh_t;
+
+typedef struct {
+    int32_t sub[3];          /* elements per subdomain per axis; must divide nel */
+} de_partition_t;
+
+typedef struct {
+    double theta;            /* fractional index theta of H~_theta; default 0.5 */
+    int32_t lanczos_k;       /* inverse-Lanczos basis size k; default 10 */
+    int32_t inner_mode;      /* preconditioner: 1 = inverse Lanczos with exact inner solves (mode X,
+                                DESIGN.md R10); 3 = identity S~ = I. (0 = SPEC face-PCG inner: not
+                                on the GPU path yet -> DE_EINVAL) */
+    double inner_tol;        /* reserved for inner_mode 0 */
+    int32_t inner_max_iter;  /* reserved for inner_mode 0 */
+    int32_t max_iter;        /* outer PCG iteration cap; default 20000 */
+    int32_t beta_variant;    /* 0 = Fletcher-Reeves (default), 1 = Polak-Ribiere (flexible) */
+    int32_t warm_start;      /* 1: start PCG from the previous solve's u_Gamma (config-5 sequence) */
+    int32_t rank, nranks;    /* nranks == 1: single GPU, no NCCL */
+    int32_t device;          /* CUDA device ordinal */
+    const void* nccl_id;     /* 128-byte ncclUniqueId (from de_nccl_unique_id on rank 0), nranks > 1 only */
+    void* stream;            /* cudaStream_t to run on, or NULL for a library-owned stream */
+    int32_t check_every;     /* convergence poll period in iterations (device-side early exit makes
+                                extra launches no-ops); default 8 */
+    int32_t use_graph;       /* 1 (default): capture check_every PCG iterations into a CUDA graph */
+    int32_t host_only;       /* 1: run only the host setup (topology, DOF map, skeleton queries);
+                                no device is touched and de_factor/de_solve return DE_ESTATE */
+} de_options_t;
+
+typedef struct {
+    int64_t ndof, n_free, n_I, n_Gamma, n_sub, n_sub_local;
+    int32_t band;            /* uniform half bandwidth of the interior factors */
+    int32_t iterations;      /* outer PCG iterations of the last solve */
+    int32_t restarts;        /* residual-replacement restarts of the last solve */
+    double relres_recursive; /* ||r_Gamma|| / ||f_free|| at exit (recursive residual) */
+    double relres_true;      /* ||f - K u||_2 / ||f||_2 over free dofs (matrix-free K) */
+    double ms_factor;        /* de_factor: SIMP assembly + band Cholesky */
+    double ms_solve;         /* last de_solve, whole call incl. transfers */
+    double ms_pcg;           /* PCG loop only */
+    double ms_schur;         /* sum of Schur-apply kernel time (event-timed when profiling enabled) */
+    double bytes_factor;     /* algorithmic bytes of one pass over the local interior factors */
+    double bytes_iter;       /* algorithmic bytes of one PCG iteration on this rank */
+    int32_t launches_per_iter; /* kernels launched per PCG iteration (graph nodes) */
+    int32_t singular_components; /* bitmask of components using H_theta (R7) */
+    int64_t n_cross[3];      /* cross points / wirebasket nodes per component */
+    int64_t n_faces[3];
+    int64_t n_gamma_c[3];
+} de_stats_t;
+
+/* Fill *opt with defaults (theta 0.5, k 10, inner_mode 1, max_iter 20000, FR, 1 rank). */
+void de_default_options(de_options_t* opt);
+
+/* Setup (host topology + density-independent preconditioner structures, device upload).
+ * density: host, prod(nel) values in (0, inf); E0 > 0; Emin >= 0; p > 0; nu in (-1, 1/2).
+ * PAPER.md:56 (decomposition), :111-120 (interior-first ordering), :167-181 (trace M, L). */
+de_status_t de_setup(const de_mesh_t* mesh, const double* density, double E0, double Emin,
+                     double p, double nu, const de_partition_t* part, const de_options_t* opt,
+                     de_ctx_t** out);
+
+/* Replace the element densities (host array, prod(nel)); de_factor must be called next. */
+de_status_t de_update_densities(de_ctx_t* ctx, const double* density);
+/* Same with a device pointer (float64, prod(nel)) on options.device. */
+de_status_t de_update_densities_device(de_ctx_t* ctx, const double* d_density);
+
+/* SIMP scaling + subdomain blocks A_II (band), A_IG, A_GG (ring) + batched band Cholesky
+ * A_II,i = L_i L_i^T. Returns DE_ENOTSPD on a non-positive pivot. */
+de_status_t de_factor(de_ctx_t* ctx);
+
+/* Solve K(rho) u = f. rhs: host, ndof (Dirichlet entries ignored);
+ * u: host, ndof out (0 at Dirichlet dofs). rtol relative to ||rhs_free||_2 (R11).
+ * iterations/final_relres may be NULL. final_relres = true ||f - K u|| / ||f|| over free dofs. */
+de_status_t de_solve(de_ctx_t* ctx, const double* rhs, double rtol, double* u,
+                     int32_t* iterations, double* final_relres);
+
+/* Same with device-resident rhs and u (float64, ndof, on options.device). */
+de_status_t de_solve_device(de_ctx_t* ctx, const double* d_rhs, double rtol, double* d_u,
+                            int32_t* iterations, double* final_relres);
+
+/* Bit-exact DOF map (R4/R5): cls[ndof] (0 = I, 1 = Gamma, 2 = Dirichlet),
+ * sub[ndof] (owning subdomain of interior dofs, -1 otherwise), reduced[ndof] (canonical index:
+ * interior dofs by (s, dof), then Gamma dofs by dof; -1 for Dirichlet). Any pointer may be NULL. */
+de_status_t de_get_dofmap(const de_ctx_t* ctx, int8_t* cls, int32_t* sub, int32_t* reduced,
+                          int64_t* n_I, int64_t* n_Gamma);
+
+/* Interface skeleton of component c (R6/R8): node ids of Gamma_c (ascending),
+ * per node its face id (-1 for a cross point). Arrays sized n_gamma_c[c] (see de_get_stats). */
+de_status_t de_get_skeleton(const de_ctx_t* ctx, int32_t c, int32_t* nodes, int32_t* face_of_node);
+
+de_status_t de_get_stats(const de_ctx_t* ctx, de_stats_t* stats);
+
+/* ---- component-level entry points (parity tests and profiling) --------------------------
+ * All vectors are device pointers (float64) of the stated lengths. */
+
+/* q = S p over this rank's subdomains, assembled (and all-reduced when nranks > 1); n_Gamma. */
+de_status_t de_schur_apply_device(de_ctx_t* ctx, const double* d_p, double* d_q);
+/* z = H^_theta^-1 r (or r when inner_mode == 3); n_Gamma. */
+de_status_t de_precond_apply_device(de_ctx_t* ctx, const double* d_r, double* d_z);
+/* Lower band of the factor of local subdomain sl: out[n_I_s * (band+1)], column-major,
+ * out[j*(band+1)+k] = L[j+k][j] (k = 0 holds L[j][j] itself). Host pointer. */
+de_status_t de_get_factor_band(const de_ctx_t* ctx, int32_t sl, double* out, int32_t* n_I_s);
+/* Same layout for the assembled A_II,s (before factorisation; recomputed on demand). */
+de_status_t de_get_assembled_band(de_ctx_t* ctx, int32_t sl, double* out, int32_t* n_I_s);
+
+/* NCCL unique id (128 bytes) for a multi-rank setup; call on rank 0 and broadcast. */
+de_status_t de_nccl_unique_id(void* out128);
+
+/* Record per-kernel CUDA-event timing of the Schur apply inside de_solve (bench only). */
+de_status_t de_set_profiling(de_ctx_t* ctx, int32_t on);
+/* Average device time (ms) of one launch of the Schur-apply kernel over the last solve. */
+de_status_t de_get_kernel_time(const de_ctx_t* ctx, double* ms_schur_per_launch, int64_t* launches);
+
+void de_destroy(de_ctx_t* ctx);
+const char* de_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DE_H_ */

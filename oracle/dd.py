@@ -36,8 +36,9 @@ class SubBlocks:
     chol: np.ndarray = None   # lower band Cholesky factor (scipy cholesky_banded layout)
 
 
-def subdomain_blocks(prob, topo):
-    """A_II,i, A_IG,i, A_GG,i from subdomain i's elements only."""
+def subdomain_blocks(prob, topo, only=None):
+    """A_II,i, A_IG,i, A_GG,i from subdomain i's elements only.
+    `only`: optional list of subdomain ids (sampled checks at full size)."""
     KE = element_stiffness(prob.dim, prob.nu, 1.0, prob.h)
     E_e = simp_modulus(prob.density, prob.E0, prob.Emin, prob.p)
     edofs = element_dofs(prob.dim, prob.nel)
@@ -46,7 +47,7 @@ def subdomain_blocks(prob, topo):
     eb = np.searchsorted(topo.elem_sub[order], np.arange(topo.nsub + 1))
     m = edofs.shape[1]
     out = []
-    for s in range(topo.nsub):
+    for s in (range(topo.nsub) if only is None else only):
         els = order[eb[s]:eb[s + 1]]
         ed = edofs[els]
         loc, inv = np.unique(ed, return_inverse=True)

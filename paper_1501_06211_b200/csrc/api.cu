@@ -1,0 +1,1039 @@
+// api.cu — the C ABI of include/de.h: context lifetime, device upload, de_factor, and the
+// de_solve orchestration: condense -> interface PCG (CUDA-graph captured
+// iterations with device-side scalars and early exit) -> back-substitution -> true residual.
+// Multi-GPU: owned subdomain slabs, replicated interface vectors, one ncclAllReduce of the
+// partial interface sums per iteration (NCCL resolved with dlopen; torch has it loaded).
+#include "de_internal.h"
+
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+namespace de {
+
+static thread_local char g_err[1024] = "";
+
+void set_error(const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+// ------------------------------------------------------------------ NCCL (dlopen)
+struct NcclId {
+    char internal[128];
+};
+typedef int (*nccl_get_id_t)(NcclId*);
+typedef int (*nccl_init_rank_t)(void**, int, NcclId, int);
+typedef int (*nccl_allreduce_t)(const void*, void*, size_t, int, int, void*, cudaStream_t);
+typedef int (*nccl_destroy_t)(void*);
+typedef const char* (*nccl_errstr_t)(int);
+struct NcclApi {
+    bool ok = false;
+    nccl_get_id_t get_id = nullptr;
+    nccl_init_rank_t init_rank = nullptr;
+    nccl_allreduce_t allreduce = nullptr;
+    nccl_destroy_t destroy = nullptr;
+    nccl_errstr_t errstr = nullptr;
+};
+static NcclApi& nccl() {
+    static NcclApi api;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            const char* p = getenv("DE_NCCL_LIB");
+            if (p) h = dlopen(p, RTLD_NOW | RTLD_GLOBAL);
+        }
+        if (h) {
+            api.get_id = (nccl_get_id_t)dlsym(h, "ncclGetUniqueId");
+            api.init_rank = (nccl_init_rank_t)dlsym(h, "ncclCommInitRank");
+            api.allreduce = (nccl_allreduce_t)dlsym(h, "ncclAllReduce");
+            api.destroy = (nccl_destroy_t)dlsym(h, "ncclCommDestroy");
+            api.errstr = (nccl_errstr_t)dlsym(h, "ncclGetErrorString");
+            api.ok = api.get_id && api.init_rank && api.allreduce && api.destroy;
+        }
+    }
+    return api;
+}
+
+}  // namespace de
+
+using namespace de;
+
+struct de_ctx {
+    HostSetup hs;
+    de_options_t opt;
+    double E0 = 1, Emin = 0, p = 3, nu = 0.3;
+    cudaStream_t st = nullptr;
+    bool own_stream = false;
+    int rank = 0, nranks = 1;
+    std::vector<int32_t> owned;
+    std::vector<SubDesc> hsd;
+    int nsl = 0, max_nI = 0, max_nG = 0;
+    MeshDev md{};
+    int64_t n_local_I = 0, n_local_G = 0;
+    // device memory
+    std::vector<void*> allocs;
+    SubDesc* d_sd = nullptr;
+    double *d_rho = nullptr, *d_Ee = nullptr;
+    int8_t* d_cls = nullptr;
+    int32_t *d_idofs = nullptr, *d_Rg = nullptr, *d_igp = nullptr, *d_ig_col = nullptr, *d_ig_da = nullptr,
+            *d_ig_db = nullptr, *d_ig_sub = nullptr, *d_gxp = nullptr, *d_gx_col = nullptr, *d_gx_da = nullptr,
+            *d_gx_db = nullptr, *d_gx_sub = nullptr;
+    double *d_ig_val = nullptr, *d_gx_val = nullptr, *d_band = nullptr, *d_scratch = nullptr, *d_qloc = nullptr;
+    int64_t n_ig = 0, n_gx = 0;
+    int32_t *d_gptr = nullptr, *d_gsrc = nullptr, *d_gamma_dofs = nullptr;
+    double *d_fG = nullptr, *d_res = nullptr, *d_ubuf = nullptr, *d_fbuf = nullptr;
+    double *d_x = nullptr, *d_r = nullptr, *d_z = nullptr, *d_p = nullptr, *d_q = nullptr, *d_g = nullptr,
+           *d_rold = nullptr, *d_xprev = nullptr;
+    PcgState* d_state = nullptr;
+    RedBuf rb{};
+    double* d_scal = nullptr;
+    int* d_fail = nullptr;
+    PrecDev P{};
+    bool have_prec = false;
+    bool factored = false, have_prev = false;
+    // graph
+    cudaGraphExec_t gexec = nullptr;
+    int graph_iters = 0;
+    bool graph_prof = false;
+    int launches_per_iter = 0;
+    // profiling
+    bool profiling = false;
+    std::vector<cudaEvent_t> ev;
+    double prof_ms = 0.0;
+    int64_t prof_n = 0;
+    // nccl
+    void* comm = nullptr;
+    de_stats_t stats{};
+};
+
+namespace {
+
+template <class T>
+de_status_t dalloc(de_ctx* c, T** p, size_t n) {
+    *p = nullptr;
+    if (n == 0) n = 1;
+    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), n * sizeof(T));
+    if (e != cudaSuccess) {
+        set_error("cudaMalloc(%zu bytes) failed: %s", n * sizeof(T), cudaGetErrorString(e));
+        return e == cudaErrorMemoryAllocation ? DE_ENOMEM : DE_ECUDA;
+    }
+    c->allocs.push_back(*p);
+    return DE_OK;
+}
+
+template <class T>
+de_status_t dupload(de_ctx* c, T** p, const std::vector<T>& h) {
+    de_status_t s = dalloc(c, p, h.size());
+    if (s != DE_OK) return s;
+    if (!h.empty()) DE_CUDA(cudaMemcpyAsync(*p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, c->st));
+    return DE_OK;
+}
+
+#define TRY(x)                          \
+    do {                                \
+        de_status_t s_ = (x);           \
+        if (s_ != DE_OK) return s_;     \
+    } while (0)
+
+de_status_t check_launch() {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        set_error("kernel launch failed: %s", cudaGetErrorString(e));
+        return DE_ECUDA;
+    }
+    return DE_OK;
+}
+
+de_status_t allreduce(de_ctx* c, double* buf, size_t n) {
+    if (c->nranks <= 1) return DE_OK;
+    int r = nccl().allreduce(buf, buf, n, 8 /*ncclFloat64*/, 0 /*ncclSum*/, c->comm, c->st);
+    if (r != 0) {
+        set_error("ncclAllReduce failed: %s", nccl().errstr ? nccl().errstr(r) : "?");
+        return DE_ENCCL;
+    }
+    return DE_OK;
+}
+
+SchurArgs schur_args(de_ctx* c, int mode, const double* xin, const double* f, double* u, const PcgState* s) {
+    SchurArgs a{};
+    a.sd = c->d_sd;
+    a.nsl = c->nsl;
+    a.band = c->d_band;
+    a.ld = c->hs.ld;
+    a.band_w = c->hs.band;
+    a.idofs = c->d_idofs;
+    a.Rg = c->d_Rg;
+    a.igp = c->d_igp;
+    a.ig_col = c->d_ig_col;
+    a.ig_val = c->d_ig_val;
+    a.gxp = c->d_gxp;
+    a.gx_col = c->d_gx_col;
+    a.gx_val = c->d_gx_val;
+    a.scratch = c->d_scratch;
+    a.xin = xin;
+    a.f = f;
+    a.qloc = c->d_qloc;
+    a.u = u;
+    a.state = s;
+    a.mode = mode;
+    a.maxG = c->max_nG;
+    return a;
+}
+
+// q = S x (assembled over ranks). Used outside the captured loop.
+de_status_t schur_apply(de_ctx* c, const double* x, double* q) {
+    launch_schur_local(schur_args(c, SCHUR_APPLY, x, nullptr, nullptr, nullptr), c->st);
+    launch_gather(c->d_gptr, c->d_gsrc, c->d_qloc, nullptr, q, c->hs.n_G, nullptr, c->st);
+    TRY(check_launch());
+    return allreduce(c, q, size_t(c->hs.n_G));
+}
+
+de_status_t precond(de_ctx* c, const double* r, double* z, const PcgState* s, int* nl) {
+    if (c->have_prec) {
+        prec_apply(c->P, r, z, s, c->st, nl);
+    } else {
+        launch_copy(z, r, c->hs.n_G, s, c->st);
+        if (nl) *nl = 1;
+    }
+    return check_launch();
+}
+
+// one PCG iteration (all on c->st; capturable)
+de_status_t pcg_iteration(de_ctx* c, int* nl, cudaEvent_t e0, cudaEvent_t e1) {
+    const int64_t nG = c->hs.n_G;
+    int n = 0;
+    if (e0) cudaEventRecord(e0, c->st);
+    launch_schur_local(schur_args(c, SCHUR_APPLY, c->d_p, nullptr, nullptr, c->d_state), c->st);
+    if (e1) cudaEventRecord(e1, c->st);
+    launch_gather(c->d_gptr, c->d_gsrc, c->d_qloc, nullptr, c->d_q, nG, c->d_state, c->st);
+    n += 2;
+    TRY(allreduce(c, c->d_q, size_t(nG)));
+    const bool pr = c->opt.beta_variant == 1;
+    launch_pcg_pq(c->d_p, c->d_q, nG, c->rb, c->d_state, c->st);
+    launch_pcg_update_xr(c->d_x, c->d_r, pr ? c->d_rold : nullptr, c->d_p, c->d_q, nG, c->rb, c->d_state, c->st);
+    n += 2;
+    int np = 0;
+    TRY(precond(c, c->d_r, c->d_z, c->d_state, &np));
+    n += np;
+    launch_pcg_rz(c->d_r, c->d_z, c->d_rold, nG, pr ? 1 : 0, c->rb, c->d_state, c->st);
+    launch_pcg_update_p(c->d_p, c->d_z, nG, c->d_state, c->st);
+    n += 2;
+    if (nl) *nl = n;
+    return check_launch();
+}
+
+de_status_t build_graph(de_ctx* c) {
+    if (c->gexec) {
+        cudaGraphExecDestroy(c->gexec);
+        c->gexec = nullptr;
+    }
+    const int ni = std::max(1, c->opt.check_every);
+    const bool prof = c->profiling;
+    if (prof && int(c->ev.size()) < 2 * ni) {
+        for (auto e : c->ev) cudaEventDestroy(e);
+        c->ev.assign(2 * ni, nullptr);
+        for (auto& e : c->ev) DE_CUDA(cudaEventCreate(&e));
+    }
+    cudaGraph_t g;
+    DE_CUDA(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
+    de_status_t s = DE_OK;
+    for (int i = 0; i < ni && s == DE_OK; ++i)
+        s = pcg_iteration(c, &c->launches_per_iter, prof ? c->ev[2 * i] : nullptr, prof ? c->ev[2 * i + 1] : nullptr);
+    cudaError_t e = cudaStreamEndCapture(c->st, &g);
+    if (s != DE_OK) return s;
+    DE_CUDA(e);
+    e = cudaGraphInstantiate(&c->gexec, g, 0);
+    cudaGraphDestroy(g);
+    DE_CUDA(e);
+    c->graph_iters = ni;
+    c->graph_prof = prof;
+    return DE_OK;
+}
+
+de_status_t read_state(de_ctx* c, PcgState* h) {
+    DE_CUDA(cudaMemcpyAsync(h, c->d_state, sizeof(PcgState), cudaMemcpyDeviceToHost, c->st));
+    DE_CUDA(cudaStreamSynchronize(c->st));
+    return DE_OK;
+}
+
+de_status_t run_loop(de_ctx* c, PcgState& hsv) {
+    const bool use_graph = c->opt.use_graph != 0;
+    if (use_graph && (!c->gexec || c->graph_prof != c->profiling)) TRY(build_graph(c));
+    while (true) {
+        const int it_before = hsv.it;
+        if (use_graph) {
+            DE_CUDA(cudaGraphLaunch(c->gexec, c->st));
+        } else {
+            const int ni = std::max(1, c->opt.check_every);
+            for (int i = 0; i < ni; ++i) TRY(pcg_iteration(c, &c->launches_per_iter, nullptr, nullptr));
+        }
+        TRY(read_state(c, &hsv));
+        if (use_graph && c->graph_prof) {
+            const int ran = std::min(hsv.it - it_before, c->graph_iters);
+            for (int i = 0; i < ran; ++i) {
+                float ms = 0.f;
+                if (cudaEventElapsedTime(&ms, c->ev[2 * i], c->ev[2 * i + 1]) == cudaSuccess) {
+                    c->prof_ms += ms;
+                    c->prof_n += 1;
+                }
+            }
+        }
+        if (hsv.done) break;
+    }
+    return DE_OK;
+}
+
+de_status_t masked_norm2(de_ctx* c, const double* f, double* out_host) {
+    launch_copy(c->d_res, f, c->hs.ndof, nullptr, c->st);
+    launch_zero_dirichlet(c->d_cls, c->d_res, c->hs.ndof, c->st);
+    launch_norm2(c->d_res, c->hs.ndof, c->rb, c->d_scal, c->st);
+    TRY(check_launch());
+    DE_CUDA(cudaMemcpyAsync(out_host, c->d_scal, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    DE_CUDA(cudaStreamSynchronize(c->st));
+    return DE_OK;
+}
+
+de_status_t upload_prec(de_ctx* c) {
+    HostSetup& hs = c->hs;
+    PrecDev& P = c->P;
+    P.ncomp = hs.ncomp;
+    P.nflat = int32_t(hs.comp_off[hs.ncomp]);
+    P.kmax = std::min(std::max(1, c->opt.lanczos_k), KMAX);
+    for (int i = 0; i <= MAXC; ++i) P.comp_off[i] = hs.comp_off[std::min(i, hs.ncomp)];
+    for (int i = 0; i < MAXC; ++i) P.singular[i] = (hs.singular_mask >> i) & 1;
+    P.theta = c->opt.theta;
+    TRY(dupload(c, &P.cmap, hs.cmap));
+    auto up_csr = [&](const HCsr& A, CsrDev& D) -> de_status_t {
+        D.n = A.n;
+        TRY(dupload(c, &D.ptr, A.ptr));
+        TRY(dupload(c, &D.col, A.col));
+        TRY(dupload(c, &D.val, A.val));
+        return DE_OK;
+    };
+    TRY(up_csr(hs.M, P.M));
+    TRY(up_csr(hs.L, P.L));
+    TRY(up_csr(hs.K, P.K));
+    double* gjbuf = nullptr;
+    int64_t maxsc = 0;
+    for (const HElim* E : {&hs.elimK, &hs.elimM})
+        for (int cc = 0; cc < hs.ncomp; ++cc) maxsc = std::max(maxsc, E->sc_off[cc + 1] - E->sc_off[cc]);
+    TRY(dalloc(c, &gjbuf, size_t(std::max<int64_t>(maxsc, 1))));
+    auto up_elim = [&](const HElim& E, ElimDev& D) -> de_status_t {
+        D.nfaces = E.nfaces;
+        D.ncross = E.ncross;
+        D.ncomp = hs.ncomp;
+        int mf = 1, mfac = 1;
+        for (int F = 0; F < E.nfaces; ++F) {
+            const int n = E.face_off[F + 1] - E.face_off[F];
+            mf = std::max(mf, n);
+            mfac = std::max(mfac, int(E.face_fac_off[F + 1] - E.face_fac_off[F]));
+        }
+        if (mf > 0xffff || mfac > 0x7fff) {
+            set_error("interface face too large for the face-solve kernel");
+            return DE_EINVAL;
+        }
+        D.maxface = (mfac << 16) | mf;
+        TRY(dupload(c, &D.face_off, E.face_off));
+        TRY(dupload(c, &D.face_nodes, E.face_nodes));
+        TRY(dupload(c, &D.face_band, E.face_band));
+        TRY(dupload(c, &D.face_fac_off, E.face_fac_off));
+        TRY(dupload(c, &D.face_fac, E.face_fac));
+        TRY(dupload(c, &D.cross_flat, E.cross_flat));
+        for (int i = 0; i <= MAXC; ++i) D.cross_comp_off[i] = E.cross_comp_off[i];
+        TRY(dupload(c, &D.xcf_ptr, E.XCF.ptr));
+        TRY(dupload(c, &D.xcf_col, E.XCF.col));
+        TRY(dupload(c, &D.xcf_val, E.XCF.val));
+        TRY(dupload(c, &D.xfc_ptr, E.XFC.ptr));
+        TRY(dupload(c, &D.xfc_col, E.XFC.col));
+        TRY(dupload(c, &D.xfc_val, E.XFC.val));
+        for (int i = 0; i <= MAXC; ++i) D.sc_off[i] = E.sc_off[std::min(i, hs.ncomp)];
+        TRY(dupload(c, &D.Sinv, E.SC));
+        for (int cc = 0; cc < hs.ncomp; ++cc) {   // S_C^-1 by Gauss-Jordan on the device (setup only)
+            const int nc = E.cross_comp_off[cc + 1] - E.cross_comp_off[cc];
+            if (nc > 0) launch_gauss_jordan(D.Sinv + E.sc_off[cc], gjbuf, nc, c->st);
+        }
+        return check_launch();
+    };
+    TRY(up_elim(hs.elimK, P.eK));
+    TRY(up_elim(hs.elimM, P.eM));
+    const size_t nf = size_t(P.nflat);
+    TRY(dalloc(c, &P.rf, nf));
+    TRY(dalloc(c, &P.s, nf));
+    TRY(dalloc(c, &P.v, nf));
+    TRY(dalloc(c, &P.w, nf));
+    TRY(dalloc(c, &P.Mw, nf));
+    TRY(dalloc(c, &P.y, 2 * nf + 16));
+    TRY(dalloc(c, &P.zf, nf));
+    TRY(dalloc(c, &P.W, nf * KMAX));
+    TRY(dalloc(c, &P.LW, nf * KMAX));
+    TRY(dalloc(c, &P.MW, nf * KMAX));
+    DE_CUDA(cudaMemsetAsync(P.W, 0, nf * KMAX * sizeof(double), c->st));
+    TRY(dalloc(c, &P.lz, MAXC));
+    DE_CUDA(cudaMemsetAsync(P.lz, 0, MAXC * sizeof(LzState), c->st));
+    int64_t maxc = 1;
+    for (int cc = 0; cc < hs.ncomp; ++cc) maxc = std::max(maxc, hs.comp_off[cc + 1] - hs.comp_off[cc]);
+    P.nblk = int(std::max<int64_t>(1, std::min<int64_t>(64, (maxc + 4095) / 4096)));
+    const int nslots = 8 + MAXC * KMAX + MAXC * (KMAX * (KMAX + 1) + KMAX);
+    TRY(dalloc(c, &P.part, size_t(nslots) * P.nblk));
+    TRY(dalloc(c, &P.counter, size_t(nslots)));
+    DE_CUDA(cudaMemsetAsync(P.counter, 0, size_t(nslots) * sizeof(unsigned int), c->st));
+    prec_prepare(P);
+    c->have_prec = true;
+    return DE_OK;
+}
+
+de_status_t setup_impl(const de_mesh_t* mesh, const double* density, double E0, double Emin, double p,
+                       double nu, const de_partition_t* part, const de_options_t* opt_in, de_ctx* c) {
+    de_options_t opt;
+    if (opt_in) opt = *opt_in;
+    else de_default_options(&opt);
+    if (!mesh || !part || !density || !mesh->fixed) {
+        set_error("null argument");
+        return DE_EINVAL;
+    }
+    if (!(E0 > 0) || !(Emin >= 0) || !(p > 0) || !(nu > -1.0 && nu < 0.5) || !(mesh->h > 0)) {
+        set_error("invalid material parameters (E0 > 0, Emin >= 0, p > 0, -1 < nu < 1/2, h > 0)");
+        return DE_EINVAL;
+    }
+    if (opt.inner_mode != 1 && opt.inner_mode != 3) {
+        set_error("inner_mode %d not supported on the GPU path (1 = exact-inner inverse Lanczos, 3 = identity)",
+                  opt.inner_mode);
+        return DE_EINVAL;
+    }
+    if (opt.inner_mode == 1 && (opt.lanczos_k < 1 || opt.lanczos_k > KMAX)) {
+        set_error("lanczos_k must be in [1, %d]", KMAX);
+        return DE_EINVAL;
+    }
+    if (opt.nranks < 1 || opt.rank < 0 || opt.rank >= opt.nranks) {
+        set_error("bad rank/nranks");
+        return DE_EINVAL;
+    }
+    c->opt = opt;
+    c->E0 = E0;
+    c->Emin = Emin;
+    c->p = p;
+    c->nu = nu;
+    c->rank = opt.rank;
+    c->nranks = opt.nranks;
+    TRY(host_setup(mesh, part, nu, c->hs));
+    HostSetup& hs = c->hs;
+    for (int64_t e = 0; e < hs.nelem; ++e)
+        if (!(density[e] > 0.0) || !std::isfinite(density[e])) {
+            set_error("density[%lld] = %g must be positive and finite", (long long)e, density[e]);
+            return DE_EINVAL;
+        }
+    c->stats.ndof = hs.ndof;
+    c->stats.n_free = hs.n_free;
+    c->stats.n_I = hs.n_I;
+    c->stats.n_Gamma = hs.n_G;
+    c->stats.n_sub = hs.nsub;
+    for (int cc = 0; cc < hs.ncomp; ++cc) c->stats.n_gamma_c[cc] = hs.comp_off[cc + 1] - hs.comp_off[cc];
+    if (opt.host_only) return DE_OK;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        set_error("no CUDA device available (libde has no CPU path)");
+        return DE_ECUDA;
+    }
+    DE_CUDA(cudaSetDevice(opt.device));
+    if (opt.stream) {
+        c->st = static_cast<cudaStream_t>(opt.stream);
+    } else {
+        DE_CUDA(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+        c->own_stream = true;
+    }
+    // ---- ownership: slabs of subdomain columns along x
+    const int px = hs.ps[0];
+    const int lo = int((int64_t(c->rank) * px) / c->nranks), hi = int((int64_t(c->rank + 1) * px) / c->nranks);
+    for (int s = 0; s < hs.nsub; ++s) {
+        const int sx = s % px;
+        if (sx >= lo && sx < hi) c->owned.push_back(s);
+    }
+    c->nsl = int(c->owned.size());
+    HRing ring;
+    build_ring(hs, c->owned, ring);
+    std::vector<int32_t> idofs, Rg, ig_sub, gx_sub;
+    int64_t ioff = 0, goff = 0;
+    for (int k = 0; k < c->nsl; ++k) {
+        const int s = c->owned[k];
+        SubDesc d{};
+        d.gid = s;
+        d.nI = hs.nI[s];
+        d.nG = hs.nGs[s];
+        d.ioff = ioff;
+        d.band_off = ioff * hs.ld;
+        d.goff = goff;
+        d.igp_off = ring.igp_off[k];
+        d.gxp_off = ring.gxp_off[k];
+        c->hsd.push_back(d);
+        idofs.insert(idofs.end(), hs.idofs.begin() + hs.ioff[s], hs.idofs.begin() + hs.ioff[s + 1]);
+        for (int l = 0; l < d.nG; ++l) Rg.push_back(hs.gpos[hs.gdofs[hs.goff[s] + l]]);
+        c->max_nI = std::max(c->max_nI, d.nI);
+        c->max_nG = std::max(c->max_nG, d.nG);
+        ioff += d.nI;
+        goff += d.nG;
+        const int32_t ig0 = ring.igp[ring.igp_off[k]], ig1 = ring.igp[ring.igp_off[k] + d.nI];
+        ig_sub.insert(ig_sub.end(), size_t(ig1 - ig0), s);
+        const int32_t gx0 = ring.gxp[ring.gxp_off[k]], gx1 = ring.gxp[ring.gxp_off[k] + d.nG];
+        gx_sub.insert(gx_sub.end(), size_t(gx1 - gx0), s);
+    }
+    c->n_local_I = ioff;
+    c->n_local_G = goff;
+    // ---- interface gather table (owned contributions, ascending subdomain)
+    std::vector<int32_t> gcnt(hs.n_G + 1, 0);
+    for (int32_t g : Rg) gcnt[g + 1]++;
+    for (int64_t g = 0; g < hs.n_G; ++g) gcnt[g + 1] += gcnt[g];
+    std::vector<int32_t> gsrc(Rg.size());
+    {
+        std::vector<int32_t> fill(gcnt.begin(), gcnt.end() - 1);
+        for (size_t i = 0; i < Rg.size(); ++i) gsrc[fill[Rg[i]]++] = int32_t(i);
+    }
+    // ---- device upload
+    c->md.dim = hs.dim;
+    for (int a = 0; a < 3; ++a) {
+        c->md.nel[a] = hs.nel[a];
+        c->md.nn[a] = hs.nn[a];
+        c->md.sub[a] = hs.sub[a];
+        c->md.ps[a] = hs.ps[a];
+    }
+    c->md.nke = hs.nke;
+    upload_KE0(hs.KE0, hs.nke, c->st);
+    TRY(dupload(c, &c->d_sd, c->hsd));
+    TRY(dalloc(c, &c->d_rho, hs.nelem));
+    DE_CUDA(cudaMemcpyAsync(c->d_rho, density, sizeof(double) * hs.nelem, cudaMemcpyHostToDevice, c->st));
+    TRY(dalloc(c, &c->d_Ee, hs.nelem));
+    TRY(dupload(c, &c->d_cls, hs.cls));
+    TRY(dupload(c, &c->d_idofs, idofs));
+    TRY(dupload(c, &c->d_Rg, Rg));
+    TRY(dupload(c, &c->d_igp, ring.igp));
+    TRY(dupload(c, &c->d_ig_col, ring.ig_col));
+    TRY(dupload(c, &c->d_ig_da, ring.ig_da));
+    TRY(dupload(c, &c->d_ig_db, ring.ig_db));
+    TRY(dupload(c, &c->d_ig_sub, ig_sub));
+    TRY(dupload(c, &c->d_gxp, ring.gxp));
+    TRY(dupload(c, &c->d_gx_col, ring.gx_col));
+    TRY(dupload(c, &c->d_gx_da, ring.gx_da));
+    TRY(dupload(c, &c->d_gx_db, ring.gx_db));
+    TRY(dupload(c, &c->d_gx_sub, gx_sub));
+    c->n_ig = int64_t(ring.ig_col.size());
+    c->n_gx = int64_t(ring.gx_col.size());
+    TRY(dalloc(c, &c->d_ig_val, size_t(c->n_ig)));
+    TRY(dalloc(c, &c->d_gx_val, size_t(c->n_gx)));
+    TRY(dalloc(c, &c->d_band, size_t(c->n_local_I) * hs.ld));
+    TRY(dalloc(c, &c->d_scratch, size_t(c->n_local_I) + 32));
+    TRY(dalloc(c, &c->d_qloc, size_t(c->n_local_G) + 32));
+    TRY(dupload(c, &c->d_gptr, gcnt));
+    TRY(dupload(c, &c->d_gsrc, gsrc));
+    TRY(dupload(c, &c->d_gamma_dofs, hs.gamma_dofs));
+    const size_t nG = size_t(hs.n_G) + 32, nd = size_t(hs.ndof);
+    for (double** v : {&c->d_x, &c->d_r, &c->d_z, &c->d_p, &c->d_q, &c->d_g, &c->d_rold, &c->d_xprev, &c->d_fG})
+        TRY(dalloc(c, v, nG));
+    DE_CUDA(cudaMemsetAsync(c->d_x, 0, nG * sizeof(double), c->st));
+    DE_CUDA(cudaMemsetAsync(c->d_rold, 0, nG * sizeof(double), c->st));
+    TRY(dalloc(c, &c->d_res, nd));
+    TRY(dalloc(c, &c->d_ubuf, nd));
+    TRY(dalloc(c, &c->d_fbuf, nd));
+    TRY(dalloc(c, &c->d_state, 1));
+    TRY(dalloc(c, &c->d_scal, 8));
+    TRY(dalloc(c, &c->d_fail, 1));
+    c->rb.nblk = 148 * 2;
+    TRY(dalloc(c, &c->rb.part, size_t(c->rb.nblk) * 4));
+    TRY(dalloc(c, &c->rb.counter, 1));
+    DE_CUDA(cudaMemsetAsync(c->rb.counter, 0, sizeof(unsigned int), c->st));
+    if (opt.inner_mode == 1) TRY(upload_prec(c));
+    DE_CUDA(cudaStreamSynchronize(c->st));
+    TRY(check_launch());
+    // ---- NCCL
+    if (c->nranks > 1) {
+        if (!nccl().ok) {
+            set_error("nranks > 1 but libnccl.so.2 could not be loaded");
+            return DE_ENCCL;
+        }
+        if (!opt.nccl_id) {
+            set_error("nranks > 1 requires options.nccl_id");
+            return DE_EINVAL;
+        }
+        NcclId id;
+        memcpy(id.internal, opt.nccl_id, 128);
+        int r = nccl().init_rank(&c->comm, c->nranks, id, c->rank);
+        if (r != 0) {
+            set_error("ncclCommInitRank failed: %s", nccl().errstr ? nccl().errstr(r) : "?");
+            return DE_ENCCL;
+        }
+    }
+    // ---- stats
+    de_stats_t& S = c->stats;
+    S.ndof = hs.ndof;
+    S.n_free = hs.n_free;
+    S.n_I = hs.n_I;
+    S.n_Gamma = hs.n_G;
+    S.n_sub = hs.nsub;
+    S.n_sub_local = c->nsl;
+    S.band = hs.band;
+    S.singular_components = hs.singular_mask;
+    for (int cc = 0; cc < hs.ncomp; ++cc) {
+        S.n_cross[cc] = hs.n_cross_c[cc];
+        S.n_faces[cc] = hs.n_faces_c[cc];
+        S.n_gamma_c[cc] = hs.comp_off[cc + 1] - hs.comp_off[cc];
+    }
+    // algorithmic bytes of one Schur apply on this rank: one pass over the factor band entries
+    // (b+1 per row) + the ring matrices + the local interface vectors
+    double fb = 0.0;
+    for (const auto& d : c->hsd) fb += double(d.nI) * (hs.band + 1) * 8.0;
+    S.bytes_factor = fb;
+    S.bytes_iter = fb + double(c->n_ig + c->n_gx) * 12.0 + double(c->n_local_G) * 8.0 * 3.0 +
+                   double(hs.n_G) * 8.0 * 11.0;
+    return DE_OK;
+}
+
+de_status_t factor_impl(de_ctx* c) {
+    HostSetup& hs = c->hs;
+    if (c->opt.host_only) {
+        set_error("context was created with host_only = 1");
+        return DE_ESTATE;
+    }
+    cudaEvent_t e0, e1;
+    DE_CUDA(cudaEventCreate(&e0));
+    DE_CUDA(cudaEventCreate(&e1));
+    DE_CUDA(cudaEventRecord(e0, c->st));
+    launch_simp(c->d_rho, c->d_Ee, hs.nelem, c->E0, c->Emin, c->p, c->st);
+    launch_assemble_band(c->md, c->d_sd, c->nsl, c->d_idofs, c->d_Ee, c->d_band, hs.ld, hs.band, c->max_nI, c->st);
+    launch_assemble_pairs(c->md, c->d_ig_da, c->d_ig_db, c->d_ig_sub, c->d_Ee, c->d_ig_val, c->n_ig, c->st);
+    launch_assemble_pairs(c->md, c->d_gx_da, c->d_gx_db, c->d_gx_sub, c->d_Ee, c->d_gx_val, c->n_gx, c->st);
+    DE_CUDA(cudaMemsetAsync(c->d_fail, 0, sizeof(int), c->st));
+    launch_band_cholesky(c->d_sd, c->nsl, c->d_band, hs.ld, hs.band, c->d_fail, c->st);
+    TRY(check_launch());
+    DE_CUDA(cudaEventRecord(e1, c->st));
+    int fail = 0;
+    DE_CUDA(cudaMemcpyAsync(&fail, c->d_fail, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+    DE_CUDA(cudaStreamSynchronize(c->st));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    c->stats.ms_factor = ms;
+    if (fail) {
+        c->factored = false;
+        set_error("non-positive pivot in the interior factorisation of subdomain %d", fail - 1);
+        return DE_ENOTSPD;
+    }
+    c->factored = true;
+    return DE_OK;
+}
+
+de_status_t solve_impl(de_ctx* c, const double* d_f, double rtol, double* d_u, int32_t* iters, double* relres) {
+    if (!c->factored) {
+        set_error("de_solve called before a successful de_factor");
+        return DE_ESTATE;
+    }
+    if (!(rtol > 0)) {
+        set_error("rtol must be positive");
+        return DE_EINVAL;
+    }
+    HostSetup& hs = c->hs;
+    const int64_t nG = hs.n_G;
+    auto t0 = std::chrono::steady_clock::now();
+    double f2 = 0.0;
+    TRY(masked_norm2(c, d_f, &f2));
+    const double fnorm = std::sqrt(f2);
+    DE_CUDA(cudaMemsetAsync(d_u, 0, sizeof(double) * hs.ndof, c->st));
+    c->stats.iterations = 0;
+    c->stats.restarts = 0;
+    if (fnorm == 0.0) {
+        DE_CUDA(cudaStreamSynchronize(c->st));
+        if (iters) *iters = 0;
+        if (relres) *relres = 0.0;
+        c->stats.relres_true = c->stats.relres_recursive = 0.0;
+        return DE_OK;
+    }
+    // condensed rhs g = f_G - sum_s R_s^T A_GI,s A_II,s^-1 f_I,s
+    launch_gather_gamma(c->d_gamma_dofs, d_f, c->d_fG, nG, c->st);
+    launch_schur_local(schur_args(c, SCHUR_CONDENSE, nullptr, d_f, nullptr, nullptr), c->st);
+    launch_gather(c->d_gptr, c->d_gsrc, c->d_qloc, c->rank == 0 ? c->d_fG : nullptr, c->d_g, nG, nullptr, c->st);
+    TRY(check_launch());
+    TRY(allreduce(c, c->d_g, size_t(nG)));
+    PcgState hsv{};
+    hsv.tol2 = (rtol * fnorm) * (rtol * fnorm);
+    hsv.maxit = c->opt.max_iter > 0 ? c->opt.max_iter : 20000;
+    DE_CUDA(cudaMemcpyAsync(c->d_state, &hsv, sizeof(PcgState), cudaMemcpyHostToDevice, c->st));
+    const bool warm = c->opt.warm_start && c->have_prev;
+    cudaEvent_t l0, l1;
+    DE_CUDA(cudaEventCreate(&l0));
+    DE_CUDA(cudaEventCreate(&l1));
+    DE_CUDA(cudaEventRecord(l0, c->st));
+    if (warm) {
+        launch_copy(c->d_x, c->d_xprev, nG, nullptr, c->st);
+        TRY(schur_apply(c, c->d_x, c->d_q));
+        launch_pcg_init(c->d_r, c->d_p, c->d_z, c->d_g, c->d_q, nG, 1, c->rb, c->d_state, c->st);
+    } else {
+        DE_CUDA(cudaMemsetAsync(c->d_x, 0, sizeof(double) * nG, c->st));
+        launch_pcg_init(c->d_r, c->d_p, c->d_z, c->d_g, nullptr, nG, 0, c->rb, c->d_state, c->st);
+    }
+    int restarts = 0;
+    while (true) {
+        TRY(precond(c, c->d_r, c->d_z, c->d_state, nullptr));
+        launch_pcg_init(c->d_r, c->d_p, c->d_z, c->d_g, nullptr, nG, 2, c->rb, c->d_state, c->st);
+        TRY(check_launch());
+        TRY(read_state(c, &hsv));
+        if (!hsv.done) TRY(run_loop(c, hsv));
+        if (hsv.status == DE_EBREAKDOWN) break;
+        // residual replacement (R11): recompute r = g - S x and continue if needed
+        TRY(schur_apply(c, c->d_x, c->d_q));
+        const int it_keep = hsv.it;
+        launch_pcg_init(c->d_r, c->d_p, c->d_z, c->d_g, c->d_q, nG, 1, c->rb, c->d_state, c->st);
+        TRY(check_launch());
+        TRY(read_state(c, &hsv));
+        if (hsv.done || hsv.it >= hsv.maxit || restarts >= 5) {
+            hsv.it = it_keep;
+            break;
+        }
+        ++restarts;
+        hsv.status = 0;
+        DE_CUDA(cudaMemcpyAsync(c->d_state, &hsv, sizeof(PcgState), cudaMemcpyHostToDevice, c->st));
+    }
+    DE_CUDA(cudaEventRecord(l1, c->st));
+    // back-substitution u_I = A_II^-1 (f_I - A_IG u_G); u_G = x; u_D = 0
+    if (c->rank == 0) launch_scatter_gamma(c->d_gamma_dofs, c->d_x, d_u, nG, c->st);
+    launch_schur_local(schur_args(c, SCHUR_BACKSUB, c->d_x, d_f, d_u, nullptr), c->st);
+    TRY(check_launch());
+    TRY(allreduce(c, d_u, size_t(hs.ndof)));
+    launch_copy(c->d_xprev, c->d_x, nG, nullptr, c->st);
+    c->have_prev = true;
+    // true residual ||f - K u|| / ||f|| over free dofs (matrix-free)
+    launch_apply_K(c->md, c->d_Ee, d_u, d_f, c->d_cls, c->d_res, hs.ndof, c->st);
+    launch_norm2(c->d_res, hs.ndof, c->rb, c->d_scal, c->st);
+    TRY(check_launch());
+    double r2 = 0.0;
+    DE_CUDA(cudaMemcpyAsync(&r2, c->d_scal, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    DE_CUDA(cudaStreamSynchronize(c->st));
+    float lms = 0.f;
+    cudaEventElapsedTime(&lms, l0, l1);
+    cudaEventDestroy(l0);
+    cudaEventDestroy(l1);
+    auto t1 = std::chrono::steady_clock::now();
+    c->stats.iterations = hsv.it;
+    c->stats.restarts = restarts;
+    c->stats.relres_recursive = std::sqrt(std::max(hsv.rr, 0.0)) / fnorm;
+    c->stats.relres_true = std::sqrt(r2) / fnorm;
+    c->stats.ms_pcg = lms;
+    c->stats.ms_solve = std::chrono::duration<double, std::milli>(t1 - t0).count();
+    c->stats.launches_per_iter = c->launches_per_iter;
+    if (iters) *iters = hsv.it;
+    if (relres) *relres = c->stats.relres_true;
+    if (hsv.status == DE_EBREAKDOWN) {
+        set_error("PCG breakdown (p^T S p <= 0 or a non-positive Ritz value) at iteration %d", hsv.it);
+        return DE_EBREAKDOWN;
+    }
+    if (hsv.rr > hsv.tol2) {
+        set_error("PCG did not reach rtol in %d iterations (relres %.3e)", hsv.it, c->stats.relres_recursive);
+        return DE_ENOCONV;
+    }
+    return DE_OK;
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+
+static de_status_t need_device(const de_ctx_t* c) {
+    if (c->opt.host_only) {
+        set_error("context was created with host_only = 1");
+        return DE_ESTATE;
+    }
+    return DE_OK;
+}
+
+
+extern "C" {
+
+void de_default_options(de_options_t* o) {
+    if (!o) return;
+    memset(o, 0, sizeof(*o));
+    o->theta = 0.5;
+    o->lanczos_k = 10;
+    o->inner_mode = 1;
+    o->inner_tol = 1e-3;
+    o->inner_max_iter = 1000;
+    o->max_iter = 20000;
+    o->beta_variant = 0;
+    o->warm_start = 0;
+    o->rank = 0;
+    o->nranks = 1;
+    o->device = 0;
+    o->nccl_id = nullptr;
+    o->stream = nullptr;
+    o->check_every = 8;
+    o->use_graph = 1;
+}
+
+const char* de_last_error(void) { return g_err; }
+
+de_status_t de_setup(const de_mesh_t* mesh, const double* density, double E0, double Emin, double p, double nu,
+                     const de_partition_t* part, const de_options_t* opt, de_ctx_t** out) {
+    if (!out) {
+        set_error("null out pointer");
+        return DE_EINVAL;
+    }
+    *out = nullptr;
+    de_ctx* c = new (std::nothrow) de_ctx();
+    if (!c) return DE_ENOMEM;
+    de_status_t s;
+    try {
+        s = setup_impl(mesh, density, E0, Emin, p, nu, part, opt, c);
+    } catch (const std::bad_alloc&) {
+        set_error("host allocation failed");
+        s = DE_ENOMEM;
+    }
+    if (s != DE_OK) {
+        std::string keep = g_err;
+        de_destroy(c);
+        snprintf(g_err, sizeof(g_err), "%s", keep.c_str());
+        return s;
+    }
+    *out = c;
+    return DE_OK;
+}
+
+de_status_t de_update_densities(de_ctx_t* c, const double* density) {
+    if (!c || !density) {
+        set_error("null argument");
+        return DE_EINVAL;
+    }
+    for (int64_t e = 0; e < c->hs.nelem; ++e)
+        if (!(density[e] > 0.0) || !std::isfinite(density[e])) {
+            set_error("density[%lld] must be positive and finite", (long long)e);
+            return DE_EINVAL;
+        }
+    TRY(need_device(c));
+    DE_CUDA(cudaSetDevice(c->opt.device));
+    DE_CUDA(cudaMemcpyAsync(c->d_rho, density, sizeof(double) * c->hs.nelem, cudaMemcpyHostToDevice, c->st));
+    c->factored = false;
+    return DE_OK;
+}
+
+de_status_t de_update_densities_device(de_ctx_t* c, const double* d_density) {
+    if (!c || !d_density) {
+        set_error("null argument");
+        return DE_EINVAL;
+    }
+    TRY(need_device(c));
+    DE_CUDA(cudaSetDevice(c->opt.device));
+    DE_CUDA(cudaMemcpyAsync(c->d_rho, d_density, sizeof(double) * c->hs.nelem, cudaMemcpyDeviceToDevice, c->st));
+    c->factored = false;
+    return DE_OK;
+}
+
+de_status_t de_factor(de_ctx_t* c) {
+    if (!c) {
+        set_error("null context");
+        return DE_EINVAL;
+    }
+    TRY(need_device(c));
+    DE_CUDA(cudaSetDevice(c->opt.device));
+    return factor_impl(c);
+}
+
+de_status_t de_solve_device(de_ctx_t* c, const double* d_rhs, double rtol, double* d_u, int32_t* iterations,
+                            double* final_relres) {
+    if (!c || !d_rhs || !d_u) {
+        set_error("null argument");
+        return DE_EINVAL;
+    }
+    TRY(need_device(c));
+    DE_CUDA(cudaSetDevice(c->opt.device));
+    return solve_impl(c, d_rhs, rtol, d_u, iterations, final_relres);
+}
+
+de_status_t de_solve(de_ctx_t* c, const double* rhs, double rtol, double* u, int32_t* iterations,
+                     double* final_relres) {
+    if (!c || !rhs || !u) {
+        set_error("null argument");
+        return DE_EINVAL;
+    }
+    TRY(need_device(c));
+    DE_CUDA(cudaSetDevice(c->opt.device));
+    const size_t nb = sizeof(double) * size_t(c->hs.ndof);
+    DE_CUDA(cudaMemcpyAsync(c->d_fbuf, rhs, nb, cudaMemcpyHostToDevice, c->st));
+    de_status_t s = solve_impl(c, c->d_fbuf, rtol, c->d_ubuf, iterations, final_relres);
+    if (s != DE_OK && s != DE_ENOCONV) return s;
+    DE_CUDA(cudaMemcpyAsync(u, c->d_ubuf, nb, cudaMemcpyDeviceToHost, c->st));
+    DE_CUDA(cudaStreamSynchronize(c->st));
+    return s;
+}
+
+de_status_t de_get_dofmap(const de_ctx_t* c, int8_t* cls, int32_t* sub, int32_t* reduced, int64_t* n_I,
+                          int64_t* n_Gamma) {
+    if (!c) {
+        set_error("null context");
+        return DE_EINVAL;
+    }
+    const HostSetup& hs = c->hs;
+    if (cls) memcpy(cls, hs.cls.data(), hs.ndof);
+    if (sub) memcpy(sub, hs.dof_sub.data(), hs.ndof * sizeof(int32_t));
+    if (reduced) memcpy(reduced, hs.reduced.data(), hs.ndof * sizeof(int32_t));
+    if (n_I) *n_I = hs.n_I;
+    if (n_Gamma) *n_Gamma = hs.n_G;
+    return DE_OK;
+}
+
+de_status_t de_get_skeleton(const de_ctx_t* c, int32_t comp, int32_t* nodes, int32_t* face_of_node) {
+    if (!c || comp < 0 || comp >= c->hs.ncomp) {
+        set_error("bad component");
+        return DE_EINVAL;
+    }
+    const HostSetup& hs = c->hs;
+    for (int64_t f = hs.comp_off[comp]; f < hs.comp_off[comp + 1]; ++f) {
+        if (nodes) nodes[f - hs.comp_off[comp]] = hs.cnode[f];
+        if (face_of_node) face_of_node[f - hs.comp_off[comp]] = hs.face_of[f];
+    }
+    return DE_OK;
+}
+
+de_status_t de_get_stats(const de_ctx_t* c, de_stats_t* s) {
+    if (!c || !s) {
+        set_error("null argument");
+        return DE_EINVAL;
+    }
+    *s = c->stats;
+    return DE_OK;
+}
+
+de_status_t de_schur_apply_device(de_ctx_t* c, const double* d_p, double* d_q) {
+    if (!c || !d_p || !d_q) {
+        set_error("null argument");
+        return DE_EINVAL;
+    }
+    if (!c->factored) {
+        set_error("de_schur_apply_device before de_factor");
+        return DE_ESTATE;
+    }
+    TRY(need_device(c));
+    DE_CUDA(cudaSetDevice(c->opt.device));
+    TRY(schur_apply(c, d_p, d_q));
+    DE_CUDA(cudaStreamSynchronize(c->st));
+    return DE_OK;
+}
+
+de_status_t de_precond_apply_device(de_ctx_t* c, const double* d_r, double* d_z) {
+    if (!c || !d_r || !d_z) {
+        set_error("null argument");
+        return DE_EINVAL;
+    }
+    TRY(need_device(c));
+    DE_CUDA(cudaSetDevice(c->opt.device));
+    TRY(precond(c, d_r, d_z, nullptr, nullptr));
+    DE_CUDA(cudaStreamSynchronize(c->st));
+    if (c->have_prec) {
+        LzState lz[MAXC];
+        DE_CUDA(cudaMemcpy(lz, c->P.lz, sizeof(lz), cudaMemcpyDeviceToHost));
+        for (int cc = 0; cc < c->hs.ncomp; ++cc)
+            if (lz[cc].status == DE_EBREAKDOWN) {
+                set_error("non-positive Ritz value in component %d", cc);
+                return DE_EBREAKDOWN;
+            }
+    }
+    return DE_OK;
+}
+
+de_status_t de_get_factor_band(const de_ctx_t* c, int32_t sl, double* out, int32_t* n_I_s) {
+    if (!c || sl < 0 || sl >= c->nsl) {
+        set_error("bad local subdomain index");
+        return DE_EINVAL;
+    }
+    const SubDesc& d = c->hsd[sl];
+    if (n_I_s) *n_I_s = d.nI;
+    if (out) {
+        const int ld = c->hs.ld, w = c->hs.band + 1;
+        std::vector<double> tmp(size_t(d.nI) * ld);
+        DE_CUDA(cudaMemcpy(tmp.data(), c->d_band + d.band_off, tmp.size() * sizeof(double), cudaMemcpyDeviceToHost));
+        for (int j = 0; j < d.nI; ++j)
+            for (int k = 0; k < w; ++k) out[size_t(j) * w + k] = tmp[size_t(j) * ld + k];
+        if (c->factored)   // slot 0 holds 1/L_jj internally
+            for (int j = 0; j < d.nI; ++j) out[size_t(j) * w] = 1.0 / out[size_t(j) * w];
+    }
+    return DE_OK;
+}
+
+de_status_t de_get_assembled_band(de_ctx_t* c, int32_t sl, double* out, int32_t* n_I_s) {
+    if (!c || sl < 0 || sl >= c->nsl) {
+        set_error("bad local subdomain index");
+        return DE_EINVAL;
+    }
+    TRY(need_device(c));
+    DE_CUDA(cudaSetDevice(c->opt.device));
+    const HostSetup& hs = c->hs;
+    launch_simp(c->d_rho, c->d_Ee, hs.nelem, c->E0, c->Emin, c->p, c->st);
+    launch_assemble_band(c->md, c->d_sd, c->nsl, c->d_idofs, c->d_Ee, c->d_band, hs.ld, hs.band, c->max_nI, c->st);
+    TRY(check_launch());
+    DE_CUDA(cudaStreamSynchronize(c->st));
+    c->factored = false;   // the band now holds A_II, not its factor
+    return de_get_factor_band(c, sl, out, n_I_s);
+}
+
+de_status_t de_nccl_unique_id(void* out128) {
+    if (!out128) {
+        set_error("null argument");
+        return DE_EINVAL;
+    }
+    if (!nccl().ok) {
+        set_error("libnccl.so.2 could not be loaded");
+        return DE_ENCCL;
+    }
+    NcclId id;
+    int r = nccl().get_id(&id);
+    if (r != 0) {
+        set_error("ncclGetUniqueId failed");
+        return DE_ENCCL;
+    }
+    memcpy(out128, id.internal, 128);
+    return DE_OK;
+}
+
+de_status_t de_set_profiling(de_ctx_t* c, int32_t on) {
+    if (!c) {
+        set_error("null context");
+        return DE_EINVAL;
+    }
+    c->profiling = on != 0;
+    c->prof_ms = 0.0;
+    c->prof_n = 0;
+    return DE_OK;
+}
+
+de_status_t de_get_kernel_time(const de_ctx_t* c, double* ms, int64_t* launches) {
+    if (!c) {
+        set_error("null context");
+        return DE_EINVAL;
+    }
+    if (ms) *ms = c->prof_n ? c->prof_ms / double(c->prof_n) : 0.0;
+    if (launches) *launches = c->prof_n;
+    return DE_OK;
+}
+
+void de_destroy(de_ctx_t* c) {
+    if (!c) return;
+    if (c->opt.host_only && c->allocs.empty()) {
+        delete c;
+        return;
+    }
+    cudaSetDevice(c->opt.device);
+    if (c->st) cudaStreamSynchronize(c->st);
+    if (c->gexec) cudaGraphExecDestroy(c->gexec);
+    for (auto e : c->ev)
+        if (e) cudaEventDestroy(e);
+    if (c->comm && nccl().destroy) nccl().destroy(c->comm);
+    for (void* p : c->allocs) cudaFree(p);
+    if (c->own_stream && c->st) cudaStreamDestroy(c->st);
+    delete c;
+}
+
+}  // extern "C"

@@ -1,0 +1,260 @@
+// de_internal.h — internal structures of libde (B200-native interface PCG).
+// Host setup (topology, trace matrices, preconditioner structures) is plain C++;
+// all numerics of the hot path run in the sm_100a kernels declared at the bottom.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+#include <cuda_runtime.h>
+
+#include "../../include/de.h"
+
+namespace de {
+
+constexpr int KMAX = 16;            // max inverse-Lanczos basis size supported on device
+constexpr int MAXC = 3;             // max displacement components
+
+void set_error(const char* fmt, ...);
+
+#define DE_CUDA(call)                                                                   \
+    do {                                                                                \
+        cudaError_t e_ = (call);                                                        \
+        if (e_ != cudaSuccess) {                                                        \
+            ::de::set_error("CUDA error %s at %s:%d: %s", cudaGetErrorName(e_), __FILE__, \
+                            __LINE__, cudaGetErrorString(e_));                          \
+            return DE_ECUDA;                                                            \
+        }                                                                               \
+    } while (0)
+
+// ------------------------------------------------------------------------ host setup
+
+// Sparse matrix in CSR with int32 indices (host side).
+struct HCsr {
+    int32_t n = 0, m = 0;
+    std::vector<int32_t> ptr, col;
+    std::vector<double> val;
+};
+
+// Exact-elimination structure of one skeleton operator X (X = K_c or M_c), all components
+// flattened (R10): faces F (cross points removed), cross points C,
+//   x_C = S_C^-1 (b_C - X_CF X_FF^-1 b_F),  x_F = X_FF^-1 (b_F - X_FC x_C),
+//   S_C = X_CC - X_CF X_FF^-1 X_FC  (dense, per component, inverted on the GPU).
+struct HElim {
+    int32_t nfaces = 0;
+    std::vector<int32_t> face_off;      // [nfaces+1] into face_nodes
+    std::vector<int32_t> face_nodes;    // flattened skeleton index of each face node
+    std::vector<int32_t> face_band;     // half bandwidth of X_FF in face order
+    std::vector<int64_t> face_fac_off;  // offset of each face factor (column band, ld = band+1)
+    std::vector<double> face_fac;       // band Cholesky factors, slot 0 holds 1/L_jj
+    int32_t ncross = 0;
+    int32_t cross_comp_off[MAXC + 1] = {0, 0, 0, 0};
+    std::vector<int32_t> cross_flat;    // flattened skeleton index of each cross point
+    HCsr XCF;                           // rows: cross points; cols: flattened skeleton index (face nodes)
+    HCsr XFC;                           // rows: face-node slots (face_nodes order); cols: cross index
+    std::vector<int64_t> sc_off;        // [ncomp+1] offsets of dense S_C per component
+    std::vector<double> SC;             // dense S_C (row-major per component), inverted on device
+};
+
+struct HostSetup {
+    // mesh / partition
+    int dim = 2;
+    int nel[3] = {1, 1, 1}, nn[3] = {2, 2, 1}, sub[3] = {1, 1, 1}, ps[3] = {1, 1, 1};
+    int64_t nnodes = 0, ndof = 0, nelem = 0;
+    int32_t nsub = 0;
+    double h = 1.0;
+    // dof map (bit-exact contract, R4/R5)
+    std::vector<int8_t> cls;          // 0 I, 1 Gamma, 2 D
+    std::vector<int32_t> dof_sub;     // owning subdomain of interior dofs, -1 otherwise
+    std::vector<int32_t> reduced;     // canonical index or -1
+    std::vector<int32_t> gpos;        // Gamma index of a dof or -1
+    std::vector<int32_t> lidx;        // local interior index of an interior dof
+    std::vector<int32_t> gamma_dofs;  // ascending
+    int64_t n_I = 0, n_G = 0, n_free = 0;
+    std::vector<int32_t> node_nsub;   // distinct subdomains per node
+    std::vector<int32_t> node_subs;   // up to 8 subdomain ids per node (sorted), -1 padded
+    // per subdomain
+    std::vector<int64_t> ioff;        // offset into idofs (canonical interior start)
+    std::vector<int32_t> nI;
+    std::vector<int32_t> idofs;       // interior dofs, concatenated by subdomain
+    std::vector<int64_t> goff;
+    std::vector<int32_t> nGs;
+    std::vector<int32_t> gdofs;       // Gamma dofs touched by each subdomain, concatenated
+    std::vector<int32_t> band_s;      // per-subdomain half bandwidth
+    int32_t band = 0, ld = 0;
+    // component skeletons (flattened)
+    int ncomp = 0;
+    int64_t comp_off[MAXC + 1] = {0, 0, 0, 0};
+    std::vector<int32_t> cmap;        // flat -> Gamma index
+    std::vector<int32_t> cnode;       // flat -> node id
+    std::vector<int32_t> face_of;     // flat -> face id within component, -1 cross
+    int64_t n_faces_c[MAXC] = {0, 0, 0}, n_cross_c[MAXC] = {0, 0, 0};
+    int singular_mask = 0;
+    HCsr M, L, K;                     // block diagonal over components (flattened)
+    HElim elimK, elimM;
+    double KE0[24 * 24];              // unit-E element stiffness, local order lexicographic
+    int nke = 8;
+};
+
+// Build everything density-independent. Returns DE_OK or DE_EINVAL with the error set.
+de_status_t host_setup(const de_mesh_t* mesh, const de_partition_t* part, double nu,
+                       HostSetup& hs);
+
+// Per-subdomain ring structures (A_IG rows over interior, A_GG/A_GI rows over Gamma).
+struct HRing {
+    std::vector<int32_t> igp;               // per local subdomain: nI+1 row pointers (absolute)
+    std::vector<int32_t> ig_col;            // local Gamma column
+    std::vector<int32_t> ig_da, ig_db;      // dof pair (row dof, col dof)
+    std::vector<int32_t> gxp;               // per local subdomain: nG+1 row pointers (absolute)
+    std::vector<int32_t> gx_col;            // >= 0 local Gamma col; < 0: -(interior local)-1
+    std::vector<int32_t> gx_da, gx_db;
+    std::vector<int64_t> igp_off, gxp_off;  // per local subdomain offsets into igp / gxp
+};
+void build_ring(const HostSetup& hs, const std::vector<int32_t>& owned, HRing& ring);
+
+// ------------------------------------------------------------------------ device side
+
+struct SubDesc {          // one owned subdomain
+    int32_t gid;          // global subdomain id
+    int32_t nI;
+    int32_t nG;
+    int32_t pad;
+    int64_t ioff;         // offset into d_idofs / scratch (local concatenation)
+    int64_t band_off;     // offset (doubles) into the factor band
+    int64_t goff;         // offset into d_Rg / qloc
+    int64_t igp_off;      // offset into d_igp (nI+1 entries)
+    int64_t gxp_off;      // offset into d_gxp (nG+1 entries)
+};
+
+struct MeshDev {
+    int dim;
+    int nel[3];
+    int nn[3];
+    int sub[3];
+    int ps[3];
+    int nke;
+};
+
+struct PcgState {
+    double rz, pq, alpha, beta, rr, tol2, rz_old;
+    int32_t it, done, status, maxit;
+};
+
+struct ElimDev {
+    int32_t nfaces, ncross, ncomp, maxface;
+    int32_t *face_off, *face_nodes, *face_band;
+    int64_t* face_fac_off;
+    double* face_fac;
+    int32_t* cross_flat;
+    int32_t cross_comp_off[MAXC + 1];
+    int32_t *xcf_ptr, *xcf_col;
+    double* xcf_val;
+    int32_t *xfc_ptr, *xfc_col;
+    double* xfc_val;
+    int64_t sc_off[MAXC + 1];
+    double* Sinv;
+};
+
+struct CsrDev {
+    int32_t n;
+    int32_t *ptr, *col;
+    double* val;
+};
+
+struct LzState {                    // per component inverse-Lanczos bookkeeping
+    int32_t active, kc, broke, status;
+    double nb2, na2, nrm2, rr;
+    double h[KMAX];
+    double A[KMAX * KMAX], B[KMAX * KMAX];
+    double wr[KMAX];
+    double coef[KMAX];
+    double theta_ritz[KMAX];
+};
+
+// kernel launchers (implemented in *.cu); all asynchronous on `st`
+void launch_simp(const double* rho, double* Ee, int64_t nelem, double E0, double Emin, double p,
+                 cudaStream_t st);
+void upload_KE0(const double* ke, int nke, cudaStream_t st);
+void launch_assemble_band(const MeshDev& m, const SubDesc* sd, int nsl, const int32_t* idofs,
+                          const double* Ee, double* band, int ld, int band_w, int max_nI,
+                          cudaStream_t st);
+void launch_assemble_pairs(const MeshDev& m, const int32_t* da, const int32_t* db,
+                           const int32_t* sub_of_entry, const double* Ee, double* val, int64_t n,
+                           cudaStream_t st);
+int launch_band_cholesky(const SubDesc* sd, int nsl, double* band, int ld, int band_w,
+                         int* d_fail, cudaStream_t st);
+void launch_apply_K(const MeshDev& m, const double* Ee, const double* u, const double* f,
+                    const int8_t* cls, double* res, int64_t ndof, cudaStream_t st);
+
+enum SchurMode { SCHUR_APPLY = 0, SCHUR_CONDENSE = 1, SCHUR_BACKSUB = 2 };
+struct SchurArgs {
+    const SubDesc* sd;
+    int nsl;
+    const double* band;
+    int ld, band_w;
+    const int32_t* idofs;
+    const int32_t* Rg;
+    const int32_t* igp;
+    const int32_t* ig_col;
+    const double* ig_val;
+    const int32_t* gxp;
+    const int32_t* gx_col;
+    const double* gx_val;
+    double* scratch;
+    const double* xin;      // interface vector (n_Gamma) gathered through Rg
+    const double* f;        // full rhs (ndof) for condense/backsub
+    double* qloc;           // per-subdomain local outputs
+    double* u;              // full solution (backsub)
+    const PcgState* state;  // early exit when state->done (may be null)
+    int mode;
+    int maxG;
+};
+int launch_schur_local(const SchurArgs& a, cudaStream_t st);
+
+void launch_gather(const int32_t* gptr, const int32_t* gsrc, const double* qloc,
+                   const double* add, double* q, int64_t nG, const PcgState* st_done,
+                   cudaStream_t st);
+// PCG building blocks (deterministic two-level reductions, device-side scalars)
+struct RedBuf {
+    double* part;
+    unsigned int* counter;
+    int nblk;
+};
+void launch_pcg_pq(const double* p, const double* q, int64_t n, RedBuf rb, PcgState* s,
+                   cudaStream_t st);
+void launch_pcg_update_xr(double* x, double* r, double* r_old, const double* p, const double* q,
+                          int64_t n, RedBuf rb, PcgState* s, cudaStream_t st);
+void launch_pcg_rz(const double* r, const double* z, const double* r_old, int64_t n, int beta_pr,
+                   RedBuf rb, PcgState* s, cudaStream_t st);
+void launch_pcg_update_p(double* p, const double* z, int64_t n, PcgState* s, cudaStream_t st);
+void launch_pcg_init(double* r, double* p, const double* z, const double* g, const double* Sx,
+                     int64_t n, int mode, RedBuf rb, PcgState* s, cudaStream_t st);
+void launch_norm2(const double* v, int64_t n, RedBuf rb, double* out, cudaStream_t st);
+void launch_copy(double* dst, const double* src, int64_t n, const PcgState* s, cudaStream_t st);
+void launch_scatter_gamma(const int32_t* gamma_dofs, const double* uG, double* u, int64_t nG,
+                          cudaStream_t st);
+void launch_gather_gamma(const int32_t* gamma_dofs, const double* f, double* fG, int64_t nG,
+                         cudaStream_t st);
+void launch_zero_dirichlet(const int8_t* cls, double* u, int64_t ndof, cudaStream_t st);
+
+// preconditioner
+struct PrecDev {
+    int32_t ncomp, nflat, kmax;
+    int64_t comp_off[MAXC + 1];
+    int32_t singular[MAXC];
+    double theta;
+    int32_t* cmap;
+    CsrDev M, L, K;
+    ElimDev eK, eM;
+    double *rf, *s, *v, *w, *Mw, *y, *zf, *W, *LW, *MW;
+    LzState* lz;
+    double* part;
+    unsigned int* counter;
+    int nblk;
+};
+void prec_apply(const PrecDev& P, const double* r, double* z, const PcgState* s, cudaStream_t st,
+                int* nlaunch);
+void launch_gauss_jordan(double* A, double* Bbuf, int n, cudaStream_t st);
+void prec_prepare(const PrecDev& P);   // one-time kernel attributes (outside graph capture)
+
+}  // namespace de
