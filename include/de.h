@@ -95,7 +95,7 @@ typedef struct {
     int64_t ndof, n_free, n_I, n_Gamma, n_sub, n_sub_local;
     int32_t band;            /* uniform half bandwidth of the interior factors */
     int32_t iterations;      /* outer PCG iterations of the last solve */
-    int32_t restarts;        /* residual-replacement restarts of the last solve */
+    int32_t restarts;        /* iterative-refinement rounds of the last solve (R11) */
     double relres_recursive; /* ||r_Gamma|| / ||f_free|| at exit (recursive residual) */
     double relres_true;      /* ||f - K u||_2 / ||f||_2 over free dofs (matrix-free K) */
     double ms_factor;        /* de_factor: SIMP assembly + band Cholesky */
@@ -109,6 +109,11 @@ typedef struct {
     int64_t n_cross[3];      /* cross points / wirebasket nodes per component */
     int64_t n_faces[3];
     int64_t n_gamma_c[3];
+    double bytes_schur;      /* algorithmic bytes of one Schur-apply launch: one pass over the local
+                                factor band + ring blocks A_IG/A_GG + local interface vectors */
+    int64_t kernels_launched; /* kernels launched by the last de_solve (graph nodes included) */
+    int32_t iterations_pass1; /* PCG iterations before iterative refinement */
+    int32_t pad_;
 } de_stats_t;
 
 /* Fill *opt with defaults (theta 0.5, k 10, inner_mode 1, max_iter 20000, FR, 1 rank). */

@@ -12,7 +12,9 @@ from dataclasses import dataclass, field
 import numpy as np
 import scipy.sparse.linalg as spla
 
-from .fem import free_system, true_relres
+from dataclasses import replace
+
+from .fem import free_system, true_relres, apply_K
 from .topology import build_topology
 from .dd import subdomain_blocks, factor_subdomains, schur_apply, condensed_rhs, back_substitute
 from .precond import build_components, apply_precond
@@ -35,6 +37,7 @@ class DDResult:
     relres: float
     uG: np.ndarray
     history: list = field(default_factory=list)
+    its_pass1: int = 0
 
 
 class DDOracle:
@@ -59,7 +62,18 @@ class DDOracle:
     def P(self, r):
         return apply_precond(self.comps, r, self.mode, self.theta, self.k, self.inner)
 
-    def solve(self, rtol=None, maxit=20000, warm=False):
+    def _dd_solve(self, rhs, tol_abs, maxit, x0):
+        """One pass of Eq. (7) for the load vector `rhs`."""
+        prob = replace(self.prob, rhs=rhs)
+        g = condensed_rhs(prob, self.topo, self.blocks)
+        uG, its, conv, hist = pcg(self.S, g, self.P, tol_abs, maxit, x0=x0, beta=self.beta)
+        return back_substitute(prob, self.topo, self.blocks, uG), its, conv, hist
+
+    def solve(self, rtol=None, maxit=20000, warm=False, max_refine=3):
+        """Interface PCG to ||r_Gamma|| <= rtol ||f_free|| (recursive residual), then iterative
+        refinement on the full system while the true ||f - K u|| > rtol ||f|| (R11):
+        u += DD-solve(f - K u) with the interface tolerance 0.5 rtol ||f||, at most max_refine times,
+        and only while each round at least halves the residual."""
         prob = self.prob
         rtol = prob.rtol if rtol is None else rtol
         if self.blocks is None:
@@ -68,9 +82,22 @@ class DDOracle:
         nf = np.linalg.norm(prob.rhs[free])
         if nf == 0:
             return DDResult(np.zeros(prob.ndof), 0, True, 0.0, np.zeros(self.topo.n_G))
-        g = condensed_rhs(prob, self.topo, self.blocks)
         x0 = self.uG_prev if (warm and self.uG_prev is not None) else None
-        uG, its, conv, hist = pcg(self.S, g, self.P, rtol * nf, maxit, x0=x0, beta=self.beta)
+        u, its, conv, hist = self._dd_solve(prob.rhs, rtol * nf, maxit, x0)
+        its1 = its
+        relres = true_relres(prob, u)
+        prev = np.inf
+        for _ in range(max_refine):
+            # stop when converged, or when a round no longer halves the residual (FP64 floor)
+            if relres <= rtol or not conv or its >= maxit or not relres < 0.5 * prev:
+                break
+            prev = relres
+            res = np.where(free, prob.rhs - apply_K(prob, u), 0.0)
+            du, k, conv, h2 = self._dd_solve(res, 0.5 * rtol * nf, maxit - its, None)
+            u = u + du
+            its += k
+            hist += h2
+            relres = true_relres(prob, u)
+        uG = u[self.topo.gamma_dofs]
         self.uG_prev = uG
-        u = back_substitute(prob, self.topo, self.blocks, uG)
-        return DDResult(u, its, conv, true_relres(prob, u), uG, hist)
+        return DDResult(u, its, conv and relres <= rtol, relres, uG, hist, its1)

@@ -49,7 +49,9 @@ class de_stats_t(C.Structure):
                 ("ms_pcg", C.c_double), ("ms_schur", C.c_double), ("bytes_factor", C.c_double),
                 ("bytes_iter", C.c_double), ("launches_per_iter", C.c_int32),
                 ("singular_components", C.c_int32), ("n_cross", C.c_int64 * 3), ("n_faces", C.c_int64 * 3),
-                ("n_gamma_c", C.c_int64 * 3)]
+                ("n_gamma_c", C.c_int64 * 3),
+                ("bytes_schur", C.c_double), ("kernels_launched", C.c_int64),
+                ("iterations_pass1", C.c_int32), ("pad_", C.c_int32)]
 
 
 _lib = None

@@ -111,6 +111,8 @@ struct de_ctx {
     std::vector<cudaEvent_t> ev;
     double prof_ms = 0.0;
     int64_t prof_n = 0;
+    int64_t launches = 0;
+    double* d_ubuf2 = nullptr;
     // nccl
     void* comm = nullptr;
     de_stats_t stats{};
@@ -273,9 +275,11 @@ de_status_t run_loop(de_ctx* c, PcgState& hsv) {
         const int it_before = hsv.it;
         if (use_graph) {
             DE_CUDA(cudaGraphLaunch(c->gexec, c->st));
+            c->launches += int64_t(c->launches_per_iter) * c->graph_iters;
         } else {
             const int ni = std::max(1, c->opt.check_every);
             for (int i = 0; i < ni; ++i) TRY(pcg_iteration(c, &c->launches_per_iter, nullptr, nullptr));
+            c->launches += int64_t(c->launches_per_iter) * ni;
         }
         TRY(read_state(c, &hsv));
         if (use_graph && c->graph_prof) {
@@ -338,10 +342,13 @@ de_status_t upload_prec(de_ctx* c) {
             mf = std::max(mf, n);
             mfac = std::max(mfac, int(E.face_fac_off[F + 1] - E.face_fac_off[F]));
         }
-        if (mf > 0xffff || mfac > 0x7fff) {
-            set_error("interface face too large for the face-solve kernel");
+        int maxb = 0;
+        for (int F = 0; F < E.nfaces; ++F) maxb = std::max(maxb, E.face_band[F]);
+        if (mf > 256 || maxb > 31) {
+            set_error("interface face too large for the face-solve kernel (nodes %d > 256 or band %d > 31)", mf, maxb);
             return DE_EINVAL;
         }
+        mfac = std::min(mfac, 0x7fff);
         D.maxface = (mfac << 16) | mf;
         TRY(dupload(c, &D.face_off, E.face_off));
         TRY(dupload(c, &D.face_nodes, E.face_nodes));
@@ -382,8 +389,8 @@ de_status_t upload_prec(de_ctx* c) {
     DE_CUDA(cudaMemsetAsync(P.lz, 0, MAXC * sizeof(LzState), c->st));
     int64_t maxc = 1;
     for (int cc = 0; cc < hs.ncomp; ++cc) maxc = std::max(maxc, hs.comp_off[cc + 1] - hs.comp_off[cc]);
-    P.nblk = int(std::max<int64_t>(1, std::min<int64_t>(64, (maxc + 4095) / 4096)));
-    const int nslots = 8 + MAXC * KMAX + MAXC * (KMAX * (KMAX + 1) + KMAX);
+    P.nblk = int(std::max<int64_t>(1, std::min<int64_t>(256, (maxc + 1023) / 1024)));
+    const int nslots = 8 + MAXC * KMAX + MAXC * KMAX * (2 * KMAX + 1);
     TRY(dalloc(c, &P.part, size_t(nslots) * P.nblk));
     TRY(dalloc(c, &P.counter, size_t(nslots)));
     DE_CUDA(cudaMemsetAsync(P.counter, 0, size_t(nslots) * sizeof(unsigned int), c->st));
@@ -470,7 +477,7 @@ de_status_t setup_impl(const de_mesh_t* mesh, const double* density, double E0, 
         d.nI = hs.nI[s];
         d.nG = hs.nGs[s];
         d.ioff = ioff;
-        d.band_off = ioff * hs.ld;
+        d.band_off = 2 * ioff * hs.ld;   // [L | M] per subdomain
         d.goff = goff;
         d.igp_off = ring.igp_off[k];
         d.gxp_off = ring.gxp_off[k];
@@ -528,7 +535,7 @@ de_status_t setup_impl(const de_mesh_t* mesh, const double* density, double E0, 
     c->n_gx = int64_t(ring.gx_col.size());
     TRY(dalloc(c, &c->d_ig_val, size_t(c->n_ig)));
     TRY(dalloc(c, &c->d_gx_val, size_t(c->n_gx)));
-    TRY(dalloc(c, &c->d_band, size_t(c->n_local_I) * hs.ld));
+    TRY(dalloc(c, &c->d_band, 2 * size_t(c->n_local_I) * hs.ld));
     TRY(dalloc(c, &c->d_scratch, size_t(c->n_local_I) + 32));
     TRY(dalloc(c, &c->d_qloc, size_t(c->n_local_G) + 32));
     TRY(dupload(c, &c->d_gptr, gcnt));
@@ -542,6 +549,7 @@ de_status_t setup_impl(const de_mesh_t* mesh, const double* density, double E0, 
     TRY(dalloc(c, &c->d_res, nd));
     TRY(dalloc(c, &c->d_ubuf, nd));
     TRY(dalloc(c, &c->d_fbuf, nd));
+    TRY(dalloc(c, &c->d_ubuf2, nd));
     TRY(dalloc(c, &c->d_state, 1));
     TRY(dalloc(c, &c->d_scal, 8));
     TRY(dalloc(c, &c->d_fail, 1));
@@ -590,6 +598,8 @@ de_status_t setup_impl(const de_mesh_t* mesh, const double* density, double E0, 
     double fb = 0.0;
     for (const auto& d : c->hsd) fb += double(d.nI) * (hs.band + 1) * 8.0;
     S.bytes_factor = fb;
+    S.bytes_schur = fb + double(c->n_ig + c->n_gx) * 12.0 + double(c->n_local_G) * (8.0 * 3 + 4.0) +
+                    double(c->n_local_I + c->nsl) * 4.0;
     S.bytes_iter = fb + double(c->n_ig + c->n_gx) * 12.0 + double(c->n_local_G) * 8.0 * 3.0 +
                    double(hs.n_G) * 8.0 * 11.0;
     return DE_OK;
@@ -630,6 +640,58 @@ de_status_t factor_impl(de_ctx* c) {
     return DE_OK;
 }
 
+// One pass of Eq. (7) for load vector d_rhs: condense, interface PCG to the
+// absolute recursive tolerance tol_abs (x0 = previous u_Gamma when warm), back-substitute into d_out.
+de_status_t dd_pass(de_ctx* c, const double* d_rhs, double tol_abs, bool warm, int maxit, double* d_out,
+                    PcgState& hsv) {
+    const int64_t nG = c->hs.n_G;
+    launch_gather_gamma(c->d_gamma_dofs, d_rhs, c->d_fG, nG, c->st);
+    launch_schur_local(schur_args(c, SCHUR_CONDENSE, nullptr, d_rhs, nullptr, nullptr), c->st);
+    launch_gather(c->d_gptr, c->d_gsrc, c->d_qloc, c->rank == 0 ? c->d_fG : nullptr, c->d_g, nG, nullptr, c->st);
+    c->launches += 3;
+    TRY(check_launch());
+    TRY(allreduce(c, c->d_g, size_t(nG)));
+    hsv = PcgState{};
+    hsv.tol2 = tol_abs * tol_abs;
+    hsv.maxit = maxit;
+    DE_CUDA(cudaMemcpyAsync(c->d_state, &hsv, sizeof(PcgState), cudaMemcpyHostToDevice, c->st));
+    if (warm) {
+        launch_copy(c->d_x, c->d_xprev, nG, nullptr, c->st);
+        TRY(schur_apply(c, c->d_x, c->d_q));
+        launch_pcg_init(c->d_r, c->d_p, c->d_z, c->d_g, c->d_q, nG, 1, c->rb, c->d_state, c->st);
+        c->launches += 4;
+    } else {
+        DE_CUDA(cudaMemsetAsync(c->d_x, 0, sizeof(double) * nG, c->st));
+        launch_pcg_init(c->d_r, c->d_p, c->d_z, c->d_g, nullptr, nG, 0, c->rb, c->d_state, c->st);
+        c->launches += 1;
+    }
+    int np = 0;
+    TRY(precond(c, c->d_r, c->d_z, c->d_state, &np));
+    launch_pcg_init(c->d_r, c->d_p, c->d_z, c->d_g, nullptr, nG, 2, c->rb, c->d_state, c->st);
+    c->launches += np + 1;
+    TRY(check_launch());
+    TRY(read_state(c, &hsv));
+    if (!hsv.done && maxit > 0) TRY(run_loop(c, hsv));
+    // back-substitution u_I = A_II^-1 (rhs_I - A_IG u_G); u_G = x; u_D = 0
+    DE_CUDA(cudaMemsetAsync(d_out, 0, sizeof(double) * c->hs.ndof, c->st));
+    if (c->rank == 0) launch_scatter_gamma(c->d_gamma_dofs, c->d_x, d_out, nG, c->st);
+    launch_schur_local(schur_args(c, SCHUR_BACKSUB, c->d_x, d_rhs, d_out, nullptr), c->st);
+    c->launches += 2;
+    TRY(check_launch());
+    return allreduce(c, d_out, size_t(c->hs.ndof));
+}
+
+// res = f - K u (free dofs), returns ||res||^2 on the host
+de_status_t true_residual(de_ctx* c, const double* d_f, const double* d_u, double* r2) {
+    launch_apply_K(c->md, c->d_Ee, d_u, d_f, c->d_cls, c->d_res, c->hs.ndof, c->st);
+    launch_norm2(c->d_res, c->hs.ndof, c->rb, c->d_scal, c->st);
+    c->launches += 2;
+    TRY(check_launch());
+    DE_CUDA(cudaMemcpyAsync(r2, c->d_scal, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    DE_CUDA(cudaStreamSynchronize(c->st));
+    return DE_OK;
+}
+
 de_status_t solve_impl(de_ctx* c, const double* d_f, double rtol, double* d_u, int32_t* iters, double* relres) {
     if (!c->factored) {
         set_error("de_solve called before a successful de_factor");
@@ -640,101 +702,77 @@ de_status_t solve_impl(de_ctx* c, const double* d_f, double rtol, double* d_u, i
         return DE_EINVAL;
     }
     HostSetup& hs = c->hs;
-    const int64_t nG = hs.n_G;
     auto t0 = std::chrono::steady_clock::now();
+    c->launches = 0;
     double f2 = 0.0;
     TRY(masked_norm2(c, d_f, &f2));
+    c->launches += 3;
     const double fnorm = std::sqrt(f2);
-    DE_CUDA(cudaMemsetAsync(d_u, 0, sizeof(double) * hs.ndof, c->st));
     c->stats.iterations = 0;
     c->stats.restarts = 0;
     if (fnorm == 0.0) {
+        DE_CUDA(cudaMemsetAsync(d_u, 0, sizeof(double) * hs.ndof, c->st));
         DE_CUDA(cudaStreamSynchronize(c->st));
         if (iters) *iters = 0;
         if (relres) *relres = 0.0;
         c->stats.relres_true = c->stats.relres_recursive = 0.0;
         return DE_OK;
     }
-    // condensed rhs g = f_G - sum_s R_s^T A_GI,s A_II,s^-1 f_I,s
-    launch_gather_gamma(c->d_gamma_dofs, d_f, c->d_fG, nG, c->st);
-    launch_schur_local(schur_args(c, SCHUR_CONDENSE, nullptr, d_f, nullptr, nullptr), c->st);
-    launch_gather(c->d_gptr, c->d_gsrc, c->d_qloc, c->rank == 0 ? c->d_fG : nullptr, c->d_g, nG, nullptr, c->st);
-    TRY(check_launch());
-    TRY(allreduce(c, c->d_g, size_t(nG)));
-    PcgState hsv{};
-    hsv.tol2 = (rtol * fnorm) * (rtol * fnorm);
-    hsv.maxit = c->opt.max_iter > 0 ? c->opt.max_iter : 20000;
-    DE_CUDA(cudaMemcpyAsync(c->d_state, &hsv, sizeof(PcgState), cudaMemcpyHostToDevice, c->st));
-    const bool warm = c->opt.warm_start && c->have_prev;
+    const int maxit = c->opt.max_iter > 0 ? c->opt.max_iter : 20000;
     cudaEvent_t l0, l1;
     DE_CUDA(cudaEventCreate(&l0));
     DE_CUDA(cudaEventCreate(&l1));
     DE_CUDA(cudaEventRecord(l0, c->st));
-    if (warm) {
-        launch_copy(c->d_x, c->d_xprev, nG, nullptr, c->st);
-        TRY(schur_apply(c, c->d_x, c->d_q));
-        launch_pcg_init(c->d_r, c->d_p, c->d_z, c->d_g, c->d_q, nG, 1, c->rb, c->d_state, c->st);
-    } else {
-        DE_CUDA(cudaMemsetAsync(c->d_x, 0, sizeof(double) * nG, c->st));
-        launch_pcg_init(c->d_r, c->d_p, c->d_z, c->d_g, nullptr, nG, 0, c->rb, c->d_state, c->st);
-    }
-    int restarts = 0;
-    while (true) {
-        TRY(precond(c, c->d_r, c->d_z, c->d_state, nullptr));
-        launch_pcg_init(c->d_r, c->d_p, c->d_z, c->d_g, nullptr, nG, 2, c->rb, c->d_state, c->st);
-        TRY(check_launch());
-        TRY(read_state(c, &hsv));
-        if (!hsv.done) TRY(run_loop(c, hsv));
-        if (hsv.status == DE_EBREAKDOWN) break;
-        // residual replacement (R11): recompute r = g - S x and continue if needed
-        TRY(schur_apply(c, c->d_x, c->d_q));
-        const int it_keep = hsv.it;
-        launch_pcg_init(c->d_r, c->d_p, c->d_z, c->d_g, c->d_q, nG, 1, c->rb, c->d_state, c->st);
-        TRY(check_launch());
-        TRY(read_state(c, &hsv));
-        if (hsv.done || hsv.it >= hsv.maxit || restarts >= 5) {
-            hsv.it = it_keep;
-            break;
-        }
-        ++restarts;
-        hsv.status = 0;
-        DE_CUDA(cudaMemcpyAsync(c->d_state, &hsv, sizeof(PcgState), cudaMemcpyHostToDevice, c->st));
+    PcgState hsv{};
+    TRY(dd_pass(c, d_f, rtol * fnorm, c->opt.warm_start && c->have_prev, maxit, d_u, hsv));
+    int its = hsv.it, status = hsv.status, refines = 0;
+    c->stats.iterations_pass1 = hsv.it;
+    bool conv = hsv.rr <= hsv.tol2;
+    double rec = std::sqrt(std::max(hsv.rr, 0.0)) / fnorm;
+    double r2 = 0.0;
+    TRY(true_residual(c, d_f, d_u, &r2));
+    // iterative refinement on the full system (R11): u += DD(f - K u)
+    // stop refining when a round no longer halves the residual (the FP64 floor, R11)
+    double r2_prev = HUGE_VAL;
+    while (std::sqrt(r2) > rtol * fnorm && conv && status != DE_EBREAKDOWN && its < maxit && refines < 3 &&
+           r2 < 0.25 * r2_prev) {
+        r2_prev = r2;
+        TRY(dd_pass(c, c->d_res, 0.5 * rtol * fnorm, false, maxit - its, c->d_ubuf2, hsv));
+        launch_axpy(d_u, c->d_ubuf2, 1.0, hs.ndof, c->st);
+        c->launches += 1;
+        its += hsv.it;
+        status = hsv.status;
+        conv = hsv.rr <= hsv.tol2;
+        ++refines;
+        TRY(true_residual(c, d_f, d_u, &r2));
     }
     DE_CUDA(cudaEventRecord(l1, c->st));
-    // back-substitution u_I = A_II^-1 (f_I - A_IG u_G); u_G = x; u_D = 0
-    if (c->rank == 0) launch_scatter_gamma(c->d_gamma_dofs, c->d_x, d_u, nG, c->st);
-    launch_schur_local(schur_args(c, SCHUR_BACKSUB, c->d_x, d_f, d_u, nullptr), c->st);
-    TRY(check_launch());
-    TRY(allreduce(c, d_u, size_t(hs.ndof)));
-    launch_copy(c->d_xprev, c->d_x, nG, nullptr, c->st);
+    launch_gather_gamma(c->d_gamma_dofs, d_u, c->d_xprev, hs.n_G, c->st);   // warm start for the next solve
+    c->launches += 1;
     c->have_prev = true;
-    // true residual ||f - K u|| / ||f|| over free dofs (matrix-free)
-    launch_apply_K(c->md, c->d_Ee, d_u, d_f, c->d_cls, c->d_res, hs.ndof, c->st);
-    launch_norm2(c->d_res, hs.ndof, c->rb, c->d_scal, c->st);
-    TRY(check_launch());
-    double r2 = 0.0;
-    DE_CUDA(cudaMemcpyAsync(&r2, c->d_scal, sizeof(double), cudaMemcpyDeviceToHost, c->st));
     DE_CUDA(cudaStreamSynchronize(c->st));
     float lms = 0.f;
     cudaEventElapsedTime(&lms, l0, l1);
     cudaEventDestroy(l0);
     cudaEventDestroy(l1);
     auto t1 = std::chrono::steady_clock::now();
-    c->stats.iterations = hsv.it;
-    c->stats.restarts = restarts;
-    c->stats.relres_recursive = std::sqrt(std::max(hsv.rr, 0.0)) / fnorm;
+    c->stats.iterations = its;
+    c->stats.restarts = refines;
+    c->stats.relres_recursive = rec;
     c->stats.relres_true = std::sqrt(r2) / fnorm;
     c->stats.ms_pcg = lms;
     c->stats.ms_solve = std::chrono::duration<double, std::milli>(t1 - t0).count();
     c->stats.launches_per_iter = c->launches_per_iter;
-    if (iters) *iters = hsv.it;
+    c->stats.kernels_launched = c->launches;
+    if (iters) *iters = its;
     if (relres) *relres = c->stats.relres_true;
-    if (hsv.status == DE_EBREAKDOWN) {
-        set_error("PCG breakdown (p^T S p <= 0 or a non-positive Ritz value) at iteration %d", hsv.it);
+    if (status == DE_EBREAKDOWN) {
+        set_error("PCG breakdown (p^T S p <= 0 or a non-positive Ritz value) at iteration %d", its);
         return DE_EBREAKDOWN;
     }
-    if (hsv.rr > hsv.tol2) {
-        set_error("PCG did not reach rtol in %d iterations (relres %.3e)", hsv.it, c->stats.relres_recursive);
+    if (!conv || c->stats.relres_true > rtol) {
+        set_error("did not reach rtol in %d iterations (true relres %.3e, recursive %.3e)", its,
+                  c->stats.relres_true, rec);
         return DE_ENOCONV;
     }
     return DE_OK;

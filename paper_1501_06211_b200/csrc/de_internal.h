@@ -231,6 +231,7 @@ void launch_pcg_init(double* r, double* p, const double* z, const double* g, con
                      int64_t n, int mode, RedBuf rb, PcgState* s, cudaStream_t st);
 void launch_norm2(const double* v, int64_t n, RedBuf rb, double* out, cudaStream_t st);
 void launch_copy(double* dst, const double* src, int64_t n, const PcgState* s, cudaStream_t st);
+void launch_axpy(double* y, const double* x, double a, int64_t n, cudaStream_t st);
 void launch_scatter_gamma(const int32_t* gamma_dofs, const double* uG, double* u, int64_t nG,
                           cudaStream_t st);
 void launch_gather_gamma(const int32_t* gamma_dofs, const double* f, double* fG, int64_t nG,

@@ -219,16 +219,20 @@ de_status_t build_elim(const HostSetup& hs, const HCsr& X, HElim& E) {
             }
         }
         E.face_band[F] = b;
-        E.face_fac_off[F + 1] = E.face_fac_off[F] + int64_t(n) * (b + 1);
+        E.face_fac_off[F + 1] = E.face_fac_off[F] + 2 * int64_t(n) * (b + 1);   // [L | M = P L^T P]
         dense[F].swap(A);
     }
     E.face_fac.assign(E.face_fac_off[E.nfaces], 0.0);
     for (int32_t F = 0; F < E.nfaces; ++F) {
-        const int32_t n = E.face_off[F + 1] - E.face_off[F];
-        if (!small_band_cholesky(n, E.face_band[F], dense[F], &E.face_fac[E.face_fac_off[F]])) {
+        const int32_t n = E.face_off[F + 1] - E.face_off[F], b = E.face_band[F], ld = b + 1;
+        double* Lf = &E.face_fac[E.face_fac_off[F]];
+        if (!small_band_cholesky(n, b, dense[F], Lf)) {
             set_error("face block %d of the interface operator is not SPD", F);
             return DE_EINVAL;
         }
+        double* Mf = Lf + size_t(n) * ld;   // column j' of M = row n-1-j' of L, reversed
+        for (int32_t j = 0; j < n; ++j)
+            for (int k = 0; k <= b && j + k < n; ++k) Mf[size_t(n - 1 - j - k) * ld + k] = Lf[size_t(j) * ld + k];
     }
     // dense cross-point Schur complements S_C = X_CC - X_CF X_FF^-1 X_FC per component
     E.sc_off.assign(hs.ncomp + 1, 0);

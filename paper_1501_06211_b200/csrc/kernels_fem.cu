@@ -5,7 +5,9 @@
 //     A_II,s (lower band, local lexicographic order), A_IG,s and A_GG,s (ring) is
 //     sum_{elements e of s containing both nodes} E_e * KE0[la,ca][lb,cb]  — node-pair centric, in a fixed
 //     element order, atomic-free and deterministic.
-// B2: A_II,s = L L^T by right-looking band Cholesky ("O(k^2 n), k is the bandwidth");
+// B2: A_II,s = L L^T by right-looking band Cholesky ("O(k^2 n), k is the bandwidth"),
+//     written twice: L (column band) and M = P L^T P (column j' of M = row n-1-j' of L, reversed),
+//     so both triangular solves of the Schur apply are forward column sweeps;
 //     2D bands (b ~ 65) keep the active (b+1)^2 window in shared memory; 3D bands (b ~ 400-500) use
 //     32-column panels in shared memory with the trailing rank-32 update in global memory (L2).
 //     Storage: column band, ld = b+1 rounded to even, slot 0 = 1/L_jj (the solves multiply).
@@ -84,6 +86,7 @@ __global__ void k_assemble_band(MeshDev m, const SubDesc* __restrict__ sd, const
         double v = 0.0;
         if (k <= bw && r < d.nI) v = stiffness_entry(m, Ee, idofs[d.ioff + r], idofs[d.ioff + j], -1);
         band[d.band_off + t] = v;
+        band[d.band_off + total + t] = 0.0;   // M copy (filled by the factorisation; zero padding)
     }
 }
 
@@ -123,6 +126,7 @@ __global__ void __launch_bounds__(256) k_band_chol_smem(const SubDesc* __restric
     const SubDesc d = sd[blockIdx.x];
     const int n = d.nI;
     double* base = band + d.band_off;
+    double* Mb = base + int64_t(n) * ld;
     const int tid = threadIdx.x, nt = blockDim.x;
     for (int i = tid; i < W * ld; i += nt) {
         const int c = i / ld;
@@ -137,7 +141,10 @@ __global__ void __launch_bounds__(256) k_band_chol_smem(const SubDesc* __restric
         if (bad && tid == 0) atomicCAS(fail, 0, d.gid + 1);
         for (int k = tid; k < ld; k += nt) l[k] = (k == 0) ? inv : (k <= bw ? cj[k] * inv : 0.0);
         __syncthreads();
-        for (int k = tid; k < ld; k += nt) base[int64_t(j) * ld + k] = l[k];
+        for (int k = tid; k < ld; k += nt) {
+            base[int64_t(j) * ld + k] = l[k];
+            if (k <= bw && j + k < n) Mb[int64_t(n - 1 - j - k) * ld + k] = l[k];   // M = P L^T P
+        }
         // rank-1 update of columns j+1..j+bw: (m, r) with m in [1,bw], r in [0, bw-m]
         for (int t = tid; t < bw * W; t += nt) {
             const int mm = 1 + t / W, rem = t - (mm - 1) * W;
@@ -158,6 +165,7 @@ __global__ void __launch_bounds__(512) k_band_chol_panel(const SubDesc* __restri
     const SubDesc d = sd[blockIdx.x];
     const int n = d.nI;
     double* base = band + d.band_off;
+    double* Mb = base + int64_t(n) * ld;
     const int tid = threadIdx.x, nt = blockDim.x;
     for (int j0 = 0; j0 < n; j0 += NBP) {
         const int nb = min(NBP, n - j0);
@@ -181,7 +189,11 @@ __global__ void __launch_bounds__(512) k_band_chol_panel(const SubDesc* __restri
             }
             __syncthreads();
         }
-        for (int i = tid; i < nb * ld; i += nt) base[int64_t(j0) * ld + i] = P[i];
+        for (int i = tid; i < nb * ld; i += nt) {
+            base[int64_t(j0) * ld + i] = P[i];
+            const int jj = i / ld, k = i - jj * ld, j = j0 + jj;
+            if (k <= bw && j + k < n) Mb[int64_t(n - 1 - j - k) * ld + k] = P[i];   // M = P L^T P
+        }
         // trailing update of columns c in [j0+nb, j0+nb-1+bw], rows r = c + rr (rr in [0,bw])
         const int c_lo = j0 + nb, c_hi = min(j0 + nb - 1 + bw, n - 1);
         const int ncol = c_hi - c_lo + 1;
@@ -219,6 +231,30 @@ int launch_band_cholesky(const SubDesc* sd, int nsl, double* band, int ld, int b
 
 // ---------------------------------------------------------------- true residual (matrix-free)
 
+// Double-double helpers (error-free transformations) for an accurate residual f - K u: the
+// computed residual is what iterative refinement (R11) and the reported final relres use.
+struct dd_t {
+    double hi, lo;
+};
+__device__ __forceinline__ dd_t two_sum(double a, double b) {
+    const double s = a + b, bb = s - a;
+    return {s, (a - (s - bb)) + (b - bb)};
+}
+__device__ __forceinline__ dd_t dd_add(dd_t a, dd_t b) {
+    dd_t s = two_sum(a.hi, b.hi);
+    s.lo += a.lo + b.lo;
+    return two_sum(s.hi, s.lo);
+}
+__device__ __forceinline__ dd_t dd_mul_d(dd_t a, double b) {
+    const double p = a.hi * b;
+    const double e = fma(a.hi, b, -p);
+    return two_sum(p, e + a.lo * b);
+}
+__device__ __forceinline__ dd_t two_prod(double a, double b) {
+    const double p = a * b;
+    return {p, fma(a, b, -p)};
+}
+
 __global__ void k_apply_K(MeshDev m, const double* __restrict__ Ee, const double* __restrict__ u,
                           const double* __restrict__ f, const int8_t* __restrict__ cls,
                           double* __restrict__ res, int64_t ndof) {
@@ -234,7 +270,7 @@ __global__ void k_apply_K(MeshDev m, const double* __restrict__ Ee, const double
             co[a] = r % m.nn[a];
             r /= m.nn[a];
         }
-        double acc = 0.0;
+        dd_t acc = {-f[d], 0.0};
         const int nz = dim == 3 ? 2 : 1;
         for (int oz = 0; oz < nz; ++oz)
             for (int oy = 0; oy < 2; ++oy)
@@ -243,15 +279,15 @@ __global__ void k_apply_K(MeshDev m, const double* __restrict__ Ee, const double
                     if (ex < 0 || ey < 0 || ez < 0 || ex >= m.nel[0] || ey >= m.nel[1] || (dim == 3 && ez >= m.nel[2])) continue;
                     const int la = (co[0] - ex) + 2 * (co[1] - ey) + 4 * (co[2] - ez);
                     const int64_t e = ex + int64_t(m.nel[0]) * (ey + int64_t(m.nel[1]) * ez);
-                    double t = 0.0;
+                    dd_t t = {0.0, 0.0};
                     for (int lb = 0; lb < (1 << dim); ++lb) {
                         const int64_t nbn = (ex + (lb & 1)) + int64_t(m.nn[0]) * ((ey + ((lb >> 1) & 1)) + int64_t(m.nn[1]) * (ez + ((lb >> 2) & 1)));
                         for (int cb = 0; cb < dim; ++cb)
-                            t += c_KE[(dim * la + c) * m.nke + dim * lb + cb] * u[dim * nbn + cb];
+                            t = dd_add(t, two_prod(c_KE[(dim * la + c) * m.nke + dim * lb + cb], u[dim * nbn + cb]));
                     }
-                    acc += Ee[e] * t;
+                    acc = dd_add(acc, dd_mul_d(t, Ee[e]));
                 }
-        res[d] = f[d] - acc;
+        res[d] = -(acc.hi + acc.lo);   // f - K u, accurate to ~1 ulp of the result
     }
 }
 

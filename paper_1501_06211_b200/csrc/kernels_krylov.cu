@@ -221,6 +221,16 @@ void launch_copy(double* dst, const double* src, int64_t n, const PcgState* s, c
     k_copy<<<blocks, 256, 0, st>>>(dst, src, n, s);
 }
 
+__global__ void k_axpy(double* __restrict__ y, const double* __restrict__ x, double a, int64_t n) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+        y[i] += a * x[i];
+}
+
+void launch_axpy(double* y, const double* x, double a, int64_t n, cudaStream_t st) {
+    const int blocks = int(std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8)));
+    k_axpy<<<blocks, 256, 0, st>>>(y, x, a, n);
+}
+
 __global__ void k_scatter_gamma(const int32_t* __restrict__ gd, const double* __restrict__ uG, double* __restrict__ u,
                                 int64_t nG) {
     for (int64_t g = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; g < nG; g += int64_t(gridDim.x) * blockDim.x)

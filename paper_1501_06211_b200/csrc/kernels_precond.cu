@@ -89,44 +89,62 @@ __global__ void k_prec_init(PrecDev P, const double* __restrict__ r, const PcgSt
 }
 
 // ------------------------------------------------------------------ exact elimination solves
-// mode 0: y_F = X_FF^-1 b_F ; mode 1: x_F = X_FF^-1 (b_F - X_FC xC)
+// mode 0: y_F = X_FF^-1 b_F ; mode 1: x_F = X_FF^-1 (b_F - X_FC xC).
+// Warp per face; both triangular solves are forward column sweeps (L, then M = P L^T P) with the
+// b+1 active rows in registers (lane l holds row j+l; b <= 31), one shuffle per row on the chain.
 __global__ void k_face_solve(ElimDev E, const double* __restrict__ b, const double* __restrict__ xC,
-                             double* __restrict__ out, int mode, int maxf, int maxfac, const PcgState* s) {
+                             double* __restrict__ out, int mode, int per_warp, int mf, const PcgState* s) {
     if (s && s->done) return;
-    extern __shared__ double fsm[];
+    extern __shared__ double fsh[];
     const int wpb = blockDim.x >> 5, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int F = blockIdx.x * wpb + w;
     if (F >= E.nfaces) return;
-    double* v = fsm + size_t(w) * (maxf + maxfac);
-    double* fac = v + maxf;
+    double* rb = fsh + size_t(w) * per_warp;
+    double* ys = rb + mf;
+    double* fs = ys + mf;                       // staged [L | M] factor of this face
     const int o = E.face_off[F], n = E.face_off[F + 1] - o, bw = E.face_band[F], ld = bw + 1;
     const double* gf = E.face_fac + E.face_fac_off[F];
-    for (int i = lane; i < n * ld; i += 32) fac[i] = gf[i];
+    for (int i = lane; i < 2 * n * ld; i += 32) fs[i] = gf[i];
+    const double* Lf = fs;
+    const double* Mf = fs + size_t(n) * ld;
     for (int i = lane; i < n; i += 32) {
         double r = b[E.face_nodes[o + i]];
         if (mode == 1)
             for (int e = E.xfc_ptr[o + i]; e < E.xfc_ptr[o + i + 1]; ++e) r -= E.xfc_val[e] * xC[E.xfc_col[e]];
-        v[i] = r;
+        rb[i] = r;
     }
     __syncwarp();
-    for (int j = 0; j < n; ++j) {
-        const double vj = v[j] * fac[j * ld];
-        for (int k = lane + 1; k <= bw && j + k < n; k += 32) v[j + k] -= fac[j * ld + k] * vj;
+#pragma unroll 1
+    for (int sw = 0; sw < 2; ++sw) {
+        const double* fac = sw == 0 ? Lf : Mf;
+        const double* src = sw == 0 ? rb : ys;
+        double v = lane < n ? src[lane] : 0.0;   // ys already holds P y
         __syncwarp();
-        if (lane == 0) v[j] = vj;
+#pragma unroll 4
+        for (int j = 0; j < n; ++j) {
+            const double* col = fac + size_t(j) * ld;
+            const double cl = (lane >= 1 && lane <= bw) ? col[lane] : 0.0;
+            const double yj = __shfl_sync(0xffffffffu, v, 0) * col[0];
+            v = fma(-cl, yj, v);
+            v = __shfl_down_sync(0xffffffffu, v, 1);
+            if (lane == 31) {
+                const int r = j + 32;
+                v = r < n ? src[r] : 0.0;
+            }
+            if (lane == 0) {
+                if (sw == 0) ys[n - 1 - j] = yj;          // y stored reversed for the M sweep
+                else out[E.face_nodes[o + n - 1 - j]] = yj;
+            }
+        }
         __syncwarp();
     }
-    for (int j = n - 1; j >= 0; --j) {
-        double t = 0.0;
-        for (int k = lane + 1; k <= bw && j + k < n; k += 32) t += fac[j * ld + k] * v[j + k];
-        for (int off = 1; off < min(bw, 32); off <<= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
-        t = __shfl_sync(0xffffffffu, t, 0);
-        const double vj = (v[j] - t) * fac[j * ld];
-        __syncwarp();
-        if (lane == 0) v[j] = vj;
-        __syncwarp();
-    }
-    for (int i = lane; i < n; i += 32) out[E.face_nodes[o + i]] = v[i];
+}
+
+static int face_warps_per_block(int per_warp_doubles) {
+    const int bytes = per_warp_doubles * 8;
+    int w = 4;
+    while (w > 1 && w * bytes > 160 * 1024) --w;
+    return w;
 }
 
 // x_C = S_C^-1 (b_C - X_CF y): each CTA rebuilds t_C of its component in smem, warps do rows.
@@ -162,16 +180,17 @@ __global__ void k_cross_solve(ElimDev E, const double* __restrict__ b, const dou
 
 static void elim_solve(const PrecDev& P, const ElimDev& E, const double* b, double* x, const PcgState* s,
                        cudaStream_t st, int* nl) {
-    const int maxf = P.nblk;   // unused placeholder
-    (void)maxf;
-    // sizes for the face kernel are stashed in E.maxface (max nodes) and derived factor size
     const int mf = E.maxface & 0xffff, mfac = E.maxface >> 16;
-    const int wpb = 4;
-    const size_t smem_face = size_t(wpb) * (mf + mfac) * sizeof(double);
+    const int per_warp = 2 * mf + mfac;
+    const int wpb = face_warps_per_block(per_warp);
+    auto face = [&](const double* xc, double* o, int mode) {
+        const int g = (E.nfaces + wpb - 1) / wpb;
+        k_face_solve<<<g, 32 * wpb, size_t(wpb) * per_warp * sizeof(double), st>>>(E, b, xc, o, mode, per_warp, mf, s);
+    };
     double* y = P.y;
     double* xC = P.y + P.nflat;   // cross solution scratch (ncross entries)
     if (E.nfaces > 0) {
-        k_face_solve<<<(E.nfaces + wpb - 1) / wpb, 32 * wpb, smem_face, st>>>(E, b, xC, y, 0, mf, mfac, s);
+        face(xC, y, 0);
         ++*nl;
     }
     if (E.ncross > 0) {
@@ -183,7 +202,7 @@ static void elim_solve(const PrecDev& P, const ElimDev& E, const double* b, doub
         ++*nl;
     }
     if (E.nfaces > 0) {
-        k_face_solve<<<(E.nfaces + wpb - 1) / wpb, 32 * wpb, smem_face, st>>>(E, b, xC, x, 1, mf, mfac, s);
+        face(xC, x, 1);
         ++*nl;
     }
 }
@@ -277,149 +296,243 @@ __global__ void k_spmv_multi(PrecDev P, CsrDev A, double* __restrict__ out, cons
     }
 }
 
-// Rayleigh-Ritz dots: tasks (i <= j) A_ij = W_i.LW_j, B_ij = W_i.MW_j, and wr_i = W_i.rf
-__global__ void k_mdot_rr(PrecDev P, int kmax, const PcgState* s) {
+// Rayleigh-Ritz Gram products G[i][jz] = W_i . Z_jz with Z = [LW_0..LW_{k-1} | MW_0..MW_{k-1} | rf]:
+// per block a tile of TR rows of all 3k+1 vectors is staged in shared memory (each vector read
+// once); one output per thread; per-block partials reduced in block order by the last block.
+constexpr int TR = 64;
+constexpr int RR_TASKS = KMAX * (2 * KMAX + 1);
+__global__ void __launch_bounds__(512) k_mdot_rr(PrecDev P, const PcgState* s) {
     if (s && s->done) return;
-    const int task = blockIdx.y, c = blockIdx.z;
+    __shared__ double tile[(3 * KMAX + 1) * (TR + 1)];
+    __shared__ bool last;
+    const int c = blockIdx.y;
     const LzState& z = P.lz[c];
     if (!z.active) return;
-    const int kc = z.kc;
-    const int npair = kc * (kc + 1) / 2;
-    int kind, i = 0, j = 0;
-    if (task < npair) kind = 0;
-    else if (task < 2 * npair) kind = 1;
-    else if (task < 2 * npair + kc) kind = 2;
-    else return;
-    int t = kind == 0 ? task : (kind == 1 ? task - npair : task - 2 * npair);
-    if (kind < 2) {
-        while (t >= kc - i) {
-            t -= kc - i;
-            ++i;
-        }
-        j = i + t;
-    } else {
-        i = t;
-    }
+    const int k = z.kc, nz = 2 * k + 1, nv = k + nz, nt = k * nz;
     const int64_t lo = P.comp_off[c], hi = P.comp_off[c + 1];
-    const double* a = P.W + size_t(i) * P.nflat;
-    const double* b = kind == 0 ? P.LW + size_t(j) * P.nflat : (kind == 1 ? P.MW + size_t(j) * P.nflat : P.rf);
-    double v = 0.0;
-    for (int64_t x = lo + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; x < hi; x += int64_t(gridDim.x) * blockDim.x)
-        v += a[x] * b[x];
-    const int ntask = kmax * (kmax + 1) + kmax;
-    double tot;
-    if (seg_reduce(v, 8 + MAXC * KMAX + c * ntask + task, gridDim.x, P.part, P.counter, &tot)) {
-        LzState& zz = P.lz[c];
-        if (kind == 0) zz.A[i * KMAX + j] = zz.A[j * KMAX + i] = tot;
-        else if (kind == 1) zz.B[i * KMAX + j] = zz.B[j * KMAX + i] = tot;
-        else zz.wr[i] = tot;
+    const int tid = threadIdx.x;
+    double acc0 = 0.0, acc1 = 0.0;
+    for (int64_t r0 = lo + int64_t(blockIdx.x) * TR; r0 < hi; r0 += int64_t(gridDim.x) * TR) {
+        for (int t = tid; t < nv * TR; t += blockDim.x) {
+            const int v = t / TR, rr = t - v * TR;
+            const int64_t r = r0 + rr;
+            double val = 0.0;
+            if (r < hi) {
+                if (v < k) val = P.W[size_t(v) * P.nflat + r];
+                else if (v < 2 * k) val = P.LW[size_t(v - k) * P.nflat + r];
+                else if (v < 3 * k) val = P.MW[size_t(v - 2 * k) * P.nflat + r];
+                else val = P.rf[r];
+            }
+            tile[v * (TR + 1) + rr] = val;
+        }
+        __syncthreads();
+        for (int t = tid, h = 0; t < nt; t += blockDim.x, ++h) {
+            const int i = t / nz, jz = t - i * nz;
+            const double* a = tile + i * (TR + 1);
+            const double* b = tile + (k + jz) * (TR + 1);
+            double acc = 0.0;
+#pragma unroll 8
+            for (int rr = 0; rr < TR; ++rr) acc += a[rr] * b[rr];
+            if (h == 0) acc0 += acc;
+            else acc1 += acc;
+        }
+        __syncthreads();
     }
+    const int nb = gridDim.x;
+    const size_t base = size_t(8 + MAXC * KMAX + c * RR_TASKS);
+    for (int t = tid, h = 0; t < nt; t += blockDim.x, ++h) P.part[(base + t) * nb + blockIdx.x] = h == 0 ? acc0 : acc1;
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) last = (atomicAdd(P.counter + base, 1u) == unsigned(nb - 1));
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    LzState& zz = P.lz[c];
+    for (int t = tid; t < nt; t += blockDim.x) {
+        double sum = 0.0;
+        for (int bx = 0; bx < nb; ++bx) sum += *((volatile double*)&P.part[(base + t) * nb + bx]);
+        const int i = t / nz, jz = t - i * nz;
+        if (jz < k) zz.A[i * KMAX + jz] = sum;
+        else if (jz < 2 * k) zz.B[i * KMAX + (jz - k)] = sum;
+        else zz.wr[i] = sum;
+    }
+    if (tid == 0) P.counter[base] = 0u;
 }
 
-// Small generalized symmetric eigenproblem A y = theta B y per component (one thread each):
-// Cholesky B = R R^T, C = R^-1 A R^-T, cyclic Jacobi, Y = R^-T V; coef = Y f(Theta) Y^T wr.
+// Small generalized symmetric eigenproblem A y = theta B y per component, one warp each:
+// B = R R^T (Cholesky), C = R^-1 A R^-T, parallel (round-robin) Jacobi C = V Theta V^T,
+// Y = R^-T V, coef = Y f(Theta) Y^T wr  (R9; SPEC.md:243-251 dense_sym_gen_eig).
 __global__ void k_lz_eig(PrecDev P, PcgState* s) {
     if (s && s->done) return;
-    const int c = threadIdx.x;
+    constexpr int LDK = KMAX + 1;
+    __shared__ double sm[MAXC][4][KMAX * LDK];
+    __shared__ double rot[MAXC][2][KMAX / 2];
+    __shared__ int rpq[MAXC][2][KMAX / 2];
+    __shared__ double fe[MAXC][KMAX], ge[MAXC][KMAX];
+    const int c = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (c >= P.ncomp) return;
     LzState& z = P.lz[c];
-    for (int i = 0; i < KMAX; ++i) z.coef[i] = 0.0;
+    if (lane < KMAX) z.coef[lane] = 0.0;
     if (!z.active) return;
     const int n = z.kc;
-    double R[KMAX][KMAX], C[KMAX][KMAX], V[KMAX][KMAX];
-    for (int i = 0; i < n; ++i)
-        for (int j = 0; j < n; ++j) R[i][j] = (j <= i) ? z.B[i * KMAX + j] : 0.0;
-    for (int j = 0; j < n; ++j) {          // Cholesky (lower)
-        double d = R[j][j];
-        for (int k = 0; k < j; ++k) d -= R[j][k] * R[j][k];
-        if (!(d > 0.0)) {
+    double* R = sm[c][0];
+    double* C = sm[c][1];
+    double* V = sm[c][2];
+    double* X = sm[c][3];
+    auto fail = [&]() {
+        if (lane == 0) {
             z.status = DE_EBREAKDOWN;
-            if (s) { s->status = DE_EBREAKDOWN; s->done = 1; }
+            if (s) {
+                s->status = DE_EBREAKDOWN;
+                s->done = 1;
+            }
+        }
+    };
+    for (int idx = lane; idx < n * n; idx += 32) {
+        const int i = idx / n, j = idx - i * n;
+        C[i * LDK + j] = 0.5 * (z.A[i * KMAX + j] + z.A[j * KMAX + i]);
+        R[i * LDK + j] = 0.5 * (z.B[i * KMAX + j] + z.B[j * KMAX + i]);
+        V[i * LDK + j] = (i == j) ? 1.0 : 0.0;
+    }
+    __syncwarp();
+    for (int j = 0; j < n; ++j) {                          // right-looking Cholesky, lower in R
+        const double d = R[j * LDK + j];
+        if (!(d > 0.0)) {
+            fail();
             return;
         }
-        R[j][j] = sqrt(d);
-        for (int i = j + 1; i < n; ++i) {
-            double t = R[i][j];
-            for (int k = 0; k < j; ++k) t -= R[i][k] * R[j][k];
-            R[i][j] = t / R[j][j];
+        const double l = sqrt(d);
+        __syncwarp();
+        if (lane == 0) R[j * LDK + j] = l;
+        if (lane > j && lane < n) R[lane * LDK + j] /= l;
+        __syncwarp();
+        for (int idx = lane; idx < (n - j - 1) * (n - j - 1); idx += 32) {
+            const int i = j + 1 + idx / (n - j - 1), kk = j + 1 + idx % (n - j - 1);
+            if (kk <= i) R[i * LDK + kk] -= R[i * LDK + j] * R[kk * LDK + j];
+        }
+        __syncwarp();
+    }
+    if (lane < n) {                                         // X = R^-1 C (lane = column)
+        for (int i = 0; i < n; ++i) {
+            double t = C[i * LDK + lane];
+            for (int kk = 0; kk < i; ++kk) t -= R[i * LDK + kk] * X[kk * LDK + lane];
+            X[i * LDK + lane] = t / R[i * LDK + i];
         }
     }
-    // X = R^-1 A (column by column), then C = X R^-T  (i.e. C^T = R^-1 X^T)
-    double X[KMAX][KMAX];
-    for (int col = 0; col < n; ++col)
+    __syncwarp();
+    if (lane < n) {                                         // C = X R^-T (lane = row)
         for (int i = 0; i < n; ++i) {
-            double t = z.A[i * KMAX + col];
-            for (int k = 0; k < i; ++k) t -= R[i][k] * X[k][col];
-            X[i][col] = t / R[i][i];
+            double t = X[lane * LDK + i];
+            for (int kk = 0; kk < i; ++kk) t -= C[lane * LDK + kk] * R[i * LDK + kk];
+            C[lane * LDK + i] = t / R[i * LDK + i];
         }
-    for (int row = 0; row < n; ++row)
-        for (int i = 0; i < n; ++i) {
-            double t = X[row][i];
-            for (int k = 0; k < i; ++k) t -= R[i][k] * C[row][k];
-            C[row][i] = t / R[i][i];
+    }
+    __syncwarp();
+    for (int idx = lane; idx < n * n; idx += 32) {          // symmetrise (read pairs once)
+        const int i = idx / n, j = idx - i * n;
+        if (j > i) {
+            const double m = 0.5 * (C[i * LDK + j] + C[j * LDK + i]);
+            C[i * LDK + j] = m;
+            C[j * LDK + i] = m;
         }
-    for (int i = 0; i < n; ++i)
-        for (int j = 0; j < n; ++j) {
-            const double m = 0.5 * (C[i][j] + C[j][i]);
-            C[i][j] = m;
-            V[i][j] = (i == j) ? 1.0 : 0.0;
-        }
-    for (int sweep = 0; sweep < 60; ++sweep) {
+    }
+    __syncwarp();
+    const int m = (n + 1) & ~1, npair = m / 2;
+    for (int sweep = 0; sweep < 40 && n > 1; ++sweep) {
         double off = 0.0, dia = 0.0;
-        for (int i = 0; i < n; ++i)
-            for (int j = 0; j < n; ++j) (i == j ? dia : off) += C[i][j] * C[i][j];
-        if (off <= 1e-32 * dia) break;
-        for (int p = 0; p < n - 1; ++p)
-            for (int q = p + 1; q < n; ++q) {
-                const double apq = C[p][q];
-                if (apq == 0.0) continue;
-                const double tau = (C[q][q] - C[p][p]) / (2.0 * apq);
-                const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-                const double cs = 1.0 / sqrt(1.0 + t * t), sn = t * cs;
-                for (int k = 0; k < n; ++k) {
-                    const double ckp = C[k][p], ckq = C[k][q];
-                    C[k][p] = cs * ckp - sn * ckq;
-                    C[k][q] = sn * ckp + cs * ckq;
-                }
-                for (int k = 0; k < n; ++k) {
-                    const double cpk = C[p][k], cqk = C[q][k];
-                    C[p][k] = cs * cpk - sn * cqk;
-                    C[q][k] = sn * cpk + cs * cqk;
-                }
-                for (int k = 0; k < n; ++k) {
-                    const double vkp = V[k][p], vkq = V[k][q];
-                    V[k][p] = cs * vkp - sn * vkq;
-                    V[k][q] = sn * vkp + cs * vkq;
-                }
+        if (lane < n)
+            for (int j = 0; j < n; ++j) {
+                const double v = C[lane * LDK + j];
+                if (j == lane) dia += v * v;
+                else off += v * v;
             }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            off += __shfl_xor_sync(0xffffffffu, off, o);
+            dia += __shfl_xor_sync(0xffffffffu, dia, o);
+        }
+        if (off <= 1e-30 * dia) break;
+        for (int rnd = 0; rnd < m - 1; ++rnd) {
+            if (lane < npair) {                             // round-robin pairs (circle method)
+                int p, q;
+                if (lane == 0) {
+                    p = m - 1;
+                    q = rnd;
+                } else {
+                    p = (rnd + lane) % (m - 1);
+                    q = (rnd - lane + (m - 1)) % (m - 1);
+                }
+                if (p > q) {
+                    const int t = p;
+                    p = q;
+                    q = t;
+                }
+                double cs = 1.0, sn = 0.0;
+                if (q < n) {
+                    const double apq = C[p * LDK + q];
+                    if (fabs(apq) > 1e-300) {
+                        const double tau = (C[q * LDK + q] - C[p * LDK + p]) / (2.0 * apq);
+                        const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+                        cs = 1.0 / sqrt(1.0 + t * t);
+                        sn = t * cs;
+                    }
+                }
+                rot[c][0][lane] = cs;
+                rot[c][1][lane] = sn;
+                rpq[c][0][lane] = p;
+                rpq[c][1][lane] = q;
+            }
+            __syncwarp();
+            if (lane < n)                                   // C <- C J (columns), V <- V J
+                for (int t = 0; t < npair; ++t) {
+                    const int p = rpq[c][0][t], q = rpq[c][1][t];
+                    if (q >= n) continue;
+                    const double cs = rot[c][0][t], sn = rot[c][1][t];
+                    const double a = C[lane * LDK + p], b = C[lane * LDK + q];
+                    C[lane * LDK + p] = cs * a - sn * b;
+                    C[lane * LDK + q] = sn * a + cs * b;
+                    const double va = V[lane * LDK + p], vb = V[lane * LDK + q];
+                    V[lane * LDK + p] = cs * va - sn * vb;
+                    V[lane * LDK + q] = sn * va + cs * vb;
+                }
+            __syncwarp();
+            if (lane < n)                                   // C <- J^T C (rows)
+                for (int t = 0; t < npair; ++t) {
+                    const int p = rpq[c][0][t], q = rpq[c][1][t];
+                    if (q >= n) continue;
+                    const double cs = rot[c][0][t], sn = rot[c][1][t];
+                    const double a = C[p * LDK + lane], b = C[q * LDK + lane];
+                    C[p * LDK + lane] = cs * a - sn * b;
+                    C[q * LDK + lane] = sn * a + cs * b;
+                }
+            __syncwarp();
+        }
     }
     const bool sing = P.singular[c] != 0;
-    double Y[KMAX][KMAX], f[KMAX];
-    for (int e = 0; e < n; ++e) {
-        const double th = C[e][e];
-        z.theta_ritz[e] = th;
-        if (!sing && !(th > 0.0)) {
-            z.status = DE_EBREAKDOWN;
-            if (s) { s->status = DE_EBREAKDOWN; s->done = 1; }
-            return;
+    int bad = 0;
+    if (lane < n) {
+        const double th = C[lane * LDK + lane];
+        z.theta_ritz[lane] = th;
+        if (!sing && !(th > 0.0)) bad = 1;
+        fe[c][lane] = sing ? 1.0 / (1.0 + pow(fmax(th, 0.0), 1.0 - P.theta)) : pow(th, P.theta - 1.0);
+        for (int i = n - 1; i >= 0; --i) {                  // Y(:,e) = R^-T V(:,e), lane = e
+            double t = V[i * LDK + lane];
+            for (int kk = i + 1; kk < n; ++kk) t -= R[kk * LDK + i] * X[kk * LDK + lane];
+            X[i * LDK + lane] = t / R[i * LDK + i];
         }
-        f[e] = sing ? 1.0 / (1.0 + pow(fmax(th, 0.0), 1.0 - P.theta)) : pow(th, P.theta - 1.0);
-        for (int i = n - 1; i >= 0; --i) {   // Y(:,e) = R^-T V(:,e)
-            double t = V[i][e];
-            for (int k = i + 1; k < n; ++k) t -= R[k][i] * Y[k][e];
-            Y[i][e] = t / R[i][i];
-        }
-    }
-    double g[KMAX];
-    for (int e = 0; e < n; ++e) {
         double t = 0.0;
-        for (int i = 0; i < n; ++i) t += Y[i][e] * z.wr[i];
-        g[e] = f[e] * t;
+        for (int i = 0; i < n; ++i) t += X[i * LDK + lane] * z.wr[i];
+        ge[c][lane] = fe[c][lane] * t;
     }
-    for (int i = 0; i < n; ++i) {
+    if (__any_sync(0xffffffffu, bad)) {
+        fail();
+        return;
+    }
+    __syncwarp();
+    if (lane < n) {
         double t = 0.0;
-        for (int e = 0; e < n; ++e) t += Y[i][e] * g[e];
-        z.coef[i] = t;
+        for (int e = 0; e < n; ++e) t += X[lane * LDK + e] * ge[c][e];
+        z.coef[lane] = t;
     }
 }
 
@@ -463,20 +576,19 @@ void prec_apply(const PrecDev& P, const double* r, double* z, const PcgState* s,
     }
     k_spmv_multi<<<dim3(eb, P.kmax), 256, 0, st>>>(P, P.L, P.LW, s); ++nl;
     k_spmv_multi<<<dim3(eb, P.kmax), 256, 0, st>>>(P, P.M, P.MW, s); ++nl;
-    const int ntask = P.kmax * (P.kmax + 1) + P.kmax;
-    k_mdot_rr<<<dim3(nb, ntask, P.ncomp), PB, 0, st>>>(P, P.kmax, s); ++nl;
-    k_lz_eig<<<1, 32, 0, st>>>(P, const_cast<PcgState*>(s)); ++nl;
+    k_mdot_rr<<<dim3(nb, P.ncomp), 512, 0, st>>>(P, s); ++nl;
+    k_lz_eig<<<1, 32 * P.ncomp, 0, st>>>(P, const_cast<PcgState*>(s)); ++nl;
     k_lz_combine<<<eb, 256, 0, st>>>(P, z, s); ++nl;
     if (nlaunch) *nlaunch = nl;
 }
 
 void prec_prepare(const PrecDev& P) {
+    int mx = 0;
     for (const ElimDev* E : {&P.eK, &P.eM}) {
-        const int mf = E->maxface & 0xffff, mfac = E->maxface >> 16;
-        const size_t smem = size_t(4) * (mf + mfac) * sizeof(double);
-        if (smem > 48 * 1024)
-            cudaFuncSetAttribute(k_face_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        const int per_warp = 2 * (E->maxface & 0xffff) + (E->maxface >> 16);
+        mx = std::max(mx, face_warps_per_block(per_warp) * per_warp * 8);
     }
+    if (mx > 48 * 1024) cudaFuncSetAttribute(k_face_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
 }
 
 // ------------------------------------------------------------------ Gauss-Jordan SPD inverse (setup)

@@ -1,19 +1,19 @@
 // kernels_schur.cu — SURVEY.md §8(a) rows C1 (condensed rhs), C2 (Schur apply, the headline kernel)
 // and C6 (back-substitution): per owned subdomain s
 //
-//   C2 (SCHUR_APPLY):   x = R_s p;  y = A_IG x;  w = A_II^-1 y;  q_s = A_GG x - A_GI w
+//   C2 (SCHUR_APPLY):    x = R_s p;  y = A_IG x;  w = A_II^-1 y;  q_s = A_GG x - A_GI w
 //   C1 (SCHUR_CONDENSE): w = A_II^-1 f_I;  q_s = -A_GI w     (g = f_G + sum_s R_s^T q_s)
 //   C6 (SCHUR_BACKSUB):  w = A_II^-1 (f_I - A_IG R_s u_G);  u_I = w   (PAPER.md:141,143 combined, :136)
 //
-// One warp per subdomain (one-warp CTAs, ~14 resident per SM at 2D sizes). The interior solve
-// w = L^-T L^-1 y streams the column-band factor twice (forward ascending, backward descending)
-// through a ring of shared-memory stages filled by TMA bulk copies (cp.async.bulk + mbarrier
-// complete_tx) issued by lane 0; the ring is shared by both sweeps so the backward sweep's first
-// stages (the columns the forward sweep read last) are prefetched while the forward sweep finishes
-// and come back from L2.
-//   forward  (column axpy): y_j = t_j / L_jj; t_{j+k} -= L_{j+k,j} y_j   (window of b+1 rows in smem)
-//   backward (blocks of G columns, lane groups own a column): t_j = y_j - sum_{i>block} L_ij x_i,
-//            then a G-step chain inside the block.
+// One warp per subdomain (one-warp CTAs). A_II = L L^T is stored twice in column-band form: L itself
+// and M = P L^T P (P = index reversal; column j' of M is row n-1-j' of L, reversed). Both triangular
+// solves are then the same forward column-axpy sweep
+//      y_j = t_j / L_jj ;  t_{j+k} -= L_{j+k,j} y_j   (k = 1..b)
+// run on L (y = L^-1 rhs) and on M (P w = M^-1 P y). The b+1 active rows live in REGISTERS: lane l
+// holds rows r = l (mod 32) in NS slots; the owner of row j broadcasts y_j with one shuffle, so the
+// dependency chain per row is SHFL + DMUL + DFMA. Columns stream through a ring of shared-memory stages
+// filled by TMA bulk copies (cp.async.bulk + mbarrier complete_tx) issued by lane 0; the ring runs
+// over L then M, so M's first stages are in flight while the L sweep finishes.
 #include "de_internal.h"
 
 namespace de {
@@ -56,31 +56,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     }
 }
 
+// Unified ring over 2*nst stages: stage T < nst streams columns [T*G, ...) of L, stage T >= nst the
+// same columns of M.
 struct Ring {
     uint64_t* bar;
     double* stg;
-    int nstage, G, ld, n, nfw;   // nfw = forward stage count (same for backward)
+    int nstage, G, ld, n, nst;
     const double* L;
-
-    // stage T of the unified ring: T < nfw forward stage T, else backward stage T - nfw
-    __device__ __forceinline__ void cols(int T, int& c0, int& nc) const {
-        if (T < nfw) {
-            c0 = T * G;
-            nc = min(G, n - c0);
-        } else {
-            const int u = T - nfw;
-            const int hi = n - u * G;
-            c0 = max(0, hi - G);
-            nc = hi - c0;
-        }
-    }
+    const double* M;
     __device__ __forceinline__ void issue(int T) const {   // lane 0 only
-        int c0, nc;
-        cols(T, c0, nc);
+        const int t = T < nst ? T : T - nst;
+        const int c0 = t * G, nc = min(G, n - c0);
         const int slot = T % nstage;
         const uint32_t bytes = uint32_t(nc) * uint32_t(ld) * 8u;
         mbar_expect_tx(bar + slot, bytes);
-        tma_load_1d(stg + size_t(slot) * G * ld, L + size_t(c0) * ld, bytes, bar + slot);
+        tma_load_1d(stg + size_t(slot) * G * ld, (T < nst ? L : M) + size_t(c0) * ld, bytes, bar + slot);
     }
     __device__ __forceinline__ const double* wait(int T) const {
         const int slot = T % nstage;
@@ -89,151 +79,152 @@ struct Ring {
     }
 };
 
-template <int G>
-__global__ void __launch_bounds__(32) k_schur_local(SchurArgs a, int nstage, int win) {
+// One forward column sweep over the ring's current matrix. `src` holds the dense right-hand side
+// (row r at src[r]); `dst` receives the solution (row j at dst[j], or dst[n-1-j] when reversed).
+// src and dst may alias: row j is written only after every row <= j + 32*NS has been read.
+// Entering rows and outputs move in coalesced 32-row batches (lane l owns rows = l mod 32).
+template <int G, int NS>
+__device__ __forceinline__ void sweep(const Ring& ring, const double* src, double* dst, bool reversed, int& T,
+                                      int lane, int B, int n) {
+    // reversed: rhs row r is src[n-1-r] and solution row j goes to dst[n-1-j] (the M = P L^T P sweep)
+    const int ld = ring.ld;
+    double v[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+        const int r = lane + 32 * s;
+        v[s] = r < n ? src[reversed ? n - 1 - r : r] : 0.0;
+    }
+    double pend = 0.0, outv = 0.0;
+    for (int t = 0; t < ring.nst; ++t, ++T) {
+        const double* S = ring.wait(T);
+        const int c0 = t * G, nc = min(G, n - c0);
+#pragma unroll
+        for (int cc = 0; cc < G; ++cc) {
+            if (cc < nc) {
+                const int j = c0 + cc;
+                const int o = j & 31;
+                if (o == 0) {   // new 32-row block: prefetch this block's entering rows (coalesced)
+                    const int r = j + lane + 32 * NS;
+                    pend = r < n ? src[reversed ? n - 1 - r : r] : 0.0;
+                }
+                const double* col = S + cc * ld;
+                const int k0 = (lane - j) & 31;
+                double cv[NS];
+#pragma unroll
+                for (int s = 0; s < NS; ++s) {
+                    const int k = k0 + 32 * s;
+                    cv[s] = (k <= B && (s > 0 || k0 != 0)) ? col[k] : 0.0;
+                }
+                const double yj = __shfl_sync(0xffffffffu, v[0], o) * col[0];
+#pragma unroll
+                for (int s = 0; s < NS; ++s) v[s] = fma(-cv[s], yj, v[s]);
+                if (lane == o) {
+                    outv = yj;
+#pragma unroll
+                    for (int s = 0; s < NS - 1; ++s) v[s] = v[s + 1];
+                    v[NS - 1] = pend;
+                }
+                if (o == 31 || j == n - 1) {   // block complete: coalesced store of 32 outputs
+                    const int r = j - o + lane;
+                    if (lane <= o) dst[reversed ? n - 1 - r : r] = outv;
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0 && T + ring.nstage < 2 * ring.nst) {
+            fence_proxy_async();
+            ring.issue(T + ring.nstage);
+        }
+    }
+}
+
+template <int G, int NS>
+__global__ void __launch_bounds__(32) k_schur_local(SchurArgs a, int nstage) {
     extern __shared__ __align__(128) unsigned char smem[];
     if (a.state != nullptr && a.state->done) return;
     const int lane = threadIdx.x;
     const SubDesc d = a.sd[blockIdx.x];
     const int n = d.nI, nG = d.nG, B = a.band_w, ld = a.ld;
     const int mode = a.mode;
-    const int wmask = win - 1;
 
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
     double* stg = reinterpret_cast<double*>(smem + 128);
-    double* wn = stg + size_t(nstage) * G * ld;
-    double* xl = wn + win;
-    double* y = a.scratch + d.ioff;     // forward solution, then w
+    double* xl = stg + size_t(nstage) * G * ld;
 
-    Ring ring{bar, stg, nstage, G, ld, n, (n + G - 1) / G, a.band + d.band_off};
-    const int ntot = 2 * ring.nfw;
+    const double* Lb = a.band + d.band_off;
+    Ring ring{bar, stg, nstage, G, ld, n, (n + G - 1) / G, Lb, Lb + size_t(n) * ld};
     if (lane == 0) {
         for (int i = 0; i < nstage; ++i) mbar_init(bar + i, 1);
         fence_mbar_init();
-        for (int T = 0; T < min(nstage, ntot); ++T) ring.issue(T);
+        for (int T = 0; T < min(nstage, 2 * ring.nst); ++T) ring.issue(T);
     }
-    // gather x_s = R_s p (or u_Gamma) into shared memory
     if (mode != SCHUR_CONDENSE)
         for (int l = lane; l < nG; l += 32) xl[l] = a.xin[a.Rg[d.goff + l]];
     __syncwarp();
-
     const int32_t* igp = a.igp + d.igp_off;
     const int32_t* idofs = a.idofs + d.ioff;
-    auto rhs = [&](int r) -> double {
+    double* y = a.scratch + d.ioff;
+    for (int r = lane; r < n; r += 32) {          // dense interior right-hand side
         double v = (mode == SCHUR_APPLY) ? 0.0 : a.f[idofs[r]];
         if (mode != SCHUR_CONDENSE) {
             double acc = 0.0;
             for (int e = igp[r]; e < igp[r + 1]; ++e) acc += a.ig_val[e] * xl[a.ig_col[e]];
             v = (mode == SCHUR_APPLY) ? acc : v - acc;
         }
-        return v;
-    };
-
-    // ------------------------------------------------------------------ forward sweep
-    for (int r = lane; r <= B && r < n; r += 32) wn[r & wmask] = rhs(r);
-    // rows entering at stage t are c0+B+1 .. c0+B+nc; prefetch them one stage ahead
-    double pend = 0.0;
-    if (lane < G) {
-        const int r = B + 1 + lane;
-        if (r < n) pend = rhs(r);
+        y[r] = v;
     }
     __syncwarp();
     int T = 0;
-    for (int t = 0; t < ring.nfw; ++t, ++T) {
-        const double* S = ring.wait(T);
-        const int c0 = t * G, nc = min(G, n - c0);
-        if (lane < nc) {
-            const int r = c0 + B + 1 + lane;
-            if (r < n) wn[r & wmask] = pend;
-        }
-        if (lane < G) {
-            const int r = c0 + G + B + 1 + lane;
-            pend = (r < n) ? rhs(r) : 0.0;
-        }
-        __syncwarp();
-        for (int cc = 0; cc < nc; ++cc) {
-            const int j = c0 + cc;
-            const double* col = S + cc * ld;
-            const double yj = wn[j & wmask] * col[0];
-            for (int k = lane + 1; k <= B; k += 32) wn[(j + k) & wmask] -= col[k] * yj;
-            if (lane == 0) y[j] = yj;
-            __syncwarp();
-        }
-        if (lane == 0 && T + nstage < ntot) {
-            fence_proxy_async();
-            ring.issue(T + nstage);
-        }
-        __syncwarp();
-    }
-    // ------------------------------------------------------------------ backward sweep
-    constexpr int LPC = 32 / G;             // lanes per column in a block
-    const int cc_me = lane / LPC, part = lane % LPC;
-    double* xw = wn;                        // window of solved x values (rows above the block)
-    for (int u = 0; u < ring.nfw; ++u, ++T) {
-        const double* S = ring.wait(T);
-        const int hi = n - u * G, c_lo = max(0, hi - G), nc = hi - c_lo;
-        double tv = 0.0;
-        const double* colme = S + cc_me * ld;
-        if (cc_me < nc) {
-            const int j = c_lo + cc_me;
-            for (int dd = (hi - j) + part; dd <= B && j + dd < n; dd += LPC) tv += colme[dd] * xw[(j + dd) & wmask];
-        }
-#pragma unroll
-        for (int o = LPC / 2; o > 0; o >>= 1) tv += __shfl_xor_sync(0xffffffffu, tv, o);
-        if (cc_me < nc) tv = y[c_lo + cc_me] - tv;
-        for (int cj = nc - 1; cj >= 0; --cj) {
-            const double mine = tv * colme[0];
-            const double xj = __shfl_sync(0xffffffffu, mine, cj * LPC);
-            if (cc_me < cj) tv -= colme[cj - cc_me] * xj;
-            if (lane == 0) {
-                xw[(c_lo + cj) & wmask] = xj;
-                y[c_lo + cj] = xj;
-            }
-        }
-        __syncwarp();
-        if (lane == 0 && T + nstage < ntot) {
-            fence_proxy_async();
-            ring.issue(T + nstage);
-        }
-        __syncwarp();
-    }
-    // ------------------------------------------------------------------ outputs
+    sweep<G, NS>(ring, y, y, false, T, lane, B, n);   // y = L^-1 rhs
+    __syncwarp();
+    sweep<G, NS>(ring, y, y, true, T, lane, B, n);    // w = L^-T y  (M^-1 on reversed vectors)
+    __syncwarp();
+    const double* w = y;
     if (mode == SCHUR_BACKSUB) {
-        for (int i = lane; i < n; i += 32) a.u[idofs[i]] = y[i];
+        for (int i = lane; i < n; i += 32) a.u[idofs[i]] = w[i];
         return;
     }
     const int32_t* gxp = a.gxp + d.gxp_off;
     for (int l = lane; l < nG; l += 32) {
         double q = 0.0;
         for (int e = gxp[l]; e < gxp[l + 1]; ++e) {
-            const int c = a.gx_col[e];
-            if (c >= 0) {
-                if (mode == SCHUR_APPLY) q += a.gx_val[e] * xl[c];
+            const int cidx = a.gx_col[e];
+            if (cidx >= 0) {
+                if (mode == SCHUR_APPLY) q += a.gx_val[e] * xl[cidx];
             } else {
-                q -= a.gx_val[e] * y[-c - 1];
+                q -= a.gx_val[e] * w[-cidx - 1];
             }
         }
         a.qloc[d.goff + l] = q;
     }
 }
 
-int launch_schur_local(const SchurArgs& a, cudaStream_t st) {
-    if (a.nsl == 0) return 0;
-    const int G = a.band_w <= 127 ? 8 : 4;
-    int win = 32;
-    while (win < a.band_w + 1 + G + 1) win <<= 1;
-    const int nstage = 3;
-    const size_t smem = 128 + sizeof(double) * (size_t(nstage) * G * a.ld + win + a.maxG);
+template <int G, int NS>
+static void launch_t(const SchurArgs& a, int nstage, size_t smem, cudaStream_t st) {
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     cudaStreamIsCapturing(st, &cs);
-    const bool set_attr = (cs == cudaStreamCaptureStatusNone) && smem > 48 * 1024;
-    if (G == 8) {
-        if (set_attr) cudaFuncSetAttribute(k_schur_local<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        k_schur_local<8><<<a.nsl, 32, smem, st>>>(a, nstage, win);
-    } else {
-        if (set_attr) cudaFuncSetAttribute(k_schur_local<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        k_schur_local<4><<<a.nsl, 32, smem, st>>>(a, nstage, win);
+    if (cs == cudaStreamCaptureStatusNone) {
+        cudaFuncSetAttribute(k_schur_local<G, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        cudaFuncSetAttribute(k_schur_local<G, NS>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             cudaSharedmemCarveoutMaxShared);
     }
+    k_schur_local<G, NS><<<a.nsl, 32, smem, st>>>(a, nstage);
+}
+
+int launch_schur_local(const SchurArgs& a, cudaStream_t st) {
+    if (a.nsl == 0) return 0;
+    const int need = (a.band_w + 1 + 31) / 32;   // register slots per lane covering b+1 rows
+    const int G = 4, nstage = 4;
+    const size_t smem = 128 + sizeof(double) * (size_t(nstage) * G * a.ld + a.maxG);
+    if (need <= 1) launch_t<4, 1>(a, nstage, smem, st);
+    else if (need <= 2) launch_t<4, 2>(a, nstage, smem, st);
+    else if (need <= 3) launch_t<4, 3>(a, nstage, smem, st);
+    else if (need <= 4) launch_t<4, 4>(a, nstage, smem, st);
+    else if (need <= 8) launch_t<4, 8>(a, nstage, smem, st);
+    else if (need <= 12) launch_t<4, 12>(a, nstage, smem, st);
+    else if (need <= 16) launch_t<4, 16>(a, nstage, smem, st);
+    else if (need <= 20) launch_t<4, 20>(a, nstage, smem, st);
+    else return -1;
     return 1;
 }
 
