@@ -89,6 +89,8 @@ typedef struct {
     int32_t use_graph;       /* 1 (default): capture check_every PCG iterations into a CUDA graph */
     int32_t host_only;       /* 1: run only the host setup (topology, DOF map, skeleton queries);
                                 no device is touched and de_factor/de_solve return DE_ESTATE */
+    int32_t prec_kernels;    /* 0 (default): one persistent cooperative kernel per preconditioner
+                                application; 1: one kernel per phase (same arithmetic) */
 } de_options_t;
 
 typedef struct {

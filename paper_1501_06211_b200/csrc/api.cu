@@ -100,6 +100,8 @@ struct de_ctx {
     int* d_fail = nullptr;
     PrecDev P{};
     bool have_prec = false;
+    CoopBuffers coop{};
+    bool use_coop = false;
     bool factored = false, have_prev = false;
     // graph
     cudaGraphExec_t gexec = nullptr;
@@ -201,7 +203,13 @@ de_status_t schur_apply(de_ctx* c, const double* x, double* q) {
 }
 
 de_status_t precond(de_ctx* c, const double* r, double* z, const PcgState* s, int* nl) {
-    if (c->have_prec) {
+    if (c->have_prec && c->use_coop) {
+        if (prec_apply_coop(c->P, c->coop, r, z, s, c->st) < 0) {
+            set_error("cooperative preconditioner launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+            return DE_ECUDA;
+        }
+        if (nl) *nl = 1;
+    } else if (c->have_prec) {
         prec_apply(c->P, r, z, s, c->st, nl);
     } else {
         launch_copy(z, r, c->hs.n_G, s, c->st);
@@ -214,9 +222,9 @@ de_status_t precond(de_ctx* c, const double* r, double* z, const PcgState* s, in
 de_status_t pcg_iteration(de_ctx* c, int* nl, cudaEvent_t e0, cudaEvent_t e1) {
     const int64_t nG = c->hs.n_G;
     int n = 0;
-    if (e0) cudaEventRecord(e0, c->st);
+    if (e0) cudaEventRecordWithFlags(e0, c->st, cudaEventRecordExternal);   // a real node when captured
     launch_schur_local(schur_args(c, SCHUR_APPLY, c->d_p, nullptr, nullptr, c->d_state), c->st);
-    if (e1) cudaEventRecord(e1, c->st);
+    if (e1) cudaEventRecordWithFlags(e1, c->st, cudaEventRecordExternal);
     launch_gather(c->d_gptr, c->d_gsrc, c->d_qloc, nullptr, c->d_q, nG, c->d_state, c->st);
     n += 2;
     TRY(allreduce(c, c->d_q, size_t(nG)));
@@ -316,6 +324,9 @@ de_status_t upload_prec(de_ctx* c) {
     for (int i = 0; i <= MAXC; ++i) P.comp_off[i] = hs.comp_off[std::min(i, hs.ncomp)];
     for (int i = 0; i < MAXC; ++i) P.singular[i] = (hs.singular_mask >> i) & 1;
     P.theta = c->opt.theta;
+    P.max_face_band = 0;
+    for (const HElim* E : {&hs.elimK, &hs.elimM})
+        for (int F = 0; F < E->nfaces; ++F) P.max_face_band = std::max(P.max_face_band, E->face_band[F]);
     TRY(dupload(c, &P.cmap, hs.cmap));
     auto up_csr = [&](const HCsr& A, CsrDev& D) -> de_status_t {
         D.n = A.n;
@@ -369,6 +380,47 @@ de_status_t upload_prec(de_ctx* c) {
             const int nc = E.cross_comp_off[cc + 1] - E.cross_comp_off[cc];
             if (nc > 0) launch_gauss_jordan(D.Sinv + E.sc_off[cc], gjbuf, nc, c->st);
         }
+        // face-interleaved tridiagonal copy (2D faces are paths): coalesced thread-per-face solves
+        D.tri = 1;
+        for (int F = 0; F < E.nfaces && D.tri; ++F) {
+            const int o = E.face_off[F], n = E.face_off[F + 1] - o;
+            int nx = 0;
+            for (int i = 0; i < n; ++i) nx += E.XFC.ptr[o + i + 1] - E.XFC.ptr[o + i];
+            if (E.face_band[F] > 1 || n > TRI_N || nx > 2) D.tri = 0;
+        }
+        if (D.tri && E.nfaces > 0) {
+            const int ng = (E.nfaces + 31) / 32;
+            std::vector<int32_t> tn(E.nfaces), tnode(size_t(ng) * TRI_N * 32, 0), txj(2 * E.nfaces, -1),
+                txc(2 * E.nfaces, 0);
+            std::vector<double> tinv(size_t(ng) * TRI_N * 32, 0.0), tsub(size_t(ng) * TRI_N * 32, 0.0),
+                txv(2 * E.nfaces, 0.0);
+            for (int F = 0; F < E.nfaces; ++F) {
+                const int o = E.face_off[F], n = E.face_off[F + 1] - o, ld = E.face_band[F] + 1;
+                const double* fac = &E.face_fac[E.face_fac_off[F]];
+                tn[F] = n;
+                const size_t g = F / 32, lane = F % 32;
+                for (int j = 0; j < n; ++j) {
+                    const size_t at = (g * TRI_N + j) * 32 + lane;
+                    tnode[at] = E.face_nodes[o + j];
+                    tinv[at] = fac[size_t(j) * ld];
+                    tsub[at] = ld > 1 ? fac[size_t(j) * ld + 1] : 0.0;
+                }
+                int k = 0;
+                for (int j = 0; j < n; ++j)
+                    for (int e = E.XFC.ptr[o + j]; e < E.XFC.ptr[o + j + 1]; ++e, ++k) {
+                        txj[2 * F + k] = j;
+                        txc[2 * F + k] = E.XFC.col[e];
+                        txv[2 * F + k] = E.XFC.val[e];
+                    }
+            }
+            TRY(dupload(c, &D.tri_n, tn));
+            TRY(dupload(c, &D.tri_node, tnode));
+            TRY(dupload(c, &D.tri_inv, tinv));
+            TRY(dupload(c, &D.tri_sub, tsub));
+            TRY(dupload(c, &D.tri_xj, txj));
+            TRY(dupload(c, &D.tri_xc, txc));
+            TRY(dupload(c, &D.tri_xv, txv));
+        }
         return check_launch();
     };
     TRY(up_elim(hs.elimK, P.eK));
@@ -396,6 +448,18 @@ de_status_t upload_prec(de_ctx* c) {
     DE_CUDA(cudaMemsetAsync(P.counter, 0, size_t(nslots) * sizeof(unsigned int), c->st));
     prec_prepare(P);
     c->have_prec = true;
+    if (c->opt.prec_kernels == 0 && prec_coop_prepare(P, c->opt.device, c->coop)) {
+        TRY(dalloc(c, &c->coop.red, prec_coop_red_doubles(c->coop)));
+        TRY(dalloc(c, &c->coop.gram, prec_coop_gram_doubles(c->coop)));
+        TRY(dalloc(c, &c->coop.gram_tot, prec_coop_gramtot_doubles()));
+        TRY(dalloc(c, &c->coop.w1, nf));
+        TRY(dalloc(c, &c->coop.mw1, nf));
+        if (getenv("DE_PREC_TIMERS")) {
+            TRY(dalloc(c, &c->coop.timers, 200 + 8192));
+            DE_CUDA(cudaMemsetAsync(c->coop.timers, 0, (200 + 8192) * sizeof(unsigned long long), c->st));
+        }
+        c->use_coop = true;
+    }
     return DE_OK;
 }
 
@@ -1045,6 +1109,13 @@ de_status_t de_set_profiling(de_ctx_t* c, int32_t on) {
     c->prof_ms = 0.0;
     c->prof_n = 0;
     return DE_OK;
+}
+
+// diagnostics: copy the cooperative preconditioner's phase stamps (ns) of the last application
+extern "C" int de_debug_prec_timers(const de_ctx_t* c, unsigned long long* out, int n) {
+    if (!c || !c->coop.timers || n > 200 + 8192) return -1;
+    cudaMemcpy(out, c->coop.timers, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost);
+    return 0;
 }
 
 de_status_t de_get_kernel_time(const de_ctx_t* c, double* ms, int64_t* launches) {

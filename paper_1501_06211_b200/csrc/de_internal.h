@@ -153,7 +153,17 @@ struct ElimDev {
     double* xfc_val;
     int64_t sc_off[MAXC + 1];
     double* Sinv;
+    // face-interleaved tridiagonal copy (2D): 32 faces per group, entry (j, lane) at (g*TRI_N + j)*32 + lane
+    int32_t tri;                 // 1 if every face block is tridiagonal with <= TRI_N nodes and <= 2 cross couplings
+    int32_t* tri_n;              // [nfaces] nodes per face
+    int32_t* tri_node;           // flat index of node j (or 0 past the end)
+    double* tri_inv;             // 1 / L_jj
+    double* tri_sub;             // L_{j+1,j}
+    int32_t* tri_xj;             // [2*nfaces] node index j of cross coupling k (or -1)
+    int32_t* tri_xc;             // [2*nfaces] cross index of coupling k
+    double* tri_xv;              // [2*nfaces] X_{F_j, c}
 };
+constexpr int TRI_N = 32;
 
 struct CsrDev {
     int32_t n;
@@ -241,6 +251,7 @@ void launch_zero_dirichlet(const int8_t* cls, double* u, int64_t ndof, cudaStrea
 // preconditioner
 struct PrecDev {
     int32_t ncomp, nflat, kmax;
+    int32_t max_face_band;      // max half bandwidth over all face blocks (1: tridiagonal, 2D)
     int64_t comp_off[MAXC + 1];
     int32_t singular[MAXC];
     double theta;
@@ -257,5 +268,20 @@ void prec_apply(const PrecDev& P, const double* r, double* z, const PcgState* s,
                 int* nlaunch);
 void launch_gauss_jordan(double* A, double* Bbuf, int n, cudaStream_t st);
 void prec_prepare(const PrecDev& P);   // one-time kernel attributes (outside graph capture)
+
+// persistent cooperative preconditioner (kernels_prec_coop.cu)
+struct CoopBuffers {
+    int nb = 0;
+    size_t smem = 0;
+    int stage = 0, per_warp = 0, mf = 0, ncmax = 0, nbc_max = 0, tridiag = 0;
+    double *red = nullptr, *gram = nullptr, *gram_tot = nullptr, *w1 = nullptr, *mw1 = nullptr;
+    unsigned long long* timers = nullptr;   // phase stamps (diagnostics; env DE_PREC_TIMERS=1)
+};
+bool prec_coop_prepare(const PrecDev& P, int device, CoopBuffers& B);
+size_t prec_coop_red_doubles(const CoopBuffers& B);
+size_t prec_coop_gram_doubles(const CoopBuffers& B);
+size_t prec_coop_gramtot_doubles();
+int prec_apply_coop(const PrecDev& P, const CoopBuffers& B, const double* r, double* z, const PcgState* s,
+                    cudaStream_t st);
 
 }  // namespace de

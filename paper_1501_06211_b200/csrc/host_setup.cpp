@@ -575,6 +575,10 @@ de_status_t host_setup(const de_mesh_t* mesh, const de_partition_t* part, double
     }
     hs.M = csr_from_trips(nflat, tM);
     hs.L = csr_from_trips(nflat, tL);
+    if (hs.M.ptr != hs.L.ptr || hs.M.col != hs.L.col) {   // the preconditioner fuses M and L SpMVs
+        set_error("internal: trace M and L sparsity patterns differ");
+        return DE_EINVAL;
+    }
     {   // K_c = L_c, or L_c + M_c for singular components
         std::vector<Trip> tK;
         for (int32_t r = 0; r < nflat; ++r) {

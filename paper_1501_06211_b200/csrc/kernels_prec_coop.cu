@@ -1,0 +1,892 @@
+// kernels_prec_coop.cu — the interface preconditioner z = H^_theta^-1 r as ONE
+// persistent cooperative kernel per application: the same algorithm as kernels_precond.cu
+// (R7, R9, R10), but ~60 grid-wide barriers
+// instead of ~110 kernel launches.
+//
+// Work distribution: block b serves component c = b % ncomp for row-parallel phases (rows
+// lo_c + lb*CT + tid, stride nbc*CT); face solves are warp-per-face over all components; the cross-
+// point GEMV is split over the component's blocks. Every scalar (norms, Gram-Schmidt coefficients)
+// is a fixed-order sum of per-block partials that EVERY block recomputes after the barrier, so all
+// blocks hold bitwise identical copies and no extra barrier is needed to broadcast them.
+// Per Lanczos step: exact K-solve (3 barriers) + M w & dots (1) + CGS pass 1 with M(w - W h) formed
+// on the fly (1) + CGS pass 2 and ||w||_M (1).
+#include "de_internal.h"
+
+#include <cooperative_groups.h>
+
+namespace cg = cooperative_groups;
+
+namespace de {
+
+constexpr int CT = 256;
+constexpr int CW = CT / 32;
+constexpr int NRED = KMAX + 2;
+constexpr int RW = CT - 32;                   // rows per block chunk in row-parallel phases
+constexpr int GTR = RW / 2;                   // Gram tile rows (divides RW)
+constexpr int GRAM_TASKS = KMAX * (2 * KMAX + 1);
+
+struct CoopArgs {
+    PrecDev P;
+    const double* r;
+    double* z;
+    const PcgState* s;
+    double* red;        // [2][MAXC][NRED][nbc_max]
+    double* gram;       // [MAXC][GRAM_TASKS][nbc_max]
+    double* gram_tot;   // [MAXC][GRAM_TASKS]
+    double* w1;         // second Lanczos work vector (nflat)
+    double* mw1;        // scratch (nflat)
+    int nbc_max;
+    int stage;          // 1: stage face factors in shared memory
+    int per_warp;       // doubles of shared memory per warp for face solves
+    int mf;             // max face size
+    int ncmax;          // max cross points per component
+    int tridiag;        // 1: every face block is tridiagonal with <= TRI_MAX nodes (2D) -> thread per face
+    unsigned long long* timers;   // optional phase timestamps (block 0), DE_PREC_TIMERS
+};
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define STAMP(k)                                                        \
+    do {                                                                \
+        if (a.timers && blockIdx.x == 0 && threadIdx.x == 0) a.timers[k] = gtimer(); \
+    } while (0)
+
+__device__ __forceinline__ int ccomp(const int64_t* off, int nc, int64_t i) {
+    int c = 0;
+    while (c + 1 < nc && i >= off[c + 1]) ++c;
+    return c;
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// block-reduce vals[0..nv) and write this block's partials into red[pp][c][v][lb]
+__device__ void block_partials(const CoopArgs& a, const double (&vals)[NRED], int nv, int pp, int c, int lb,
+                               double (*sred)[NRED]) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int v = 0; v < NRED; ++v) {
+        if (v < nv) {
+            const double t = warp_sum(vals[v]);
+            if (lane == 0) sred[w][v] = t;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < nv) {
+        double t = 0.0;
+        for (int k = 0; k < CW; ++k) t += sred[k][threadIdx.x];
+        a.red[((size_t(pp) * MAXC + c) * NRED + threadIdx.x) * a.nbc_max + lb] = t;
+    }
+    __syncthreads();
+}
+
+// totals of all components (fixed order over lb) into tot[c][v]
+__device__ void read_totals(const CoopArgs& a, int pp, int nv, int nb, double (*tot)[NRED]) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int nc = a.P.ncomp;
+    for (int t = w; t < nc * nv; t += CW) {
+        const int c = t / nv, v = t - c * nv;
+        const int nbc = (nb - c + nc - 1) / nc;
+        const double* p = a.red + ((size_t(pp) * MAXC + c) * NRED + v) * a.nbc_max;
+        double acc = 0.0;
+        for (int b = lane; b < nbc; b += 32) acc += *((volatile const double*)(p + b));
+        acc = warp_sum(acc);
+        if (lane == 0) tot[c][v] = acc;
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ double spmv_row(const CsrDev& A, int64_t i, const double* __restrict__ x) {
+    double acc = 0.0;
+    for (int e = A.ptr[i]; e < A.ptr[i + 1]; ++e) acc += A.val[e] * x[A.col[e]];
+    return acc;
+}
+
+// y_M = sum_e M_ie v_e and (optionally) y_L = sum_e L_ie v_e with v = x - sum_{t<nt} h_t W_t (M and L share
+// one sparsity pattern: both are assembled on the same trace facets). The basis loop is unrolled to KMAX
+// with predication so every load of a row is issued before the first use (latency-bound otherwise).
+template <bool WITH_L>
+__device__ __forceinline__ void corr_spmv(const CsrDev& M, const CsrDev& L, int64_t i, const double* __restrict__ x,
+                                          const double* __restrict__ W, int64_t nflat, const double* h, int nt,
+                                          double& yM, double& yL) {
+    const int e0 = M.ptr[i], e1 = M.ptr[i + 1];
+    double am = 0.0, al = 0.0;
+    for (int e = e0; e < e1; ++e) {
+        const int col = M.col[e];
+        const double mv = M.val[e];
+        const double lv = WITH_L ? L.val[e] : 0.0;
+        double w[KMAX];
+#pragma unroll
+        for (int t = 0; t < KMAX; ++t) w[t] = t < nt ? W[size_t(t) * nflat + col] : 0.0;
+        double v = x[col];
+#pragma unroll
+        for (int t = 0; t < KMAX; ++t) v -= h[t] * w[t];
+        am += mv * v;
+        if (WITH_L) al += lv * v;
+    }
+    yM = am;
+    yL = al;
+}
+
+// sum_t h_t W_t[i] with all loads issued up front
+__device__ __forceinline__ double basis_comb(const double* __restrict__ W, int64_t nflat, int64_t i, const double* h,
+                                             int nt) {
+    double w[KMAX];
+#pragma unroll
+    for (int t = 0; t < KMAX; ++t) w[t] = t < nt ? W[size_t(t) * nflat + i] : 0.0;
+    double acc = 0.0;
+#pragma unroll
+    for (int t = 0; t < KMAX; ++t) acc += h[t] * w[t];
+    return acc;
+}
+
+// Warp solve of one face block (L then M = P L^T P forward sweeps, b <= 31, row window in registers).
+// rhs = scale * b_F (mode 0) or scale * b_F - X_FC xC (mode 1).
+__device__ void face_warp(const CoopArgs& a, const ElimDev& E, int F, const double* __restrict__ b,
+                          const double* scl, const double* __restrict__ xC, double* __restrict__ out, int mode,
+                          double* wsm, int lane) {
+    __syncwarp();
+    const PrecDev& P = a.P;
+    const int o = E.face_off[F], n = E.face_off[F + 1] - o, bw = E.face_band[F], ld = bw + 1;
+    double* rb = wsm;
+    double* ys = wsm + a.mf;
+    int* idx = reinterpret_cast<int*>(wsm + 2 * a.mf);
+    const double* gf = E.face_fac + E.face_fac_off[F];
+    const double* fac0 = gf;
+    if (a.stage) {
+        double* fs = wsm + 3 * a.mf;
+        for (int i = lane; i < 2 * n * ld; i += 32) fs[i] = gf[i];
+        fac0 = fs;
+    }
+    const double sc = scl[ccomp(P.comp_off, P.ncomp, E.face_nodes[o])];
+    for (int i = lane; i < n; i += 32) {
+        const int node = E.face_nodes[o + i];
+        idx[i] = node;
+        double r = sc * b[node];
+        if (mode == 1)
+            for (int e = E.xfc_ptr[o + i]; e < E.xfc_ptr[o + i + 1]; ++e) r -= E.xfc_val[e] * xC[E.xfc_col[e]];
+        rb[i] = r;
+    }
+    __syncwarp();
+    for (int sw = 0; sw < 2; ++sw) {
+        const double* __restrict__ fac = fac0 + (sw == 0 ? 0 : size_t(n) * ld);
+        const double* __restrict__ src = sw == 0 ? rb : ys;
+        double* dst = sw == 0 ? ys : rb;          // both in shared memory; y reversed, then x reversed back
+        double v = lane < n ? src[lane] : 0.0;
+        double outv = 0.0;                        // lane l keeps the solution of rows = l (mod 32)
+        __syncwarp();
+        for (int j0 = 0; j0 < n; j0 += 32) {      // 32-row blocks: the loop body has loads only
+            const int jn = min(32, n - j0);
+#pragma unroll 4
+            for (int jj = 0; jj < jn; ++jj) {
+                const int j = j0 + jj;
+                const double* col = fac + size_t(j) * ld;
+                const double cl = (lane >= 1 && lane <= bw) ? col[lane] : 0.0;
+                const double nxt = (j + 32 < n) ? src[j + 32] : 0.0;   // row entering lane 31 (uniform load)
+                const double yj = __shfl_sync(0xffffffffu, v, 0) * col[0];
+                v = fma(-cl, yj, v);
+                const double vs = __shfl_down_sync(0xffffffffu, v, 1);
+                v = (lane == 31) ? nxt : vs;                           // branch-free: keeps the warp converged
+                outv = (lane == jj) ? yj : outv;
+            }
+            __syncwarp();
+            if (lane < jn) dst[n - 1 - (j0 + lane)] = outv;            // flush this block's solutions
+            __syncwarp();
+        }
+    }
+    for (int i = lane; i < n; i += 32) out[idx[i]] = rb[i];
+    __syncwarp();
+}
+
+// Thread solve of one tridiagonal face block (2D: every face is a path of <= 64 trace nodes):
+// forward y_j = (r_j - L_{j,j-1} y_{j-1}) / L_jj, backward x_j = (y_j - L_{j+1,j} x_{j+1}) / L_jj.
+// The face data is interleaved over groups of 32 faces (ElimDev::tri_*), so lane l of a warp reads
+// entry j of face 32g+l with one coalesced access per step; the 2*n-step recurrence stays in registers.
+__device__ void face_thread_tridiag(const CoopArgs& a, const ElimDev& E, int F, const double* __restrict__ b,
+                                    const double* scl, const double* __restrict__ xC, double* __restrict__ out,
+                                    int mode, double* ysm) {
+    const PrecDev& P = a.P;
+    const int n = E.tri_n[F];
+    const size_t base = size_t(F / 32) * TRI_N * 32 + (F % 32);
+    const double sc = scl[ccomp(P.comp_off, P.ncomp, E.tri_node[base])];
+    int xj0 = -1, xj1 = -1;
+    double xr0 = 0.0, xr1 = 0.0;
+    if (mode == 1) {
+        xj0 = E.tri_xj[2 * F];
+        xj1 = E.tri_xj[2 * F + 1];
+        if (xj0 >= 0) xr0 = E.tri_xv[2 * F] * xC[E.tri_xc[2 * F]];
+        if (xj1 >= 0) xr1 = E.tri_xv[2 * F + 1] * xC[E.tri_xc[2 * F + 1]];
+    }
+    constexpr int U = 8;                            // rows per chunk: all loads of a chunk in flight together
+    double prev = 0.0, lprev = 0.0;
+    for (int j0 = 0; j0 < n; j0 += U) {
+        double r[U], inv[U], sub[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int j = j0 + u;
+            r[u] = 0.0;
+            inv[u] = 0.0;
+            sub[u] = 0.0;
+            if (j < n) {
+                const size_t at = base + size_t(j) * 32;
+                r[u] = sc * b[E.tri_node[at]] - (j == xj0 ? xr0 : 0.0) - (j == xj1 ? xr1 : 0.0);
+                inv[u] = E.tri_inv[at];
+                sub[u] = E.tri_sub[at];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (j0 + u < n) {
+                prev = (r[u] - lprev * prev) * inv[u];
+                ysm[(j0 + u) * RW] = prev;
+                lprev = sub[u];
+            }
+        }
+    }
+    double nxt = 0.0;
+    for (int j1 = n - 1; j1 >= 0; j1 -= U) {
+        double inv[U], sub[U];
+        int node[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int j = j1 - u;
+            inv[u] = 0.0;
+            sub[u] = 0.0;
+            node[u] = 0;
+            if (j >= 0) {
+                const size_t at = base + size_t(j) * 32;
+                inv[u] = E.tri_inv[at];
+                sub[u] = E.tri_sub[at];
+                node[u] = E.tri_node[at];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int j = j1 - u;
+            if (j >= 0) {
+                nxt = (ysm[j * RW] - sub[u] * nxt) * inv[u];
+                out[node[u]] = nxt;
+            }
+        }
+    }
+}
+
+// x = X^-1 (scl * b) by exact elimination (faces -> cross points -> faces); 3 grid barriers.
+__device__ void elim_coop(cg::grid_group& grid, const CoopArgs& a, const ElimDev& E, const double* b,
+                          const double* scl, double* out, double* dsm, int c, int lb, int nbc, int& stamp) {
+    const PrecDev& P = a.P;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    // warp 0 hosts the grid-barrier thread; it comes out of every barrier late, so face solves run
+    // on warps 1..CW-1 only (measured: warp 0 otherwise sets the phase time)
+    const int gw = blockIdx.x * (CW - 1) + (w - 1), nwarps = gridDim.x * (CW - 1);
+    const int gt = blockIdx.x * RW + (threadIdx.x - 32), nthr = gridDim.x * RW;
+    double* y = P.y;
+    double* xC = P.y + P.nflat;
+    double* wsm = dsm + size_t(w) * a.per_warp;
+    long long tf0 = clock64();
+    if (E.tri) {
+        if (w > 0)
+            for (int F = gt; F < E.nfaces; F += nthr) face_thread_tridiag(a, E, F, b, scl, nullptr, y, 0, dsm + (threadIdx.x - 32));
+    } else if (w > 0)
+        for (int F = gw; F < E.nfaces; F += nwarps) face_warp(a, E, F, b, scl, nullptr, y, 0, wsm, lane);
+    if (a.timers && lane == 0 && w > 0 && gw < 4096) a.timers[200 + gw] = clock64() - tf0;
+    grid.sync();
+    __syncwarp();   // lane 0 spun in the barrier: reconverge before warp-synchronous code
+    STAMP(stamp++);
+    // cross points of this block's component: t_C = scl*b_C - X_CF y in smem, then rows of S_C^-1 t_C
+    {
+        const int base = E.cross_comp_off[c], ncc = E.cross_comp_off[c + 1] - base;
+        if (ncc > 0) {
+            double* tC = dsm;
+            for (int i = threadIdx.x; i < ncc; i += CT) {
+                const int ci = base + i;
+                double t = scl[c] * b[E.cross_flat[ci]];
+                for (int e = E.xcf_ptr[ci]; e < E.xcf_ptr[ci + 1]; ++e) t -= E.xcf_val[e] * y[E.xcf_col[e]];
+                tC[i] = t;
+            }
+            __syncthreads();
+            const double* S = E.Sinv + E.sc_off[c];
+            for (int rr = lb * CW + w; rr < ncc; rr += nbc * CW) {
+                const double* __restrict__ row = S + size_t(rr) * ncc;
+                double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;   // independent chains: 4 loads in flight
+                int j = lane;
+                for (; j + 96 < ncc; j += 128) {
+                    a0 += row[j] * tC[j];
+                    a1 += row[j + 32] * tC[j + 32];
+                    a2 += row[j + 64] * tC[j + 64];
+                    a3 += row[j + 96] * tC[j + 96];
+                }
+                for (; j < ncc; j += 32) a0 += row[j] * tC[j];
+                double acc = warp_sum((a0 + a1) + (a2 + a3));
+                if (lane == 0) {
+                    xC[base + rr] = acc;
+                    out[E.cross_flat[base + rr]] = acc;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    grid.sync();
+    __syncwarp();   // lane 0 spun in the barrier: reconverge before warp-synchronous code
+    STAMP(stamp++);
+    tf0 = clock64();
+    if (E.tri) {
+        if (w > 0)
+            for (int F = gt; F < E.nfaces; F += nthr) face_thread_tridiag(a, E, F, b, scl, xC, out, 1, dsm + (threadIdx.x - 32));
+    } else if (w > 0)
+        for (int F = gw; F < E.nfaces; F += nwarps) face_warp(a, E, F, b, scl, xC, out, 1, wsm, lane);
+    if (a.timers && lane == 0 && w > 0 && gw < 4096) a.timers[200 + 4096 + gw] = clock64() - tf0;
+    grid.sync();
+    __syncwarp();   // lane 0 spun in the barrier: reconverge before warp-synchronous code
+    STAMP(stamp++);
+}
+
+// One warp: generalized eigenproblem A y = theta B y (n <= KMAX) and coef = Y f(Theta) Y^T wr.
+// Returns false on a non-SPD B or a non-positive Ritz value (non-singular component).
+__device__ bool ritz_warp(const double* Ain, const double* Bin, const double* wr, int n, bool sing, double theta,
+                          double* coef, double* R, double* C, double* V, double* X, double* rot, int* rpq,
+                          unsigned long long* tm = nullptr) {
+    const int lane = threadIdx.x & 31;
+    if (tm && lane == 0) tm[0] = gtimer();
+    constexpr int LDK = KMAX + 1;
+    for (int idx = lane; idx < n * n; idx += 32) {
+        const int i = idx / n, j = idx - i * n;
+        C[i * LDK + j] = 0.5 * (Ain[i * KMAX + j] + Ain[j * KMAX + i]);
+        R[i * LDK + j] = 0.5 * (Bin[i * KMAX + j] + Bin[j * KMAX + i]);
+        V[i * LDK + j] = (i == j) ? 1.0 : 0.0;
+    }
+    __syncwarp();
+    for (int j = 0; j < n; ++j) {
+        const double d = R[j * LDK + j];
+        if (!(d > 0.0)) return false;
+        const double l = sqrt(d);
+        __syncwarp();
+        if (lane == 0) R[j * LDK + j] = l;
+        if (lane > j && lane < n) R[lane * LDK + j] /= l;
+        __syncwarp();
+        for (int idx = lane; idx < (n - j - 1) * (n - j - 1); idx += 32) {
+            const int i = j + 1 + idx / (n - j - 1), kk = j + 1 + idx % (n - j - 1);
+            if (kk <= i) R[i * LDK + kk] -= R[i * LDK + j] * R[kk * LDK + j];
+        }
+        __syncwarp();
+    }
+    if (lane < n)
+        for (int i = 0; i < n; ++i) {
+            double t = C[i * LDK + lane];
+            for (int kk = 0; kk < i; ++kk) t -= R[i * LDK + kk] * X[kk * LDK + lane];
+            X[i * LDK + lane] = t / R[i * LDK + i];
+        }
+    __syncwarp();
+    if (lane < n)
+        for (int i = 0; i < n; ++i) {
+            double t = X[lane * LDK + i];
+            for (int kk = 0; kk < i; ++kk) t -= C[lane * LDK + kk] * R[i * LDK + kk];
+            C[lane * LDK + i] = t / R[i * LDK + i];
+        }
+    __syncwarp();
+    for (int idx = lane; idx < n * n; idx += 32) {
+        const int i = idx / n, j = idx - i * n;
+        if (j > i) {
+            const double m = 0.5 * (C[i * LDK + j] + C[j * LDK + i]);
+            C[i * LDK + j] = m;
+            C[j * LDK + i] = m;
+        }
+    }
+    __syncwarp();
+    const int m = (n + 1) & ~1, npair = m / 2;
+    if (tm && lane == 0) tm[1] = gtimer();
+    int nsw = 0;
+    for (int sweep = 0; sweep < 30 && n > 1; ++sweep) {
+        ++nsw;
+        double off = 0.0, dia = 0.0;
+        if (lane < n)
+            for (int j = 0; j < n; ++j) {
+                const double v = C[lane * LDK + j];
+                if (j == lane) dia += v * v;
+                else off += v * v;
+            }
+        off = warp_sum(off);
+        dia = warp_sum(dia);
+        if (off <= 1e-30 * dia) break;
+        int rotated = 0;
+        for (int rnd = 0; rnd < m - 1; ++rnd) {
+            if (lane < npair) {
+                int p, q;
+                if (lane == 0) {
+                    p = m - 1;
+                    q = rnd;
+                } else {
+                    p = (rnd + lane) % (m - 1);
+                    q = (rnd - lane + (m - 1)) % (m - 1);
+                }
+                if (p > q) {
+                    const int t = p;
+                    p = q;
+                    q = t;
+                }
+                double cs = 1.0, sn = 0.0;
+                if (q < n) {
+                    const double apq = C[p * LDK + q];
+                    const double app = C[p * LDK + p], aqq = C[q * LDK + q];
+                    (void)app;
+                    (void)aqq;
+                    if (fabs(apq) > 1e-15 * sqrt(dia) && fabs(apq) > 1e-300) {   // else negligible vs ||C||
+                        rotated = 1;
+                        const double tau = (C[q * LDK + q] - C[p * LDK + p]) / (2.0 * apq);
+                        const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+                        cs = 1.0 / sqrt(1.0 + t * t);
+                        sn = t * cs;
+                    }
+                }
+                rot[lane] = cs;
+                rot[KMAX / 2 + lane] = sn;
+                rpq[lane] = p;
+                rpq[KMAX / 2 + lane] = q;
+            }
+            __syncwarp();
+            // the pairs of a round are disjoint: gather every operand first, then write (pipelined smem)
+            constexpr int NP = KMAX / 2;
+            int pp[NP], qq[NP];
+            double cs[NP], sn[NP];
+#pragma unroll
+            for (int t = 0; t < NP; ++t) {
+                const bool ok = t < npair;
+                pp[t] = ok ? rpq[t] : 0;
+                qq[t] = ok ? rpq[NP + t] : n;
+                cs[t] = ok ? rot[t] : 1.0;
+                sn[t] = ok ? rot[NP + t] : 0.0;
+            }
+            if (lane < n) {                                  // C <- C J and V <- V J (row `lane`)
+                double x0[NP], x1[NP], v0[NP], v1[NP];
+#pragma unroll
+                for (int t = 0; t < NP; ++t)
+                    if (qq[t] < n) {
+                        x0[t] = C[lane * LDK + pp[t]];
+                        x1[t] = C[lane * LDK + qq[t]];
+                        v0[t] = V[lane * LDK + pp[t]];
+                        v1[t] = V[lane * LDK + qq[t]];
+                    }
+#pragma unroll
+                for (int t = 0; t < NP; ++t)
+                    if (qq[t] < n) {
+                        C[lane * LDK + pp[t]] = cs[t] * x0[t] - sn[t] * x1[t];
+                        C[lane * LDK + qq[t]] = sn[t] * x0[t] + cs[t] * x1[t];
+                        V[lane * LDK + pp[t]] = cs[t] * v0[t] - sn[t] * v1[t];
+                        V[lane * LDK + qq[t]] = sn[t] * v0[t] + cs[t] * v1[t];
+                    }
+            }
+            __syncwarp();
+            if (lane < n) {                                  // C <- J^T C (column `lane`)
+                double x0[NP], x1[NP];
+#pragma unroll
+                for (int t = 0; t < NP; ++t)
+                    if (qq[t] < n) {
+                        x0[t] = C[pp[t] * LDK + lane];
+                        x1[t] = C[qq[t] * LDK + lane];
+                    }
+#pragma unroll
+                for (int t = 0; t < NP; ++t)
+                    if (qq[t] < n) {
+                        C[pp[t] * LDK + lane] = cs[t] * x0[t] - sn[t] * x1[t];
+                        C[qq[t] * LDK + lane] = sn[t] * x0[t] + cs[t] * x1[t];
+                    }
+            }
+            __syncwarp();
+        }
+        if (!__any_sync(0xffffffffu, rotated)) break;   // every pair below threshold: converged
+    }
+    if (tm && lane == 0) {
+        tm[2] = gtimer();
+        tm[4] = nsw;
+    }
+    int bad = 0;
+    double g = 0.0;
+    if (lane < n) {
+        const double th = C[lane * LDK + lane];
+        if (!sing && !(th > 0.0)) bad = 1;
+        const double f = sing ? 1.0 / (1.0 + pow(fmax(th, 0.0), 1.0 - theta)) : pow(th, theta - 1.0);
+        for (int i = n - 1; i >= 0; --i) {
+            double t = V[i * LDK + lane];
+            for (int kk = i + 1; kk < n; ++kk) t -= R[kk * LDK + i] * X[kk * LDK + lane];
+            X[i * LDK + lane] = t / R[i * LDK + i];
+        }
+        double t = 0.0;
+        for (int i = 0; i < n; ++i) t += X[i * LDK + lane] * wr[i];
+        g = f * t;
+    }
+    if (__any_sync(0xffffffffu, bad)) return false;
+    double cf = 0.0;                                        // coef_i = sum_e Y[i][e] g_e
+    for (int e = 0; e < n; ++e) {
+        const double ge = __shfl_sync(0xffffffffu, g, e);
+        if (lane < n) cf += X[lane * LDK + e] * ge;
+    }
+    if (lane < n) coef[lane] = cf;
+    if (tm && lane == 0) tm[3] = gtimer();
+    return true;
+}
+
+__global__ void __launch_bounds__(CT) k_prec_coop(CoopArgs a) {
+    cg::grid_group grid = cg::this_grid();
+    if (a.s != nullptr && a.s->done) return;
+    int stamp = 0;
+    STAMP(stamp++);
+    const PrecDev& P = a.P;
+    extern __shared__ double dsm[];
+    __shared__ double sred[CW][NRED];
+    __shared__ double tot[MAXC][NRED];
+    __shared__ double scl[MAXC], nrmv[MAXC], nb2v[MAXC];
+    __shared__ double hsm[MAXC][KMAX];
+    __shared__ int act[MAXC], kcs[MAXC], brk[MAXC];
+    const int tid = threadIdx.x;
+    const int nb = gridDim.x, nc = P.ncomp;
+    const int c = blockIdx.x % nc, lb = blockIdx.x / nc, nbc = (nb - c + nc - 1) / nc;
+    const int64_t lo = P.comp_off[c], hi = P.comp_off[c + 1];
+    // row-parallel phases run on warps 1..CW-1 (RW rows per block chunk); warp 0 hosts the grid-barrier
+    // thread and only joins the block reductions
+    const int64_t r0 = tid >= 32 ? lo + int64_t(lb) * RW + (tid - 32) : hi, rs = int64_t(nbc) * RW;
+    const int64_t nf = P.nflat;
+    int pp = 0;
+    double vals[NRED];
+#define ZERO_VALS()                                    \
+    _Pragma("unroll") for (int v_ = 0; v_ < NRED; ++v_) vals[v_] = 0.0
+
+    // ---- r_c gather and zero test
+    ZERO_VALS();
+    for (int64_t i = r0; i < hi; i += rs) {
+        const double x = a.r[P.cmap[i]];
+        P.rf[i] = x;
+        vals[0] += x * x;
+    }
+    block_partials(a, vals, 1, pp, c, lb, sred);
+    grid.sync();
+    __syncwarp();   // lane 0 spun in the barrier: reconverge before warp-synchronous code
+    STAMP(stamp++);
+    read_totals(a, pp, 1, nb, tot);
+    pp ^= 1;
+    if (tid < nc) {
+        act[tid] = tot[tid][0] > 0.0 ? 1 : 0;
+        kcs[tid] = 0;
+        brk[tid] = 0;
+        scl[tid] = 1.0;
+    }
+    __syncthreads();
+    // ---- s = M^-1 r (exact)
+    elim_coop(grid, a, P.eM, P.rf, scl, P.s, dsm, c, lb, nbc, stamp);
+    // ---- Ms, ||s||_M; q_1 = s / ||s||_M, rhs of the next solve v = M q_1 = Ms / ||s||_M
+    ZERO_VALS();
+    for (int64_t i = r0; i < hi; i += rs) {
+        const double m = spmv_row(P.M, i, P.s);
+        P.Mw[i] = m;
+        P.LW[i] = spmv_row(P.L, i, P.s);
+        vals[0] += P.s[i] * m;
+    }
+    block_partials(a, vals, 1, pp, c, lb, sred);
+    grid.sync();
+    __syncwarp();   // lane 0 spun in the barrier: reconverge before warp-synchronous code
+    STAMP(stamp++);
+    read_totals(a, pp, 1, nb, tot);
+    pp ^= 1;
+    if (tid < nc) {
+        nrmv[tid] = sqrt(tot[tid][0]);
+        if (act[tid]) kcs[tid] = 1;
+        scl[tid] = act[tid] ? 1.0 / nrmv[tid] : 0.0;
+    }
+    __syncthreads();
+    if (act[c])
+        for (int64_t i = r0; i < hi; i += rs) {     // q_1, L q_1, M q_1 (kept for Rayleigh-Ritz)
+            P.W[i] = P.s[i] * scl[c];
+            P.LW[i] *= scl[c];
+            P.MW[i] = P.Mw[i] * scl[c];
+        }
+    // ---- inverse Lanczos steps
+    for (int j = 1; j < P.kmax; ++j) {
+        elim_coop(grid, a, P.eK, P.Mw, scl, P.w, dsm, c, lb, nbc, stamp);   // w = K^-1 M q_j
+        const bool part = act[c] && !brk[c];
+        const int kc = kcs[c];
+        // A: Mw = M w; ||w||_M^2 and h_t = W_t . Mw
+        ZERO_VALS();
+        if (part)
+            for (int64_t i = r0; i < hi; i += rs) {
+                const double m = spmv_row(P.M, i, P.w);
+                vals[0] += P.w[i] * m;
+                double wt[KMAX];
+#pragma unroll
+                for (int t = 0; t < KMAX; ++t) wt[t] = t < kc ? P.W[size_t(t) * nf + i] : 0.0;
+#pragma unroll
+                for (int t = 0; t < KMAX; ++t) vals[1 + t] += wt[t] * m;
+            }
+        block_partials(a, vals, 1 + KMAX, pp, c, lb, sred);
+        grid.sync();
+    __syncwarp();   // lane 0 spun in the barrier: reconverge before warp-synchronous code
+    STAMP(stamp++);
+        read_totals(a, pp, 1 + kc, nb, tot);   // every component's first 1+kc (kc uniform enough: use own)
+        pp ^= 1;
+        if (tid < nc) nb2v[tid] = tot[tid][0];
+        if (tid < KMAX) hsm[c][tid] = tid < kc ? tot[c][1 + tid] : 0.0;
+        __syncthreads();
+        // B: w1 = w - W h;  dots h'_t = W_t . M(w - W h)
+        ZERO_VALS();
+        if (part)
+            for (int64_t i = r0; i < hi; i += rs) {
+                double wt[KMAX];
+#pragma unroll
+                for (int t = 0; t < KMAX; ++t) wt[t] = t < kc ? P.W[size_t(t) * nf + i] : 0.0;
+                double x = P.w[i];
+#pragma unroll
+                for (int t = 0; t < KMAX; ++t) x -= hsm[c][t] * wt[t];
+                a.w1[i] = x;
+                double m, unused;
+                corr_spmv<false>(P.M, P.L, i, P.w, P.W, nf, hsm[c], kc, m, unused);
+#pragma unroll
+                for (int t = 0; t < KMAX; ++t) vals[t] += wt[t] * m;
+            }
+        block_partials(a, vals, KMAX, pp, c, lb, sred);
+        grid.sync();
+    __syncwarp();   // lane 0 spun in the barrier: reconverge before warp-synchronous code
+    STAMP(stamp++);
+        read_totals(a, pp, kc > 0 ? kc : 1, nb, tot);
+        pp ^= 1;
+        if (tid < KMAX) hsm[c][tid] = tid < kc ? tot[c][tid] : 0.0;
+        __syncthreads();
+        // C: w2 = w1 - W h'; Mw2 = M w2 (kept for the next solve); ||w2||_M^2
+        const bool dbg = a.timers && blockIdx.x == 0 && tid == 32 && j == 5;
+        if (dbg) a.timers[110] = gtimer();
+        ZERO_VALS();
+        if (part)
+            for (int64_t i = r0; i < hi; i += rs) {
+                const double x = a.w1[i] - basis_comb(P.W, nf, i, hsm[c], kc);
+                double m, l;
+                corr_spmv<true>(P.M, P.L, i, a.w1, P.W, nf, hsm[c], kc, m, l);
+                P.w[i] = x;
+                P.Mw[i] = m;
+                P.LW[size_t(j) * nf + i] = l;
+                vals[0] += x * m;
+            }
+        if (dbg) a.timers[111] = gtimer();
+        block_partials(a, vals, 1, pp, c, lb, sred);
+        if (dbg) a.timers[112] = gtimer();
+        grid.sync();
+    __syncwarp();   // lane 0 spun in the barrier: reconverge before warp-synchronous code
+    STAMP(stamp++);
+        if (dbg) a.timers[113] = gtimer();
+        read_totals(a, pp, 1, nb, tot);
+        if (dbg) a.timers[114] = gtimer();
+        pp ^= 1;
+        if (tid < nc) {
+            const bool pt = act[tid] && !brk[tid];
+            const double na = sqrt(fmax(tot[tid][0], 0.0)), nbn = sqrt(fmax(nb2v[tid], 0.0));
+            if (pt) {
+                if (na > 1e-12 * nbn) {
+                    kcs[tid] = j + 1;
+                    scl[tid] = 1.0 / na;
+                } else {
+                    brk[tid] = 1;
+                    scl[tid] = 0.0;
+                }
+            } else {
+                scl[tid] = 0.0;
+            }
+        }
+        __syncthreads();
+        if (part && kcs[c] == j + 1)
+            for (int64_t i = r0; i < hi; i += rs) {
+                P.W[size_t(j) * nf + i] = P.w[i] * scl[c];
+                P.LW[size_t(j) * nf + i] *= scl[c];
+                P.MW[size_t(j) * nf + i] = P.Mw[i] * scl[c];
+            }
+    }
+    grid.sync();
+    __syncwarp();   // lane 0 spun in the barrier: reconverge before warp-synchronous code
+    STAMP(stamp++);   // last basis vector visible everywhere
+    // ---- Rayleigh-Ritz Gram products over own rows, tiles of GTR contiguous rows
+    {
+        const int k = kcs[c], nz = 2 * k + 1, nv = k + nz, ntk = k * nz;
+        double* tile = dsm;   // nv x (GTR+1)
+        double g0 = 0.0, g1 = 0.0;
+        if (act[c]) {
+            for (int64_t base = lo + int64_t(lb) * RW; base < hi; base += rs)
+                for (int q = 0; q < RW / GTR; ++q) {
+                    const int64_t rb0 = base + q * GTR;
+                    if (rb0 >= hi) break;
+                    for (int t = tid; t < nv * GTR; t += CT) {
+                        const int v = t / GTR, rr = t - v * GTR;
+                        const int64_t i = rb0 + rr;
+                        double val = 0.0;
+                        if (i < hi) {
+                            if (v < k) val = P.W[size_t(v) * nf + i];
+                            else if (v < 2 * k) val = P.LW[size_t(v - k) * nf + i];
+                            else if (v < 3 * k) val = P.MW[size_t(v - 2 * k) * nf + i];
+                            else val = P.rf[i];
+                        }
+                        tile[v * (GTR + 1) + rr] = val;
+                    }
+                    __syncthreads();
+                    for (int t = tid, h = 0; t < ntk; t += CT, ++h) {
+                        const int ii = t / nz, jz = t - ii * nz;
+                        const double* pa = tile + ii * (GTR + 1);
+                        const double* pb = tile + (k + jz) * (GTR + 1);
+                        double acc = 0.0;
+#pragma unroll 8
+                        for (int rr = 0; rr < GTR; ++rr) acc += pa[rr] * pb[rr];
+                        if (h == 0) g0 += acc;
+                        else g1 += acc;
+                    }
+                    __syncthreads();
+                }
+        }
+        for (int t = tid, h = 0; t < ntk; t += CT, ++h)
+            a.gram[(size_t(c) * GRAM_TASKS + t) * a.nbc_max + lb] = h == 0 ? g0 : g1;
+    }
+    grid.sync();
+    __syncwarp();   // lane 0 spun in the barrier: reconverge before warp-synchronous code
+    STAMP(stamp++);
+    // distributed fixed-order reduction of the Gram partials
+    for (int gt = blockIdx.x * CT + tid; gt < nc * GRAM_TASKS; gt += nb * CT) {
+        const int cc = gt / GRAM_TASKS, t = gt - cc * GRAM_TASKS;
+        const int k = kcs[cc];
+        if (t >= k * (2 * k + 1)) continue;
+        const int nbcc = (nb - cc + nc - 1) / nc;
+        double acc = 0.0;
+        for (int b = 0; b < nbcc; ++b) acc += a.gram[(size_t(cc) * GRAM_TASKS + t) * a.nbc_max + b];
+        a.gram_tot[gt] = acc;
+    }
+    grid.sync();
+    __syncwarp();   // lane 0 spun in the barrier: reconverge before warp-synchronous code
+    STAMP(stamp++);
+    // block 0: one warp per component solves the k x k Ritz problem
+    if (blockIdx.x == 0) {
+        const int w = tid >> 5, lane = tid & 31;
+        double* ws = dsm + size_t(w) * (4 * KMAX * (KMAX + 1) + 2 * KMAX + 4 * KMAX);
+        if (w < nc) {
+            LzState& zs = P.lz[w];
+            const int k = kcs[w], nz = 2 * k + 1;
+            for (int idx = lane; idx < k * k; idx += 32) {
+                const int i = idx / k, jj = idx - i * k;
+                zs.A[i * KMAX + jj] = a.gram_tot[w * GRAM_TASKS + i * nz + jj];
+                zs.B[i * KMAX + jj] = a.gram_tot[w * GRAM_TASKS + i * nz + k + jj];
+            }
+            if (lane < k) zs.wr[lane] = a.gram_tot[w * GRAM_TASKS + lane * nz + 2 * k];
+            if (lane < KMAX) zs.coef[lane] = 0.0;
+            zs.kc = k;
+            zs.active = act[w];
+            __syncwarp();
+            if (act[w]) {
+                double* R = ws;
+                double* Cm = R + KMAX * (KMAX + 1);
+                double* V = Cm + KMAX * (KMAX + 1);
+                double* X = V + KMAX * (KMAX + 1);
+                double* rot = X + KMAX * (KMAX + 1);
+                int* rpq = reinterpret_cast<int*>(rot + KMAX);
+                if (a.timers && w == 0 && lane == 0) a.timers[100] = gtimer();
+                const bool ok = ritz_warp(zs.A, zs.B, zs.wr, k, P.singular[w] != 0, P.theta, zs.coef, R, Cm, V, X,
+                                          rot, rpq, (a.timers && w == 0) ? a.timers + 102 : nullptr);
+                if (a.timers && w == 0 && lane == 0) a.timers[101] = gtimer();
+                if (!ok && lane == 0) {
+                    zs.status = DE_EBREAKDOWN;
+                    for (int e = 0; e < KMAX; ++e) zs.coef[e] = 0.0;
+                    if (a.s) {
+                        PcgState* sm = const_cast<PcgState*>(a.s);
+                        sm->status = DE_EBREAKDOWN;
+                        sm->done = 1;
+                    }
+                }
+            }
+        }
+    }
+    grid.sync();
+    __syncwarp();   // lane 0 spun in the barrier: reconverge before warp-synchronous code
+    STAMP(stamp++);
+    // z = sum_t coef_t W_t, scattered back to interface order
+    {
+        const int k = kcs[c];
+        for (int64_t i = r0; i < hi; i += rs) {
+            double acc = 0.0;
+            if (act[c])
+                for (int t = 0; t < k; ++t) acc += P.lz[c].coef[t] * P.W[size_t(t) * nf + i];
+            a.z[P.cmap[i]] = acc;
+        }
+    }
+#undef ZERO_VALS
+}
+
+// ------------------------------------------------------------------ host side
+bool prec_coop_prepare(const PrecDev& P, int device, CoopBuffers& B) {
+    int nsm = 0;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+    int coop = 0;
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device);
+    if (!coop) return false;
+    const int mf = std::max(P.eK.maxface & 0xffff, P.eM.maxface & 0xffff);
+    const int mfac = std::max(P.eK.maxface >> 16, P.eM.maxface >> 16);
+    int ncmax = 1;
+    for (const ElimDev* E : {&P.eK, &P.eM})
+        for (int c = 0; c < P.ncomp; ++c) ncmax = std::max(ncmax, E->cross_comp_off[c + 1] - E->cross_comp_off[c]);
+    const bool stage = size_t(CW) * (3 * mf + mfac) * 8 <= 96 * 1024;
+    const int per_warp = stage ? 3 * mf + mfac : 3 * mf;
+    size_t smem = size_t(CW) * per_warp * 8;
+    smem = std::max(smem, size_t(ncmax) * 8);
+    smem = std::max(smem, size_t(3 * KMAX + 1) * (GTR + 1) * 8);
+    smem = std::max(smem, size_t(RW) * TRI_N * 8);   // per-thread forward solutions of tridiagonal faces
+    smem = std::max(smem, size_t(CW) * (4 * KMAX * (KMAX + 1) + 2 * KMAX + 4 * KMAX) * 8);
+    if (smem > 200 * 1024) return false;
+    cudaFuncSetAttribute(k_prec_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_prec_coop, CT, smem) != cudaSuccess || per_sm < 1)
+        return false;
+    const int nb = nsm * std::min(per_sm, 2);
+    if (nb < P.ncomp) return false;
+    B.nb = nb;
+    B.smem = smem;
+    B.stage = stage ? 1 : 0;
+    B.per_warp = per_warp;
+    B.mf = mf;
+    B.ncmax = ncmax;
+    B.tridiag = (P.eK.tri && P.eM.tri) ? 1 : 0;   // informational; each ElimDev carries its own flag
+    B.nbc_max = (nb + P.ncomp - 1) / P.ncomp;
+    return true;
+}
+
+size_t prec_coop_red_doubles(const CoopBuffers& B) { return size_t(2) * MAXC * NRED * B.nbc_max; }
+size_t prec_coop_gram_doubles(const CoopBuffers& B) { return size_t(MAXC) * GRAM_TASKS * B.nbc_max; }
+size_t prec_coop_gramtot_doubles() { return size_t(MAXC) * GRAM_TASKS; }
+
+int prec_apply_coop(const PrecDev& P, const CoopBuffers& B, const double* r, double* z, const PcgState* s,
+                    cudaStream_t st) {
+    CoopArgs a{};
+    a.P = P;
+    a.r = r;
+    a.z = z;
+    a.s = s;
+    a.red = B.red;
+    a.gram = B.gram;
+    a.gram_tot = B.gram_tot;
+    a.w1 = B.w1;
+    a.mw1 = B.mw1;
+    a.nbc_max = B.nbc_max;
+    a.stage = B.stage;
+    a.per_warp = B.per_warp;
+    a.mf = B.mf;
+    a.ncmax = B.ncmax;
+    a.tridiag = B.tridiag;
+    a.timers = B.timers;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(B.nb);
+    cfg.blockDim = dim3(CT);
+    cfg.dynamicSmemBytes = B.smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, k_prec_coop, a);
+    return e == cudaSuccess ? 1 : -1;
+}
+
+}  // namespace de

@@ -101,14 +101,17 @@ __global__ void k_face_solve(ElimDev E, const double* __restrict__ b, const doub
     if (F >= E.nfaces) return;
     double* rb = fsh + size_t(w) * per_warp;
     double* ys = rb + mf;
-    double* fs = ys + mf;                       // staged [L | M] factor of this face
+    int* idx = reinterpret_cast<int*>(ys + mf);
+    double* fs = ys + 2 * mf;                   // staged [L | M] factor of this face
     const int o = E.face_off[F], n = E.face_off[F + 1] - o, bw = E.face_band[F], ld = bw + 1;
     const double* gf = E.face_fac + E.face_fac_off[F];
     for (int i = lane; i < 2 * n * ld; i += 32) fs[i] = gf[i];
     const double* Lf = fs;
     const double* Mf = fs + size_t(n) * ld;
     for (int i = lane; i < n; i += 32) {
-        double r = b[E.face_nodes[o + i]];
+        const int node = E.face_nodes[o + i];
+        idx[i] = node;
+        double r = b[node];
         if (mode == 1)
             for (int e = E.xfc_ptr[o + i]; e < E.xfc_ptr[o + i + 1]; ++e) r -= E.xfc_val[e] * xC[E.xfc_col[e]];
         rb[i] = r;
@@ -118,26 +121,23 @@ __global__ void k_face_solve(ElimDev E, const double* __restrict__ b, const doub
     for (int sw = 0; sw < 2; ++sw) {
         const double* fac = sw == 0 ? Lf : Mf;
         const double* src = sw == 0 ? rb : ys;
+        double* dst = sw == 0 ? ys : rb;
         double v = lane < n ? src[lane] : 0.0;   // ys already holds P y
         __syncwarp();
 #pragma unroll 4
         for (int j = 0; j < n; ++j) {
             const double* col = fac + size_t(j) * ld;
             const double cl = (lane >= 1 && lane <= bw) ? col[lane] : 0.0;
+            const double nxt = (j + 32 < n) ? src[j + 32] : 0.0;   // row entering lane 31 (uniform load)
             const double yj = __shfl_sync(0xffffffffu, v, 0) * col[0];
             v = fma(-cl, yj, v);
-            v = __shfl_down_sync(0xffffffffu, v, 1);
-            if (lane == 31) {
-                const int r = j + 32;
-                v = r < n ? src[r] : 0.0;
-            }
-            if (lane == 0) {
-                if (sw == 0) ys[n - 1 - j] = yj;          // y stored reversed for the M sweep
-                else out[E.face_nodes[o + n - 1 - j]] = yj;
-            }
+            const double vs = __shfl_down_sync(0xffffffffu, v, 1);
+            v = (lane == 31) ? nxt : vs;                           // branch-free: keeps the warp converged
+            dst[n - 1 - j] = yj;                                   // same value from every lane
         }
         __syncwarp();
     }
+    for (int i = lane; i < n; i += 32) out[idx[i]] = rb[i];
 }
 
 static int face_warps_per_block(int per_warp_doubles) {
@@ -181,7 +181,7 @@ __global__ void k_cross_solve(ElimDev E, const double* __restrict__ b, const dou
 static void elim_solve(const PrecDev& P, const ElimDev& E, const double* b, double* x, const PcgState* s,
                        cudaStream_t st, int* nl) {
     const int mf = E.maxface & 0xffff, mfac = E.maxface >> 16;
-    const int per_warp = 2 * mf + mfac;
+    const int per_warp = 3 * mf + mfac;
     const int wpb = face_warps_per_block(per_warp);
     auto face = [&](const double* xc, double* o, int mode) {
         const int g = (E.nfaces + wpb - 1) / wpb;
@@ -438,7 +438,7 @@ __global__ void k_lz_eig(PrecDev P, PcgState* s) {
     }
     __syncwarp();
     const int m = (n + 1) & ~1, npair = m / 2;
-    for (int sweep = 0; sweep < 40 && n > 1; ++sweep) {
+    for (int sweep = 0; sweep < 30 && n > 1; ++sweep) {
         double off = 0.0, dia = 0.0;
         if (lane < n)
             for (int j = 0; j < n; ++j) {
@@ -452,6 +452,7 @@ __global__ void k_lz_eig(PrecDev P, PcgState* s) {
             dia += __shfl_xor_sync(0xffffffffu, dia, o);
         }
         if (off <= 1e-30 * dia) break;
+        int rotated = 0;
         for (int rnd = 0; rnd < m - 1; ++rnd) {
             if (lane < npair) {                             // round-robin pairs (circle method)
                 int p, q;
@@ -470,7 +471,11 @@ __global__ void k_lz_eig(PrecDev P, PcgState* s) {
                 double cs = 1.0, sn = 0.0;
                 if (q < n) {
                     const double apq = C[p * LDK + q];
-                    if (fabs(apq) > 1e-300) {
+                    const double app = C[p * LDK + p], aqq = C[q * LDK + q];
+                    (void)app;
+                    (void)aqq;
+                    if (fabs(apq) > 1e-15 * sqrt(dia) && fabs(apq) > 1e-300) {   // else negligible vs ||C||
+                        rotated = 1;
                         const double tau = (C[q * LDK + q] - C[p * LDK + p]) / (2.0 * apq);
                         const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
                         cs = 1.0 / sqrt(1.0 + t * t);
@@ -507,6 +512,7 @@ __global__ void k_lz_eig(PrecDev P, PcgState* s) {
                 }
             __syncwarp();
         }
+        if (!__any_sync(0xffffffffu, rotated)) break;   // every pair below threshold: converged
     }
     const bool sing = P.singular[c] != 0;
     int bad = 0;
@@ -585,7 +591,7 @@ void prec_apply(const PrecDev& P, const double* r, double* z, const PcgState* s,
 void prec_prepare(const PrecDev& P) {
     int mx = 0;
     for (const ElimDev* E : {&P.eK, &P.eM}) {
-        const int per_warp = 2 * (E->maxface & 0xffff) + (E->maxface >> 16);
+        const int per_warp = 3 * (E->maxface & 0xffff) + (E->maxface >> 16);
         mx = std::max(mx, face_warps_per_block(per_warp) * per_warp * 8);
     }
     if (mx > 48 * 1024) cudaFuncSetAttribute(k_face_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
