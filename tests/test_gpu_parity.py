@@ -219,7 +219,7 @@ def test_config5_sequence_warm_start():
         S.close()
 
 
-@pytest.mark.parametrize("name", ["c2", "c5"])
+@pytest.mark.parametrize("name", ["c2", "c4", "c5"])
 def test_full_size_sampled(name):
     """BASELINE sizes in the bench launch configuration: properties at any size (true residual by
     the oracle's own K) plus sampled subdomain factors/assembled blocks against the oracle."""
@@ -262,3 +262,20 @@ def residual_floor(p, u):
     np.add.at(out, ed.ravel(), fe.ravel())
     free = p.fixed == 0
     return float(np.finfo(float).eps / 2 * np.linalg.norm(out[free]) / np.linalg.norm(p.rhs[free]))
+
+
+def test_c3_full_size_budgeted_iterates_match_oracle():
+    """R15 at the BASELINE size: config 3 is FP64-ill-posed, so the gate is agreement of the GPU
+    and oracle interface iterates after the same fixed budget (same algorithm, same inputs)."""
+    p = make_config("c3")
+    S = _solver(p, max_iter=6)
+    try:
+        S.factor()
+        u, its, relres, st = S.solve(p.rhs, p.rtol, allow_noconv=True)
+        assert its == 6
+        o = DDOracle(p)
+        ro = o.solve(maxit=6)
+        uG = u[o.topo.gamma_dofs]
+        assert np.linalg.norm(uG - ro.uG) <= 1e-6 * np.linalg.norm(ro.uG)
+    finally:
+        S.close()
