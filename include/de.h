@@ -157,6 +157,10 @@ de_status_t de_get_dofmap(const de_ctx_t* ctx, int8_t* cls, int32_t* sub, int32_
  * per node its face id (-1 for a cross point). Arrays sized n_gamma_c[c] (see de_get_stats). */
 de_status_t de_get_skeleton(const de_ctx_t* ctx, int32_t c, int32_t* nodes, int32_t* face_of_node);
 
+/* Subdomains owned by this rank (ascending global ids; slab rule in the header comment). ids may be NULL
+ * to query the count; available for host_only contexts as well. */
+de_status_t de_get_owned(const de_ctx_t* ctx, int32_t* ids, int32_t* n);
+
 de_status_t de_get_stats(const de_ctx_t* ctx, de_stats_t* stats);
 
 /* ---- component-level entry points (parity tests and profiling) --------------------------

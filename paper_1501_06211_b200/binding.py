@@ -79,6 +79,7 @@ def lib():
         "de_get_dofmap": (I32, [P, P, P, P, C.POINTER(I64), C.POINTER(I64)]),
         "de_get_skeleton": (I32, [P, I32, P, P]),
         "de_get_stats": (I32, [P, C.POINTER(de_stats_t)]),
+        "de_get_owned": (I32, [P, P, C.POINTER(I32)]),
         "de_schur_apply_device": (I32, [P, P, P]),
         "de_precond_apply_device": (I32, [P, P, P]),
         "de_get_factor_band": (I32, [P, I32, P, C.POINTER(I32)]),
@@ -170,6 +171,14 @@ def de_get_stats(ctx) -> de_stats_t:
     s = de_stats_t()
     _check(lib().de_get_stats(ctx, C.byref(s)))
     return s
+
+
+def de_get_owned(ctx):
+    n = C.c_int32()
+    _check(lib().de_get_owned(ctx, None, C.byref(n)))
+    ids = np.empty(n.value, np.int32)
+    _check(lib().de_get_owned(ctx, _ptr(ids), C.byref(n)))
+    return ids
 
 
 def de_get_dofmap(ctx):

@@ -509,6 +509,15 @@ de_status_t setup_impl(const de_mesh_t* mesh, const double* density, double E0, 
     c->stats.n_Gamma = hs.n_G;
     c->stats.n_sub = hs.nsub;
     for (int cc = 0; cc < hs.ncomp; ++cc) c->stats.n_gamma_c[cc] = hs.comp_off[cc + 1] - hs.comp_off[cc];
+    // ---- ownership: slabs of subdomain columns along x
+    const int px = hs.ps[0];
+    const int lo = int((int64_t(c->rank) * px) / c->nranks), hi = int((int64_t(c->rank + 1) * px) / c->nranks);
+    for (int s = 0; s < hs.nsub; ++s) {
+        const int sx = s % px;
+        if (sx >= lo && sx < hi) c->owned.push_back(s);
+    }
+    c->nsl = int(c->owned.size());
+    c->stats.n_sub_local = c->nsl;
     if (opt.host_only) return DE_OK;
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
@@ -522,14 +531,6 @@ de_status_t setup_impl(const de_mesh_t* mesh, const double* density, double E0, 
         DE_CUDA(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
         c->own_stream = true;
     }
-    // ---- ownership: slabs of subdomain columns along x
-    const int px = hs.ps[0];
-    const int lo = int((int64_t(c->rank) * px) / c->nranks), hi = int((int64_t(c->rank + 1) * px) / c->nranks);
-    for (int s = 0; s < hs.nsub; ++s) {
-        const int sx = s % px;
-        if (sx >= lo && sx < hi) c->owned.push_back(s);
-    }
-    c->nsl = int(c->owned.size());
     HRing ring;
     build_ring(hs, c->owned, ring);
     std::vector<int32_t> idofs, Rg, ig_sub, gx_sub;
@@ -997,6 +998,17 @@ de_status_t de_get_skeleton(const de_ctx_t* c, int32_t comp, int32_t* nodes, int
         if (nodes) nodes[f - hs.comp_off[comp]] = hs.cnode[f];
         if (face_of_node) face_of_node[f - hs.comp_off[comp]] = hs.face_of[f];
     }
+    return DE_OK;
+}
+
+de_status_t de_get_owned(const de_ctx_t* c, int32_t* ids, int32_t* n) {
+    if (!c || !n) {
+        set_error("null argument");
+        return DE_EINVAL;
+    }
+    *n = c->nsl;
+    if (ids)
+        for (int k = 0; k < c->nsl; ++k) ids[k] = c->owned[k];
     return DE_OK;
 }
 

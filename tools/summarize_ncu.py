@@ -1,0 +1,59 @@
+"""Turn ncu outputs (gpurun_out/) into committed summaries under profiles/ (run on the CPU side)."""
+import csv, collections, json, subprocess, sys, io
+
+
+def launches(csv_path, out_md, title):
+    rows = list(csv.reader(open(csv_path)))
+    hi = [i for i, r in enumerate(rows) if 'Kernel Name' in r][0]
+    h = rows[hi]; data = rows[hi + 1:]
+    ki = h.index('Kernel Name'); mi = h.index('Metric Value')
+    agg = collections.defaultdict(lambda: [0, 0.0])
+    for r in data:
+        if len(r) <= mi: continue
+        agg[r[ki].split('(')[0]][0] += 1
+        agg[r[ki].split('(')[0]][1] += float(r[mi].replace(',', ''))
+    tot = sum(v[1] for v in agg.values())
+    with open(out_md, 'w') as f:
+        f.write(f"# {title}\n\nncu `--metrics gpu__time_duration.sum --clock-control none` (cold-cache, serialised "
+                "launches: compare SHARES, not absolute times). Source: `{}`.\n\n".format(csv_path))
+        f.write("| kernel | launches | total ms | avg us | share |\n|---|---:|---:|---:|---:|\n")
+        for k, v in sorted(agg.items(), key=lambda x: -x[1][1]):
+            f.write(f"| `{k}` | {v[0]} | {v[1]/1e6:.2f} | {v[1]/v[0]/1e3:.2f} | {v[1]/tot:.3f} |\n")
+    return agg, tot
+
+
+def full(rep, out_md, title, algo_bytes=None):
+    raw = subprocess.run(['ncu', '-i', rep, '--page', 'raw', '--csv'], capture_output=True, text=True).stdout
+    r = list(csv.reader(io.StringIO(raw))); h, u, v = r[0], r[1], r[2]
+    get = lambda k: (float(v[h.index(k)].replace(',', '')), u[h.index(k)]) if k in h else (None, None)
+    det = subprocess.run(['ncu', '-i', rep, '--page', 'details', '--csv'], capture_output=True, text=True).stdout
+    d = list(csv.reader(io.StringIO(det))); dh = d[0]
+    si, mi, vi, ui = (dh.index(x) for x in ('Section Name', 'Metric Name', 'Metric Value', 'Metric Unit'))
+    keep = ('GPU Speed Of Light Throughput', 'Memory Workload Analysis', 'Compute Workload Analysis', 'Occupancy',
+            'Scheduler Statistics', 'Warp State Statistics', 'Launch Statistics')
+    t, tu = get('gpu__time_duration.sum')
+    rd, rdu = get('dram__bytes_read.sum')
+    wr, wru = get('dram__bytes_write.sum')
+    scale = {'Gbyte': 1e9, 'Mbyte': 1e6, 'Kbyte': 1e3, 'byte': 1.0}
+    traffic = rd * scale[rdu] + wr * scale[wru]
+    with open(out_md, 'w') as f:
+        f.write(f"# {title}\n\n`ncu --set full --clock-control none --import-source on`, report `{rep}`.\n\n")
+        f.write(f"* duration: {t} {tu}\n* dram read: {rd} {rdu}, write: {wr} {wru} -> traffic {traffic/1e9:.3f} GB/launch\n")
+        if algo_bytes:
+            f.write(f"* algorithmic bytes (1 pass over the factor band + ring + vectors): {algo_bytes/1e9:.3f} GB "
+                    f"-> traffic / algorithmic = {traffic/algo_bytes:.2f}\n")
+        f.write("\n| section | metric | value | unit |\n|---|---|---:|---|\n")
+        for row in d[1:]:
+            if row[si] in keep:
+                f.write(f"| {row[si]} | {row[mi]} | {row[vi]} | {row[ui]} |\n")
+    return traffic
+
+
+if __name__ == '__main__':
+    launches('gpurun_out/launches_bench.csv', 'profiles/round1_launches_bench_c5.md',
+             'Round 1 launch list: `bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline` (config c5)')
+    tr = full('gpurun_out/schur_bench.ncu-rep', 'profiles/round1_schur_local_c5.md',
+              'Round 1: k_schur_local (C2 Schur apply), config c5, 2048 subdomains', algo_bytes=2285200320.0)
+    json.dump({"config": "c5", "n_gpus": 1, "kernel": "k_schur_local", "dram_bytes_per_launch": tr,
+               "source": "profiles/round1_schur_local_c5.md"}, open('profiles/schur_traffic.json', 'w'), indent=1)
+    print('traffic', tr)
