@@ -91,6 +91,10 @@ typedef struct {
                                 no device is touched and de_factor/de_solve return DE_ESTATE */
     int32_t prec_kernels;    /* 0 (default): one persistent cooperative kernel per preconditioner
                                 application; 1: one kernel per phase (same arithmetic) */
+    int32_t schur_mode;      /* S apply in the PCG loop: 0 = auto (explicit when the dense local S_s take fewer
+                                bytes than one pass over the factors, i.e. 2D), 1 = implicit through interior
+                                solves, 2 = explicit local Schur complements S_s formed at
+                                de_factor; condense/back-substitution always use the solves */
 } de_options_t;
 
 typedef struct {
@@ -115,7 +119,8 @@ typedef struct {
                                 factor band + ring blocks A_IG/A_GG + local interface vectors */
     int64_t kernels_launched; /* kernels launched by the last de_solve (graph nodes included) */
     int32_t iterations_pass1; /* PCG iterations before iterative refinement */
-    int32_t pad_;
+    int32_t schur_explicit;  /* 1 if the PCG loop applies explicit local Schur complements */
+    double bytes_schur_explicit; /* algorithmic bytes of one explicit S apply: sum_s n_Gamma,s^2 * 8 + vectors */
 } de_stats_t;
 
 /* Fill *opt with defaults (theta 0.5, k 10, inner_mode 1, max_iter 20000, FR, 1 rank). */

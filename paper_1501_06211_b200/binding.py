@@ -38,7 +38,7 @@ class de_options_t(C.Structure):
                 ("beta_variant", C.c_int32), ("warm_start", C.c_int32), ("rank", C.c_int32),
                 ("nranks", C.c_int32), ("device", C.c_int32), ("nccl_id", C.c_void_p),
                 ("stream", C.c_void_p), ("check_every", C.c_int32), ("use_graph", C.c_int32),
-                ("host_only", C.c_int32), ("prec_kernels", C.c_int32)]
+                ("host_only", C.c_int32), ("prec_kernels", C.c_int32), ("schur_mode", C.c_int32)]
 
 
 class de_stats_t(C.Structure):
@@ -51,7 +51,8 @@ class de_stats_t(C.Structure):
                 ("singular_components", C.c_int32), ("n_cross", C.c_int64 * 3), ("n_faces", C.c_int64 * 3),
                 ("n_gamma_c", C.c_int64 * 3),
                 ("bytes_schur", C.c_double), ("kernels_launched", C.c_int64),
-                ("iterations_pass1", C.c_int32), ("pad_", C.c_int32)]
+                ("iterations_pass1", C.c_int32), ("schur_explicit", C.c_int32),
+                ("bytes_schur_explicit", C.c_double)]
 
 
 _lib = None

@@ -115,6 +115,11 @@ struct de_ctx {
     int64_t prof_n = 0;
     int64_t launches = 0;
     double* d_ubuf2 = nullptr;
+    bool explicit_schur = false;
+    double* d_sexp = nullptr;
+    double* d_colscratch = nullptr;
+    int col_batch = 0;
+    int64_t n_sexp = 0;
     // nccl
     void* comm = nullptr;
     de_stats_t stats{};
@@ -195,8 +200,15 @@ SchurArgs schur_args(de_ctx* c, int mode, const double* xin, const double* f, do
 }
 
 // q = S x (assembled over ranks). Used outside the captured loop.
+void launch_apply(de_ctx* c, const double* x, const PcgState* s) {
+    if (c->explicit_schur)
+        launch_schur_explicit(c->d_sd, c->nsl, c->d_sexp, c->d_Rg, x, c->d_qloc, c->max_nG, s, c->st);
+    else
+        launch_schur_local(schur_args(c, SCHUR_APPLY, x, nullptr, nullptr, s), c->st);
+}
+
 de_status_t schur_apply(de_ctx* c, const double* x, double* q) {
-    launch_schur_local(schur_args(c, SCHUR_APPLY, x, nullptr, nullptr, nullptr), c->st);
+    launch_apply(c, x, nullptr);
     launch_gather(c->d_gptr, c->d_gsrc, c->d_qloc, nullptr, q, c->hs.n_G, nullptr, c->st);
     TRY(check_launch());
     return allreduce(c, q, size_t(c->hs.n_G));
@@ -223,7 +235,7 @@ de_status_t pcg_iteration(de_ctx* c, int* nl, cudaEvent_t e0, cudaEvent_t e1) {
     const int64_t nG = c->hs.n_G;
     int n = 0;
     if (e0) cudaEventRecordWithFlags(e0, c->st, cudaEventRecordExternal);   // a real node when captured
-    launch_schur_local(schur_args(c, SCHUR_APPLY, c->d_p, nullptr, nullptr, c->d_state), c->st);
+    launch_apply(c, c->d_p, c->d_state);
     if (e1) cudaEventRecordWithFlags(e1, c->st, cudaEventRecordExternal);
     launch_gather(c->d_gptr, c->d_gsrc, c->d_qloc, nullptr, c->d_q, nG, c->d_state, c->st);
     n += 2;
@@ -546,6 +558,8 @@ de_status_t setup_impl(const de_mesh_t* mesh, const double* density, double E0, 
         d.goff = goff;
         d.igp_off = ring.igp_off[k];
         d.gxp_off = ring.gxp_off[k];
+        d.sexp_off = c->n_sexp;
+        c->n_sexp += int64_t(hs.nGs[s]) * hs.nGs[s];
         c->hsd.push_back(d);
         idofs.insert(idofs.end(), hs.idofs.begin() + hs.ioff[s], hs.idofs.begin() + hs.ioff[s + 1]);
         for (int l = 0; l < d.nG; ++l) Rg.push_back(hs.gpos[hs.gdofs[hs.goff[s] + l]]);
@@ -601,6 +615,21 @@ de_status_t setup_impl(const de_mesh_t* mesh, const double* density, double E0, 
     TRY(dalloc(c, &c->d_ig_val, size_t(c->n_ig)));
     TRY(dalloc(c, &c->d_gx_val, size_t(c->n_gx)));
     TRY(dalloc(c, &c->d_band, 2 * size_t(c->n_local_I) * hs.ld));
+    {   // explicit local Schur complements: decide, then allocate S_s and a column batch
+        const double fac_one_pass = double(c->n_local_I) * (hs.band + 1);
+        const bool fits = c->max_nG <= 1024;
+        if (opt.schur_mode == 2 && !fits) {
+            set_error("schur_mode = 2 needs n_Gamma,s <= 1024 per subdomain");
+            return DE_EINVAL;
+        }
+        c->explicit_schur = fits && (opt.schur_mode == 2 || (opt.schur_mode == 0 && double(c->n_sexp) < fac_one_pass));
+        if (c->explicit_schur) {
+            TRY(dalloc(c, &c->d_sexp, size_t(c->n_sexp)));
+            const size_t per = size_t(std::max(1, c->max_nG)) * size_t(std::max(1, c->max_nI));
+            c->col_batch = int(std::max<size_t>(1, std::min<size_t>(c->nsl, (size_t(512) << 20) / (per * 8))));
+            TRY(dalloc(c, &c->d_colscratch, size_t(c->col_batch) * per));
+        }
+    }
     TRY(dalloc(c, &c->d_scratch, size_t(c->n_local_I) + 32));
     TRY(dalloc(c, &c->d_qloc, size_t(c->n_local_G) + 32));
     TRY(dupload(c, &c->d_gptr, gcnt));
@@ -663,6 +692,8 @@ de_status_t setup_impl(const de_mesh_t* mesh, const double* density, double E0, 
     double fb = 0.0;
     for (const auto& d : c->hsd) fb += double(d.nI) * (hs.band + 1) * 8.0;
     S.bytes_factor = fb;
+    S.schur_explicit = c->explicit_schur ? 1 : 0;
+    S.bytes_schur_explicit = double(c->n_sexp) * 8.0 + double(c->n_local_G) * (8.0 * 3 + 4.0);
     S.bytes_schur = fb + double(c->n_ig + c->n_gx) * 12.0 + double(c->n_local_G) * (8.0 * 3 + 4.0) +
                     double(c->n_local_I + c->nsl) * 4.0;
     S.bytes_iter = fb + double(c->n_ig + c->n_gx) * 12.0 + double(c->n_local_G) * 8.0 * 3.0 +
@@ -686,6 +717,16 @@ de_status_t factor_impl(de_ctx* c) {
     launch_assemble_pairs(c->md, c->d_gx_da, c->d_gx_db, c->d_gx_sub, c->d_Ee, c->d_gx_val, c->n_gx, c->st);
     DE_CUDA(cudaMemsetAsync(c->d_fail, 0, sizeof(int), c->st));
     launch_band_cholesky(c->d_sd, c->nsl, c->d_band, hs.ld, hs.band, c->d_fail, c->st);
+    if (c->explicit_schur)   // S_s e_t for every local Gamma dof t, through the same interior solves
+        for (int s0 = 0; s0 < c->nsl; s0 += c->col_batch) {
+            SchurArgs a = schur_args(c, SCHUR_COLUMNS, nullptr, nullptr, nullptr, nullptr);
+            a.col_s0 = s0;
+            a.nsl = std::min(c->col_batch, c->nsl - s0);
+            a.sexp = c->d_sexp;
+            a.colscratch = c->d_colscratch;
+            a.max_nI = c->max_nI;
+            launch_schur_local(a, c->st);
+        }
     TRY(check_launch());
     DE_CUDA(cudaEventRecord(e1, c->st));
     int fail = 0;

@@ -124,6 +124,7 @@ struct SubDesc {          // one owned subdomain
     int64_t goff;         // offset into d_Rg / qloc
     int64_t igp_off;      // offset into d_igp (nI+1 entries)
     int64_t gxp_off;      // offset into d_gxp (nG+1 entries)
+    int64_t sexp_off;     // offset (doubles) of the explicit local Schur complement S_s (nG x nG), if formed
 };
 
 struct MeshDev {
@@ -196,7 +197,7 @@ int launch_band_cholesky(const SubDesc* sd, int nsl, double* band, int ld, int b
 void launch_apply_K(const MeshDev& m, const double* Ee, const double* u, const double* f,
                     const int8_t* cls, double* res, int64_t ndof, cudaStream_t st);
 
-enum SchurMode { SCHUR_APPLY = 0, SCHUR_CONDENSE = 1, SCHUR_BACKSUB = 2 };
+enum SchurMode { SCHUR_APPLY = 0, SCHUR_CONDENSE = 1, SCHUR_BACKSUB = 2, SCHUR_COLUMNS = 3 };
 struct SchurArgs {
     const SubDesc* sd;
     int nsl;
@@ -218,8 +219,15 @@ struct SchurArgs {
     const PcgState* state;  // early exit when state->done (may be null)
     int mode;
     int maxG;
+    // SCHUR_COLUMNS (explicit S_s = columns S_s e_t): local subdomains [col_s0, col_s0+nsl)
+    double* sexp;
+    double* colscratch;     // nsl*maxG*max_nI doubles
+    int col_s0, max_nI;
 };
 int launch_schur_local(const SchurArgs& a, cudaStream_t st);
+// q_s = S_s x_s with the explicit column-major S_s (one CTA per subdomain, coalesced over rows)
+void launch_schur_explicit(const SubDesc* sd, int nsl, const double* sexp, const int32_t* Rg, const double* xin,
+                           double* qloc, int maxG, const PcgState* s, cudaStream_t st);
 
 void launch_gather(const int32_t* gptr, const int32_t* gsrc, const double* qloc,
                    const double* add, double* q, int64_t nG, const PcgState* st_done,

@@ -143,9 +143,14 @@ __global__ void __launch_bounds__(32) k_schur_local(SchurArgs a, int nstage) {
     extern __shared__ __align__(128) unsigned char smem[];
     if (a.state != nullptr && a.state->done) return;
     const int lane = threadIdx.x;
-    const SubDesc d = a.sd[blockIdx.x];
+    // SCHUR_COLUMNS: warp (sl, t) forms column t of S_sl from x = e_t
+    const bool cols = a.mode == SCHUR_COLUMNS;
+    const int sl = cols ? a.col_s0 + int(blockIdx.x) / a.maxG : int(blockIdx.x);
+    const int tcol = cols ? int(blockIdx.x) % a.maxG : 0;
+    const SubDesc d = a.sd[sl];
+    if (cols && tcol >= d.nG) return;
     const int n = d.nI, nG = d.nG, B = a.band_w, ld = a.ld;
-    const int mode = a.mode;
+    const int mode = cols ? SCHUR_APPLY : a.mode;
 
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
     double* stg = reinterpret_cast<double*>(smem + 128);
@@ -158,12 +163,14 @@ __global__ void __launch_bounds__(32) k_schur_local(SchurArgs a, int nstage) {
         fence_mbar_init();
         for (int T = 0; T < min(nstage, 2 * ring.nst); ++T) ring.issue(T);
     }
-    if (mode != SCHUR_CONDENSE)
+    if (cols)
+        for (int l = lane; l < nG; l += 32) xl[l] = (l == tcol) ? 1.0 : 0.0;
+    else if (mode != SCHUR_CONDENSE)
         for (int l = lane; l < nG; l += 32) xl[l] = a.xin[a.Rg[d.goff + l]];
     __syncwarp();
     const int32_t* igp = a.igp + d.igp_off;
     const int32_t* idofs = a.idofs + d.ioff;
-    double* y = a.scratch + d.ioff;
+    double* y = cols ? a.colscratch + size_t(blockIdx.x) * a.max_nI : a.scratch + d.ioff;
     for (int r = lane; r < n; r += 32) {          // dense interior right-hand side
         double v = (mode == SCHUR_APPLY) ? 0.0 : a.f[idofs[r]];
         if (mode != SCHUR_CONDENSE) {
@@ -195,8 +202,42 @@ __global__ void __launch_bounds__(32) k_schur_local(SchurArgs a, int nstage) {
                 q -= a.gx_val[e] * w[-cidx - 1];
             }
         }
-        a.qloc[d.goff + l] = q;
+        if (cols) a.sexp[d.sexp_off + size_t(tcol) * nG + l] = q;   // column tcol of S_sl
+        else a.qloc[d.goff + l] = q;
     }
+}
+
+// q_s = S_s x_s, S_s column-major (= row-major by symmetry): thread t accumulates row t over columns k,
+// so each step is one coalesced read of column k. One CTA per subdomain.
+__global__ void __launch_bounds__(256) k_schur_explicit(const SubDesc* __restrict__ sd, const double* __restrict__ sexp,
+                                                        const int32_t* __restrict__ Rg, const double* __restrict__ xin,
+                                                        double* __restrict__ qloc, const PcgState* s) {
+    if (s != nullptr && s->done) return;
+    __shared__ double xs[1024];
+    const SubDesc d = sd[blockIdx.x];
+    const int nG = d.nG, t = threadIdx.x;
+    for (int l = t; l < nG; l += blockDim.x) xs[l] = xin[Rg[d.goff + l]];
+    __syncthreads();
+    const double* S = sexp + d.sexp_off;
+    for (int row = t; row < nG; row += blockDim.x) {
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        int k = 0;
+        for (; k + 3 < nG; k += 4) {
+            a0 += S[size_t(k) * nG + row] * xs[k];
+            a1 += S[size_t(k + 1) * nG + row] * xs[k + 1];
+            a2 += S[size_t(k + 2) * nG + row] * xs[k + 2];
+            a3 += S[size_t(k + 3) * nG + row] * xs[k + 3];
+        }
+        for (; k < nG; ++k) a0 += S[size_t(k) * nG + row] * xs[k];
+        qloc[d.goff + row] = (a0 + a1) + (a2 + a3);
+    }
+}
+
+void launch_schur_explicit(const SubDesc* sd, int nsl, const double* sexp, const int32_t* Rg, const double* xin,
+                           double* qloc, int maxG, const PcgState* s, cudaStream_t st) {
+    if (nsl == 0) return;
+    const int threads = std::min(256, std::max(32, (maxG + 31) / 32 * 32));
+    k_schur_explicit<<<nsl, threads, 0, st>>>(sd, sexp, Rg, xin, qloc, s);
 }
 
 template <int G, int NS>
@@ -208,7 +249,8 @@ static void launch_t(const SchurArgs& a, int nstage, size_t smem, cudaStream_t s
         cudaFuncSetAttribute(k_schur_local<G, NS>, cudaFuncAttributePreferredSharedMemoryCarveout,
                              cudaSharedmemCarveoutMaxShared);
     }
-    k_schur_local<G, NS><<<a.nsl, 32, smem, st>>>(a, nstage);
+    const unsigned grid = a.mode == SCHUR_COLUMNS ? unsigned(a.nsl) * unsigned(a.maxG) : unsigned(a.nsl);
+    k_schur_local<G, NS><<<grid, 32, smem, st>>>(a, nstage);
 }
 
 int launch_schur_local(const SchurArgs& a, cudaStream_t st) {

@@ -79,20 +79,22 @@ def test_schur_apply_matches_oracle(name, kw):
     p = make_config(name, **kw)
     T = build_topology(p)
     blocks = factor_subdomains(subdomain_blocks(p, T))
-    S = _solver(p)
-    try:
-        S.factor()
-        rng = np.random.default_rng(11)
-        for trial in range(2):
-            x = rng.normal(size=T.n_G)
-            ref = schur_apply(blocks, T.n_G, x)
-            dx = torch.tensor(x, dtype=torch.float64, device="cuda")
-            dq = torch.empty_like(dx)
-            B.de_schur_apply_device(S.ctx, dx.data_ptr(), dq.data_ptr())
-            q = dq.cpu().numpy()
-            assert np.linalg.norm(q - ref) <= 1e-11 * np.linalg.norm(ref)
-    finally:
-        S.close()
+    for mode in (1, 2):     # 1: implicit (interior solves each apply), 2: explicit local S_s (NEXT(1))
+        S = _solver(p, schur_mode=mode)
+        try:
+            S.factor()
+            assert S.stats().schur_explicit == (1 if mode == 2 else 0)
+            rng = np.random.default_rng(11)
+            for trial in range(2):
+                x = rng.normal(size=T.n_G)
+                ref = schur_apply(blocks, T.n_G, x)
+                dx = torch.tensor(x, dtype=torch.float64, device="cuda")
+                dq = torch.empty_like(dx)
+                B.de_schur_apply_device(S.ctx, dx.data_ptr(), dq.data_ptr())
+                q = dq.cpu().numpy()
+                assert np.linalg.norm(q - ref) <= 1e-11 * np.linalg.norm(ref), mode
+        finally:
+            S.close()
 
 
 @pytest.mark.parametrize("name,kw", SMALL, ids=_ids(SMALL))
@@ -154,7 +156,8 @@ def test_solve_matches_monolithic(name, kw):
 def test_identity_preconditioner_and_flexible_beta():
     p = make_config("c2", nel=(64, 32), sub=(16, 16))
     u_ref = monolithic_solve(p)
-    for kw in (dict(inner_mode=3), dict(beta_variant=1), dict(use_graph=0, check_every=3), dict(prec_kernels=1)):
+    for kw in (dict(inner_mode=3), dict(beta_variant=1), dict(use_graph=0, check_every=3), dict(prec_kernels=1),
+               dict(schur_mode=1), dict(schur_mode=2)):
         S = _solver(p, **kw)
         try:
             S.factor()
