@@ -625,7 +625,7 @@ de_status_t setup_impl(const de_mesh_t* mesh, const double* density, double E0, 
         c->explicit_schur = fits && (opt.schur_mode == 2 || (opt.schur_mode == 0 && double(c->n_sexp) < fac_one_pass));
         if (c->explicit_schur) {
             TRY(dalloc(c, &c->d_sexp, size_t(c->n_sexp)));
-            const size_t per = size_t(std::max(1, c->max_nG)) * size_t(std::max(1, c->max_nI));
+            const size_t per = size_t(std::max(1, c->max_nG) + 8) * size_t(std::max(1, c->max_nI));
             c->col_batch = int(std::max<size_t>(1, std::min<size_t>(c->nsl, (size_t(512) << 20) / (per * 8))));
             TRY(dalloc(c, &c->d_colscratch, size_t(c->col_batch) * per));
         }

@@ -839,7 +839,9 @@ bool prec_coop_prepare(const PrecDev& P, int device, CoopBuffers& B) {
     int per_sm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_prec_coop, CT, smem) != cudaSuccess || per_sm < 1)
         return false;
-    const int nb = nsm * std::min(per_sm, 2);
+    int bps = 2;   // blocks per SM; DE_COOP_BPS overrides (tuning experiments only)
+    if (const char* e = getenv("DE_COOP_BPS")) bps = std::max(1, atoi(e));
+    const int nb = nsm * std::min(per_sm, bps);
     if (nb < P.ncomp) return false;
     B.nb = nb;
     B.smem = smem;

@@ -240,8 +240,158 @@ void launch_schur_explicit(const SubDesc* sd, int nsl, const double* sexp, const
     k_schur_explicit<<<nsl, threads, 0, st>>>(sd, sexp, Rg, xin, qloc, s);
 }
 
+// ------------------------------------------------------------------ explicit S_s formation, R columns per warp
+// The forward column sweep of sweep() for R right-hand sides at once: every factor column loaded from the
+// TMA stage feeds R independent chains (ILP across columns, R-fold less factor traffic per column).
+// yb holds the R right-hand sides row-major ([row][k]); solutions overwrite them (same aliasing rule).
+template <int G, int NS, int R>
+__device__ __forceinline__ void sweep_multi(const Ring& ring, double* yb, bool reversed, int& T, int lane, int B, int n) {
+    const int ld = ring.ld;
+    auto at = [&](int r) { return size_t(reversed ? n - 1 - r : r) * R; };
+    double v[R][NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+        const int r = lane + 32 * s;
+#pragma unroll
+        for (int k = 0; k < R; ++k) v[k][s] = r < n ? yb[at(r) + k] : 0.0;
+    }
+    double pend[R], outv[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) pend[k] = outv[k] = 0.0;
+    for (int t = 0; t < ring.nst; ++t, ++T) {
+        const double* S = ring.wait(T);
+        const int c0 = t * G, nc = min(G, n - c0);
+#pragma unroll
+        for (int cc = 0; cc < G; ++cc) {
+            if (cc < nc) {
+                const int j = c0 + cc;
+                const int o = j & 31;
+                if (o == 0) {
+                    const int r = j + lane + 32 * NS;
+#pragma unroll
+                    for (int k = 0; k < R; ++k) pend[k] = r < n ? yb[at(r) + k] : 0.0;
+                }
+                const double* col = S + cc * ld;
+                const int k0 = (lane - j) & 31;
+                double cv[NS];
+#pragma unroll
+                for (int s = 0; s < NS; ++s) {
+                    const int kk = k0 + 32 * s;
+                    cv[s] = (kk <= B && (s > 0 || k0 != 0)) ? col[kk] : 0.0;
+                }
+                const double inv = col[0];
+                double yj[R];
+#pragma unroll
+                for (int k = 0; k < R; ++k) yj[k] = __shfl_sync(0xffffffffu, v[k][0], o) * inv;
+#pragma unroll
+                for (int k = 0; k < R; ++k)
+#pragma unroll
+                    for (int s = 0; s < NS; ++s) v[k][s] = fma(-cv[s], yj[k], v[k][s]);
+                if (lane == o) {
+#pragma unroll
+                    for (int k = 0; k < R; ++k) {
+                        outv[k] = yj[k];
+#pragma unroll
+                        for (int s = 0; s < NS - 1; ++s) v[k][s] = v[k][s + 1];
+                        v[k][NS - 1] = pend[k];
+                    }
+                }
+                if (o == 31 || j == n - 1) {
+                    const int r = j - o + lane;
+                    if (lane <= o)
+#pragma unroll
+                        for (int k = 0; k < R; ++k) yb[at(r) + k] = outv[k];
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0 && T + ring.nstage < 2 * ring.nst) {
+            fence_proxy_async();
+            ring.issue(T + ring.nstage);
+        }
+    }
+}
+
+// Columns t0..t0+R-1 of S_s = A_GG - A_GI A_II^-1 A_IG (x = e_t), one warp per (subdomain, column group).
+template <int G, int NS, int R>
+__global__ void __launch_bounds__(32) k_schur_cols(SchurArgs a, int nstage) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int lane = threadIdx.x;
+    const int wps = (a.maxG + R - 1) / R;
+    const int sl = a.col_s0 + int(blockIdx.x) / wps, t0 = (int(blockIdx.x) % wps) * R;
+    const SubDesc d = a.sd[sl];
+    if (t0 >= d.nG) return;
+    const int n = d.nI, nG = d.nG, B = a.band_w, ld = a.ld;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
+    double* stg = reinterpret_cast<double*>(smem + 128);
+    const double* Lb = a.band + d.band_off;
+    Ring ring{bar, stg, nstage, G, ld, n, (n + G - 1) / G, Lb, Lb + size_t(n) * ld};
+    if (lane == 0) {
+        for (int i = 0; i < nstage; ++i) mbar_init(bar + i, 1);
+        fence_mbar_init();
+        for (int T = 0; T < min(nstage, 2 * ring.nst); ++T) ring.issue(T);
+    }
+    const int32_t* igp = a.igp + d.igp_off;
+    double* yb = a.colscratch + size_t(blockIdx.x) * size_t(a.max_nI) * R;
+    for (int r = lane; r < n; r += 32) {                  // rhs columns t0..t0+R-1 of A_IG
+        double acc[R];
+#pragma unroll
+        for (int k = 0; k < R; ++k) acc[k] = 0.0;
+        for (int e = igp[r]; e < igp[r + 1]; ++e) {
+            const int cidx = a.ig_col[e] - t0;
+#pragma unroll
+            for (int k = 0; k < R; ++k)
+                if (cidx == k) acc[k] += a.ig_val[e];
+        }
+#pragma unroll
+        for (int k = 0; k < R; ++k) yb[size_t(r) * R + k] = acc[k];
+    }
+    __syncwarp();
+    int T = 0;
+    sweep_multi<G, NS, R>(ring, yb, false, T, lane, B, n);
+    __syncwarp();
+    sweep_multi<G, NS, R>(ring, yb, true, T, lane, B, n);
+    __syncwarp();
+    const int32_t* gxp = a.gxp + d.gxp_off;
+    for (int l = lane; l < nG; l += 32) {
+        double q[R];
+#pragma unroll
+        for (int k = 0; k < R; ++k) q[k] = 0.0;
+        for (int e = gxp[l]; e < gxp[l + 1]; ++e) {
+            const int cidx = a.gx_col[e];
+            const double val = a.gx_val[e];
+            if (cidx >= 0) {
+#pragma unroll
+                for (int k = 0; k < R; ++k)
+                    if (cidx == t0 + k) q[k] += val;
+            } else {
+#pragma unroll
+                for (int k = 0; k < R; ++k) q[k] -= val * yb[size_t(-cidx - 1) * R + k];
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < R; ++k)
+            if (t0 + k < nG) a.sexp[d.sexp_off + size_t(t0 + k) * nG + l] = q[k];
+    }
+}
+
+constexpr int COL_R = 8;
+
+template <int G, int NS>
+static void launch_cols(const SchurArgs& a, int nstage, size_t smem, cudaStream_t st) {
+    cudaFuncSetAttribute(k_schur_cols<G, NS, COL_R>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    const unsigned wps = unsigned((a.maxG + COL_R - 1) / COL_R);
+    k_schur_cols<G, NS, COL_R><<<unsigned(a.nsl) * wps, 32, smem, st>>>(a, nstage);
+}
+
 template <int G, int NS>
 static void launch_t(const SchurArgs& a, int nstage, size_t smem, cudaStream_t st) {
+    if constexpr (NS <= 4) {
+        if (a.mode == SCHUR_COLUMNS) {   // multi-RHS formation (2D bands)
+            launch_cols<G, NS>(a, nstage, smem, st);
+            return;
+        }
+    }
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     cudaStreamIsCapturing(st, &cs);
     if (cs == cudaStreamCaptureStatusNone) {
