@@ -463,9 +463,9 @@ de_status_t upload_prec(de_ctx* c) {
     if (c->opt.prec_kernels == 0 && prec_coop_prepare(P, c->opt.device, c->coop)) {
         TRY(dalloc(c, &c->coop.red, prec_coop_red_doubles(c->coop)));
         TRY(dalloc(c, &c->coop.gram, prec_coop_gram_doubles(c->coop)));
-        TRY(dalloc(c, &c->coop.gram_tot, prec_coop_gramtot_doubles()));
         TRY(dalloc(c, &c->coop.w1, nf));
         TRY(dalloc(c, &c->coop.mw1, nf));
+        TRY(dalloc(c, &c->coop.lw1, nf));
         if (getenv("DE_PREC_TIMERS")) {
             TRY(dalloc(c, &c->coop.timers, 200 + 8192));
             DE_CUDA(cudaMemsetAsync(c->coop.timers, 0, (200 + 8192) * sizeof(unsigned long long), c->st));

@@ -282,13 +282,12 @@ struct CoopBuffers {
     int nb = 0;
     size_t smem = 0;
     int stage = 0, per_warp = 0, mf = 0, ncmax = 0, nbc_max = 0, tridiag = 0;
-    double *red = nullptr, *gram = nullptr, *gram_tot = nullptr, *w1 = nullptr, *mw1 = nullptr;
+    double *red = nullptr, *gram = nullptr, *w1 = nullptr, *mw1 = nullptr, *lw1 = nullptr;
     unsigned long long* timers = nullptr;   // phase stamps (diagnostics; env DE_PREC_TIMERS=1)
 };
 bool prec_coop_prepare(const PrecDev& P, int device, CoopBuffers& B);
 size_t prec_coop_red_doubles(const CoopBuffers& B);
 size_t prec_coop_gram_doubles(const CoopBuffers& B);
-size_t prec_coop_gramtot_doubles();
 int prec_apply_coop(const PrecDev& P, const CoopBuffers& B, const double* r, double* z, const PcgState* s,
                     cudaStream_t st);
 

@@ -13,6 +13,8 @@
 #include "de_internal.h"
 
 #include <cooperative_groups.h>
+#include <cstdio>
+#include <cstdlib>
 
 namespace cg = cooperative_groups;
 
@@ -22,8 +24,8 @@ constexpr int CT = 256;
 constexpr int CW = CT / 32;
 constexpr int NRED = KMAX + 2;
 constexpr int RW = CT - 32;                   // rows per block chunk in row-parallel phases
-constexpr int GTR = RW / 2;                   // Gram tile rows (divides RW)
-constexpr int GRAM_TASKS = KMAX * (2 * KMAX + 1);
+constexpr int GW = 2 * KMAX + 1;              // Gram row j: G_L[j][t] (t<=j), G_M[j][t] (KMAX+t), (W^T r)[j] (2 KMAX)
+constexpr int GRAM_TASKS = KMAX * GW;
 
 struct CoopArgs {
     PrecDev P;
@@ -31,10 +33,10 @@ struct CoopArgs {
     double* z;
     const PcgState* s;
     double* red;        // [2][MAXC][NRED][nbc_max]
-    double* gram;       // [MAXC][GRAM_TASKS][nbc_max]
-    double* gram_tot;   // [MAXC][GRAM_TASKS]
+    double* gram;       // [MAXC][KMAX rows][GW][nbc_max] per-block Gram partials
     double* w1;         // second Lanczos work vector (nflat)
-    double* mw1;        // scratch (nflat)
+    double* mw1;        // M w1 (nflat)
+    double* lw1;        // L w1 (nflat)
     int nbc_max;
     int stage;          // 1: stage face factors in shared memory
     int per_warp;       // doubles of shared memory per warp for face solves
@@ -98,6 +100,26 @@ __device__ void read_totals(const CoopArgs& a, int pp, int nv, int nb, double (*
         for (int b = lane; b < nbc; b += 32) acc += *((volatile const double*)(p + b));
         acc = warp_sum(acc);
         if (lane == 0) tot[c][v] = acc;
+    }
+    __syncthreads();
+}
+
+// per-thread Gram accumulators gacc[v * CT + tid], v < GW
+__device__ __forceinline__ void gram_zero(double* gacc) {
+#pragma unroll
+    for (int v = 0; v < GW; ++v) gacc[v * CT + threadIdx.x] = 0.0;
+}
+
+// block sums of gacc (fixed order) -> a.gram partial slots of Gram row j of component c
+__device__ void gram_partials(const CoopArgs& a, const double* gacc, int c, int lb, int j) {
+    __syncthreads();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int v = w; v < GW; v += CW) {
+        double t = 0.0;
+#pragma unroll
+        for (int q = 0; q < CW; ++q) t += gacc[v * CT + q * 32 + lane];
+        t = warp_sum(t);
+        if (lane == 0) a.gram[((size_t(c) * KMAX + j) * GW + v) * a.nbc_max + lb] = t;
     }
     __syncthreads();
 }
@@ -404,6 +426,7 @@ __device__ bool ritz_warp(const double* Ain, const double* Bin, const double* wr
     int nsw = 0;
     for (int sweep = 0; sweep < 30 && n > 1; ++sweep) {
         ++nsw;
+        if (tm && sweep == 0 && lane == 0) tm[13] = clock64();
         double off = 0.0, dia = 0.0;
         if (lane < n)
             for (int j = 0; j < n; ++j) {
@@ -414,8 +437,11 @@ __device__ bool ritz_warp(const double* Ain, const double* Bin, const double* wr
         off = warp_sum(off);
         dia = warp_sum(dia);
         if (off <= 1e-30 * dia) break;
+        if (tm && sweep == 0 && lane == 0) tm[12] = clock64();
         int rotated = 0;
         for (int rnd = 0; rnd < m - 1; ++rnd) {
+            const bool fine = tm && sweep == 0 && rnd == 0 && lane == 0;
+            if (fine) tm[8] = clock64();
             if (lane < npair) {
                 int p, q;
                 if (lane == 0) {
@@ -450,6 +476,7 @@ __device__ bool ritz_warp(const double* Ain, const double* Bin, const double* wr
                 rpq[KMAX / 2 + lane] = q;
             }
             __syncwarp();
+            if (fine) tm[9] = clock64();
             // the pairs of a round are disjoint: gather every operand first, then write (pipelined smem)
             constexpr int NP = KMAX / 2;
             int pp[NP], qq[NP];
@@ -482,6 +509,7 @@ __device__ bool ritz_warp(const double* Ain, const double* Bin, const double* wr
                     }
             }
             __syncwarp();
+            if (fine) tm[10] = clock64();
             if (lane < n) {                                  // C <- J^T C (column `lane`)
                 double x0[NP], x1[NP];
 #pragma unroll
@@ -498,6 +526,7 @@ __device__ bool ritz_warp(const double* Ain, const double* Bin, const double* wr
                     }
             }
             __syncwarp();
+            if (fine) tm[11] = clock64();
         }
         if (!__any_sync(0xffffffffu, rotated)) break;   // every pair below threshold: converged
     }
@@ -531,7 +560,7 @@ __device__ bool ritz_warp(const double* Ain, const double* Bin, const double* wr
     return true;
 }
 
-__global__ void __launch_bounds__(CT) k_prec_coop(CoopArgs a) {
+__global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
     cg::grid_group grid = cg::this_grid();
     if (a.s != nullptr && a.s->done) return;
     int stamp = 0;
@@ -542,6 +571,7 @@ __global__ void __launch_bounds__(CT) k_prec_coop(CoopArgs a) {
     __shared__ double tot[MAXC][NRED];
     __shared__ double scl[MAXC], nrmv[MAXC], nb2v[MAXC];
     __shared__ double hsm[MAXC][KMAX];
+    __shared__ double sclh[MAXC][KMAX];   // 1/||w_j||_M of every accepted basis vector (Gram scaling)
     __shared__ int act[MAXC], kcs[MAXC], brk[MAXC];
     const int tid = threadIdx.x;
     const int nb = gridDim.x, nc = P.ncomp;
@@ -580,12 +610,20 @@ __global__ void __launch_bounds__(CT) k_prec_coop(CoopArgs a) {
     elim_coop(grid, a, P.eM, P.rf, scl, P.s, dsm, c, lb, nbc, stamp);
     // ---- Ms, ||s||_M; q_1 = s / ||s||_M, rhs of the next solve v = M q_1 = Ms / ||s||_M
     ZERO_VALS();
+    double* gacc = dsm;   // per-thread Gram accumulators [GW][CT] (dsm is free outside face solves / Ritz)
+    gram_zero(gacc);
     for (int64_t i = r0; i < hi; i += rs) {
-        const double m = spmv_row(P.M, i, P.s);
+        double m, l, unused_h[1] = {0.0};
+        corr_spmv<true>(P.M, P.L, i, P.s, P.W, nf, unused_h, 0, m, l);
+        const double sv = P.s[i];
         P.Mw[i] = m;
-        P.LW[i] = spmv_row(P.L, i, P.s);
-        vals[0] += P.s[i] * m;
+        P.LW[i] = l;
+        vals[0] += sv * m;
+        gacc[0 * CT + tid] += sv * l;            // G_L[0][0] (unscaled)
+        gacc[KMAX * CT + tid] += sv * m;         // G_M[0][0]
+        gacc[2 * KMAX * CT + tid] += sv * P.rf[i];   // (W^T r)[0]
     }
+    gram_partials(a, gacc, c, lb, 0);
     block_partials(a, vals, 1, pp, c, lb, sred);
     grid.sync();
     __syncwarp();   // lane 0 spun in the barrier: reconverge before warp-synchronous code
@@ -596,6 +634,7 @@ __global__ void __launch_bounds__(CT) k_prec_coop(CoopArgs a) {
         nrmv[tid] = sqrt(tot[tid][0]);
         if (act[tid]) kcs[tid] = 1;
         scl[tid] = act[tid] ? 1.0 / nrmv[tid] : 0.0;
+        sclh[tid][0] = scl[tid];
     }
     __syncthreads();
     if (act[c])
@@ -609,11 +648,14 @@ __global__ void __launch_bounds__(CT) k_prec_coop(CoopArgs a) {
         elim_coop(grid, a, P.eK, P.Mw, scl, P.w, dsm, c, lb, nbc, stamp);   // w = K^-1 M q_j
         const bool part = act[c] && !brk[c];
         const int kc = kcs[c];
-        // A: Mw = M w; ||w||_M^2 and h_t = W_t . Mw
+        // A: (M w, L w) by one SpMV over the shared pattern; ||w||_M^2 and h_t = W_t . M w
         ZERO_VALS();
         if (part)
             for (int64_t i = r0; i < hi; i += rs) {
-                const double m = spmv_row(P.M, i, P.w);
+                double m, l, unused_h[1] = {0.0};
+                corr_spmv<true>(P.M, P.L, i, P.w, P.W, nf, unused_h, 0, m, l);
+                a.mw1[i] = m;
+                a.lw1[i] = l;
                 vals[0] += P.w[i] * m;
                 double wt[KMAX];
 #pragma unroll
@@ -630,19 +672,29 @@ __global__ void __launch_bounds__(CT) k_prec_coop(CoopArgs a) {
         if (tid < nc) nb2v[tid] = tot[tid][0];
         if (tid < KMAX) hsm[c][tid] = tid < kc ? tot[c][1 + tid] : 0.0;
         __syncthreads();
-        // B: w1 = w - W h;  dots h'_t = W_t . M(w - W h)
+        // B: w1 = w - W h; M w1 = M w - (M W) h and L w1 = L w - (L W) h by linearity (own rows only);
+        // dots h'_t = W_t . M w1
         ZERO_VALS();
         if (part)
             for (int64_t i = r0; i < hi; i += rs) {
-                double wt[KMAX];
+                double wt[KMAX], mt[KMAX], lt[KMAX];
 #pragma unroll
-                for (int t = 0; t < KMAX; ++t) wt[t] = t < kc ? P.W[size_t(t) * nf + i] : 0.0;
-                double x = P.w[i];
+                for (int t = 0; t < KMAX; ++t) {
+                    const bool ok = t < kc;
+                    wt[t] = ok ? P.W[size_t(t) * nf + i] : 0.0;
+                    mt[t] = ok ? P.MW[size_t(t) * nf + i] : 0.0;
+                    lt[t] = ok ? P.LW[size_t(t) * nf + i] : 0.0;
+                }
+                double x = P.w[i], m = a.mw1[i], l = a.lw1[i];
 #pragma unroll
-                for (int t = 0; t < KMAX; ++t) x -= hsm[c][t] * wt[t];
+                for (int t = 0; t < KMAX; ++t) {
+                    x -= hsm[c][t] * wt[t];
+                    m -= hsm[c][t] * mt[t];
+                    l -= hsm[c][t] * lt[t];
+                }
                 a.w1[i] = x;
-                double m, unused;
-                corr_spmv<false>(P.M, P.L, i, P.w, P.W, nf, hsm[c], kc, m, unused);
+                a.mw1[i] = m;
+                a.lw1[i] = l;
 #pragma unroll
                 for (int t = 0; t < KMAX; ++t) vals[t] += wt[t] * m;
             }
@@ -654,21 +706,47 @@ __global__ void __launch_bounds__(CT) k_prec_coop(CoopArgs a) {
         pp ^= 1;
         if (tid < KMAX) hsm[c][tid] = tid < kc ? tot[c][tid] : 0.0;
         __syncthreads();
-        // C: w2 = w1 - W h'; Mw2 = M w2 (kept for the next solve); ||w2||_M^2
+        // C: w2 = w1 - W h' with M w2, L w2 by linearity (M w2 is the next solve's rhs); ||w2||_M^2; row j of
+        // the Rayleigh-Ritz Gram matrices before normalisation: w2.(L W_t), w2.(M W_t) (t < j), w2.L w2,
+        // w2.M w2, w2.r
         const bool dbg = a.timers && blockIdx.x == 0 && tid == 32 && j == 5;
         if (dbg) a.timers[110] = gtimer();
         ZERO_VALS();
+        gram_zero(gacc);
         if (part)
             for (int64_t i = r0; i < hi; i += rs) {
-                const double x = a.w1[i] - basis_comb(P.W, nf, i, hsm[c], kc);
-                double m, l;
-                corr_spmv<true>(P.M, P.L, i, a.w1, P.W, nf, hsm[c], kc, m, l);
+                double wt[KMAX], mt[KMAX], lt[KMAX];
+#pragma unroll
+                for (int t = 0; t < KMAX; ++t) {
+                    const bool ok = t < kc;
+                    wt[t] = ok ? P.W[size_t(t) * nf + i] : 0.0;
+                    mt[t] = ok ? P.MW[size_t(t) * nf + i] : 0.0;
+                    lt[t] = ok ? P.LW[size_t(t) * nf + i] : 0.0;
+                }
+                double x = a.w1[i], m = a.mw1[i], l = a.lw1[i];
+                const double rv = P.rf[i];
+#pragma unroll
+                for (int t = 0; t < KMAX; ++t) {
+                    x -= hsm[c][t] * wt[t];
+                    m -= hsm[c][t] * mt[t];
+                    l -= hsm[c][t] * lt[t];
+                }
                 P.w[i] = x;
                 P.Mw[i] = m;
                 P.LW[size_t(j) * nf + i] = l;
                 vals[0] += x * m;
+#pragma unroll
+                for (int t = 0; t < KMAX; ++t)
+                    if (t < kc) {
+                        gacc[t * CT + tid] += x * lt[t];
+                        gacc[(KMAX + t) * CT + tid] += x * mt[t];
+                    }
+                gacc[kc * CT + tid] += x * l;
+                gacc[(KMAX + kc) * CT + tid] += x * m;
+                gacc[2 * KMAX * CT + tid] += x * rv;
             }
         if (dbg) a.timers[111] = gtimer();
+        if (part) gram_partials(a, gacc, c, lb, j);
         block_partials(a, vals, 1, pp, c, lb, sred);
         if (dbg) a.timers[112] = gtimer();
         grid.sync();
@@ -685,6 +763,7 @@ __global__ void __launch_bounds__(CT) k_prec_coop(CoopArgs a) {
                 if (na > 1e-12 * nbn) {
                     kcs[tid] = j + 1;
                     scl[tid] = 1.0 / na;
+                    sclh[tid][j] = scl[tid];
                 } else {
                     brk[tid] = 1;
                     scl[tid] = 0.0;
@@ -701,77 +780,38 @@ __global__ void __launch_bounds__(CT) k_prec_coop(CoopArgs a) {
                 P.MW[size_t(j) * nf + i] = P.Mw[i] * scl[c];
             }
     }
-    grid.sync();
-    __syncwarp();   // lane 0 spun in the barrier: reconverge before warp-synchronous code
-    STAMP(stamp++);   // last basis vector visible everywhere
-    // ---- Rayleigh-Ritz Gram products over own rows, tiles of GTR contiguous rows
-    {
-        const int k = kcs[c], nz = 2 * k + 1, nv = k + nz, ntk = k * nz;
-        double* tile = dsm;   // nv x (GTR+1)
-        double g0 = 0.0, g1 = 0.0;
-        if (act[c]) {
-            for (int64_t base = lo + int64_t(lb) * RW; base < hi; base += rs)
-                for (int q = 0; q < RW / GTR; ++q) {
-                    const int64_t rb0 = base + q * GTR;
-                    if (rb0 >= hi) break;
-                    for (int t = tid; t < nv * GTR; t += CT) {
-                        const int v = t / GTR, rr = t - v * GTR;
-                        const int64_t i = rb0 + rr;
-                        double val = 0.0;
-                        if (i < hi) {
-                            if (v < k) val = P.W[size_t(v) * nf + i];
-                            else if (v < 2 * k) val = P.LW[size_t(v - k) * nf + i];
-                            else if (v < 3 * k) val = P.MW[size_t(v - 2 * k) * nf + i];
-                            else val = P.rf[i];
-                        }
-                        tile[v * (GTR + 1) + rr] = val;
-                    }
-                    __syncthreads();
-                    for (int t = tid, h = 0; t < ntk; t += CT, ++h) {
-                        const int ii = t / nz, jz = t - ii * nz;
-                        const double* pa = tile + ii * (GTR + 1);
-                        const double* pb = tile + (k + jz) * (GTR + 1);
-                        double acc = 0.0;
-#pragma unroll 8
-                        for (int rr = 0; rr < GTR; ++rr) acc += pa[rr] * pb[rr];
-                        if (h == 0) g0 += acc;
-                        else g1 += acc;
-                    }
-                    __syncthreads();
-                }
-        }
-        for (int t = tid, h = 0; t < ntk; t += CT, ++h)
-            a.gram[(size_t(c) * GRAM_TASKS + t) * a.nbc_max + lb] = h == 0 ? g0 : g1;
-    }
-    grid.sync();
-    __syncwarp();   // lane 0 spun in the barrier: reconverge before warp-synchronous code
-    STAMP(stamp++);
-    // distributed fixed-order reduction of the Gram partials
-    for (int gt = blockIdx.x * CT + tid; gt < nc * GRAM_TASKS; gt += nb * CT) {
-        const int cc = gt / GRAM_TASKS, t = gt - cc * GRAM_TASKS;
-        const int k = kcs[cc];
-        if (t >= k * (2 * k + 1)) continue;
-        const int nbcc = (nb - cc + nc - 1) / nc;
-        double acc = 0.0;
-        for (int b = 0; b < nbcc; ++b) acc += a.gram[(size_t(cc) * GRAM_TASKS + t) * a.nbc_max + b];
-        a.gram_tot[gt] = acc;
-    }
-    grid.sync();
-    __syncwarp();   // lane 0 spun in the barrier: reconverge before warp-synchronous code
-    STAMP(stamp++);
-    // block 0: one warp per component solves the k x k Ritz problem
+    // The combine below reads only own rows (written by this thread), so no barrier is needed before the
+    // Ritz step: every Gram row was reduced to per-block partials at its step's last barrier.
+    // block 0: fixed-order reduction of the Gram partials (one thread per entry, scaled by the
+    // normalisation of its row), then one warp per component solves the k x k Ritz problem
     if (blockIdx.x == 0) {
+        for (int e = tid; e < nc * KMAX * GW; e += CT) {
+            const int cc = e / (KMAX * GW), rem = e - cc * (KMAX * GW), jr = rem / GW, v = rem - jr * GW;
+            if (jr >= kcs[cc]) continue;
+            const int kind = v < KMAX ? 0 : (v < 2 * KMAX ? 1 : 2), t = kind == 0 ? v : v - KMAX;
+            if (kind < 2 && t > jr) continue;
+            const int nbcc = (nb - cc + nc - 1) / nc;
+            const double* pg = a.gram + ((size_t(cc) * KMAX + jr) * GW + v) * a.nbc_max;
+            double acc = 0.0;
+            for (int b = 0; b < nbcc; ++b) acc += pg[b];
+            const double sj = sclh[cc][jr];
+            LzState& zs = P.lz[cc];
+            if (kind == 2) {
+                zs.wr[jr] = sj * acc;
+            } else {
+                const double g = (t == jr ? sj * sj : sj) * acc;
+                double* G = kind == 0 ? zs.A : zs.B;
+                G[jr * KMAX + t] = g;
+                G[t * KMAX + jr] = g;
+            }
+        }
+        __syncthreads();
+        STAMP(stamp++);
         const int w = tid >> 5, lane = tid & 31;
         double* ws = dsm + size_t(w) * (4 * KMAX * (KMAX + 1) + 2 * KMAX + 4 * KMAX);
         if (w < nc) {
             LzState& zs = P.lz[w];
-            const int k = kcs[w], nz = 2 * k + 1;
-            for (int idx = lane; idx < k * k; idx += 32) {
-                const int i = idx / k, jj = idx - i * k;
-                zs.A[i * KMAX + jj] = a.gram_tot[w * GRAM_TASKS + i * nz + jj];
-                zs.B[i * KMAX + jj] = a.gram_tot[w * GRAM_TASKS + i * nz + k + jj];
-            }
-            if (lane < k) zs.wr[lane] = a.gram_tot[w * GRAM_TASKS + lane * nz + 2 * k];
+            const int k = kcs[w];
             if (lane < KMAX) zs.coef[lane] = 0.0;
             zs.kc = k;
             zs.active = act[w];
@@ -831,7 +871,7 @@ bool prec_coop_prepare(const PrecDev& P, int device, CoopBuffers& B) {
     const int per_warp = stage ? 3 * mf + mfac : 3 * mf;
     size_t smem = size_t(CW) * per_warp * 8;
     smem = std::max(smem, size_t(ncmax) * 8);
-    smem = std::max(smem, size_t(3 * KMAX + 1) * (GTR + 1) * 8);
+    smem = std::max(smem, size_t(GW) * CT * 8);      // per-thread Gram accumulators
     smem = std::max(smem, size_t(RW) * TRI_N * 8);   // per-thread forward solutions of tridiagonal faces
     smem = std::max(smem, size_t(CW) * (4 * KMAX * (KMAX + 1) + 2 * KMAX + 4 * KMAX) * 8);
     if (smem > 200 * 1024) return false;
@@ -843,6 +883,8 @@ bool prec_coop_prepare(const PrecDev& P, int device, CoopBuffers& B) {
     if (const char* e = getenv("DE_COOP_BPS")) bps = std::max(1, atoi(e));
     const int nb = nsm * std::min(per_sm, bps);
     if (nb < P.ncomp) return false;
+    if (getenv("DE_VERBOSE"))
+        fprintf(stderr, "[de] k_prec_coop: %d blocks (%d resident/SM possible), %zu B smem\n", nb, per_sm, smem);
     B.nb = nb;
     B.smem = smem;
     B.stage = stage ? 1 : 0;
@@ -856,7 +898,6 @@ bool prec_coop_prepare(const PrecDev& P, int device, CoopBuffers& B) {
 
 size_t prec_coop_red_doubles(const CoopBuffers& B) { return size_t(2) * MAXC * NRED * B.nbc_max; }
 size_t prec_coop_gram_doubles(const CoopBuffers& B) { return size_t(MAXC) * GRAM_TASKS * B.nbc_max; }
-size_t prec_coop_gramtot_doubles() { return size_t(MAXC) * GRAM_TASKS; }
 
 int prec_apply_coop(const PrecDev& P, const CoopBuffers& B, const double* r, double* z, const PcgState* s,
                     cudaStream_t st) {
@@ -867,9 +908,9 @@ int prec_apply_coop(const PrecDev& P, const CoopBuffers& B, const double* r, dou
     a.s = s;
     a.red = B.red;
     a.gram = B.gram;
-    a.gram_tot = B.gram_tot;
     a.w1 = B.w1;
     a.mw1 = B.mw1;
+    a.lw1 = B.lw1;
     a.nbc_max = B.nbc_max;
     a.stage = B.stage;
     a.per_warp = B.per_warp;
