@@ -369,6 +369,119 @@ __device__ void elim_coop(cg::grid_group& grid, const CoopArgs& a, const ElimDev
     STAMP(stamp++);
 }
 
+// Circle-method position map for the parallel Jacobi ordering on M (even) slots: pairs are always the
+// fixed slots (2k, 2k+1); between rounds slot 0 stays and the others rotate t_1 -> t_2 -> .. -> t_{H-1} ->
+// b_{H-1} -> .. -> b_0 -> t_1 (t_i = slot 2i, b_i = slot 2i+1), so every pair meets once in M-1 rounds.
+// Returns the slot whose content moves INTO slot `pos`.
+__device__ __forceinline__ constexpr int circle_src(int pos, int M) {
+    const int H = M / 2;
+    if (pos == 0) return 0;
+    if ((pos & 1) == 0) {
+        const int i = pos / 2;
+        return i == 1 ? 1 : 2 * (i - 1);
+    }
+    const int i = (pos - 1) / 2;
+    return i == H - 1 ? 2 * (H - 1) : 2 * (i + 1) + 1;
+}
+
+// Cyclic parallel Jacobi on the symmetric n x n matrix C (smem, leading dim KMAX+1) with eigenvectors
+// accumulated into V (smem, starts as I). One warp; lane r < M holds row r of C and of V in registers,
+// slots >= n are decoupled ghosts. On return C's diagonal holds the eigenvalues and V's columns the
+// eigenvectors (same order: full sweeps return every slot to its place). Returns the sweep count.
+template <int M>
+__device__ int jacobi_reg(double* C, double* V, int n) {
+    constexpr int LDK = KMAX + 1, H = M / 2;
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    double c[M], v[M];
+#pragma unroll
+    for (int b = 0; b < M; ++b) {
+        c[b] = (lane < n && b < n) ? C[lane * LDK + b] : 0.0;
+        v[b] = lane == b ? 1.0 : 0.0;
+    }
+    const int srcl = lane < M ? circle_src(lane, M) : lane;
+    const bool even = (lane & 1) == 0;
+    int nsw = 0;
+    for (int sweep = 0; sweep < 30; ++sweep) {
+        double off = 0.0, dia = 0.0;
+#pragma unroll
+        for (int b = 0; b < M; ++b) {
+            const double x = lane < M ? c[b] * c[b] : 0.0;
+            if (b == lane) dia += x;
+            else off += x;
+        }
+        off = warp_sum(off);
+        dia = warp_sum(dia);
+        if (off <= 1e-30 * dia) break;
+        ++nsw;
+        const double thr = 1e-15 * sqrt(dia);
+        int rotated = 0;
+        for (int rnd = 0; rnd < M - 1; ++rnd) {
+            double diag = 0.0, offp = 0.0;
+#pragma unroll
+            for (int b = 0; b < M; ++b) {
+                if (b == lane) diag = c[b];
+                if (b == (lane ^ 1)) offp = c[b];
+            }
+            const double dq = __shfl_xor_sync(FULL, diag, 1);
+            double cs = 1.0, sn = 0.0;
+            if (even && lane < M && fabs(offp) > thr && fabs(offp) > 1e-300) {
+                // rotation zeroing C[p][q] (p = lane, q = lane + 1): t = tan of the angle, |t| <= 1
+                const double d = dq - diag, apq = offp;
+                const double rt = sqrt(d * d + 4.0 * apq * apq);
+                const double t = 2.0 * apq / (d >= 0.0 ? d + rt : d - rt);
+                cs = rsqrt(1.0 + t * t);
+                sn = t * cs;
+                rotated = 1;
+            }
+            cs = __shfl_sync(FULL, cs, lane & ~1);
+            sn = __shfl_sync(FULL, sn, lane & ~1);
+            // C <- C J and V <- V J: columns (2k, 2k+1) of this lane's rows
+#pragma unroll
+            for (int k = 0; k < H; ++k) {
+                const double ck = __shfl_sync(FULL, cs, 2 * k), sk = __shfl_sync(FULL, sn, 2 * k);
+                const double x0 = c[2 * k], x1 = c[2 * k + 1], y0 = v[2 * k], y1 = v[2 * k + 1];
+                c[2 * k] = ck * x0 - sk * x1;
+                c[2 * k + 1] = sk * x0 + ck * x1;
+                v[2 * k] = ck * y0 - sk * y1;
+                v[2 * k + 1] = sk * y0 + ck * y1;
+            }
+            // C <- J^T C: rows 2k (even lane) and 2k+1 (odd lane) combine
+#pragma unroll
+            for (int b = 0; b < M; ++b) {
+                const double o = __shfl_xor_sync(FULL, c[b], 1);
+                c[b] = even ? cs * c[b] - sn * o : sn * o + cs * c[b];
+            }
+            // next pairing: rows move between lanes, columns between registers (static map)
+#pragma unroll
+            for (int b = 0; b < M; ++b) c[b] = __shfl_sync(FULL, c[b], srcl);
+            double tc[M], tv[M];
+#pragma unroll
+            for (int b = 0; b < M; ++b) {
+                tc[b] = c[b];
+                tv[b] = v[b];
+            }
+#pragma unroll
+            for (int b = 0; b < M; ++b) {
+                c[b] = tc[circle_src(b, M)];
+                v[b] = tv[circle_src(b, M)];
+            }
+        }
+        if (!__any_sync(FULL, rotated)) break;   // every pair below threshold: converged
+    }
+    __syncwarp();
+    if (lane < n) {
+#pragma unroll
+        for (int b = 0; b < M; ++b)
+            if (b < n) {
+                if (b == lane) C[lane * LDK + b] = c[b];
+                V[lane * LDK + b] = v[b];
+            }
+    }
+    __syncwarp();
+    return nsw;
+}
+
 // One warp: generalized eigenproblem A y = theta B y (n <= KMAX) and coef = Y f(Theta) Y^T wr.
 // Returns false on a non-SPD B or a non-positive Ritz value (non-singular component).
 __device__ bool ritz_warp(const double* Ain, const double* Bin, const double* wr, int n, bool sing, double theta,
@@ -421,114 +534,19 @@ __device__ bool ritz_warp(const double* Ain, const double* Bin, const double* wr
         }
     }
     __syncwarp();
-    const int m = (n + 1) & ~1, npair = m / 2;
     if (tm && lane == 0) tm[1] = gtimer();
     int nsw = 0;
-    for (int sweep = 0; sweep < 30 && n > 1; ++sweep) {
-        ++nsw;
-        if (tm && sweep == 0 && lane == 0) tm[13] = clock64();
-        double off = 0.0, dia = 0.0;
-        if (lane < n)
-            for (int j = 0; j < n; ++j) {
-                const double v = C[lane * LDK + j];
-                if (j == lane) dia += v * v;
-                else off += v * v;
-            }
-        off = warp_sum(off);
-        dia = warp_sum(dia);
-        if (off <= 1e-30 * dia) break;
-        if (tm && sweep == 0 && lane == 0) tm[12] = clock64();
-        int rotated = 0;
-        for (int rnd = 0; rnd < m - 1; ++rnd) {
-            const bool fine = tm && sweep == 0 && rnd == 0 && lane == 0;
-            if (fine) tm[8] = clock64();
-            if (lane < npair) {
-                int p, q;
-                if (lane == 0) {
-                    p = m - 1;
-                    q = rnd;
-                } else {
-                    p = (rnd + lane) % (m - 1);
-                    q = (rnd - lane + (m - 1)) % (m - 1);
-                }
-                if (p > q) {
-                    const int t = p;
-                    p = q;
-                    q = t;
-                }
-                double cs = 1.0, sn = 0.0;
-                if (q < n) {
-                    const double apq = C[p * LDK + q];
-                    const double app = C[p * LDK + p], aqq = C[q * LDK + q];
-                    (void)app;
-                    (void)aqq;
-                    if (fabs(apq) > 1e-15 * sqrt(dia) && fabs(apq) > 1e-300) {   // else negligible vs ||C||
-                        rotated = 1;
-                        const double tau = (C[q * LDK + q] - C[p * LDK + p]) / (2.0 * apq);
-                        const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-                        cs = 1.0 / sqrt(1.0 + t * t);
-                        sn = t * cs;
-                    }
-                }
-                rot[lane] = cs;
-                rot[KMAX / 2 + lane] = sn;
-                rpq[lane] = p;
-                rpq[KMAX / 2 + lane] = q;
-            }
-            __syncwarp();
-            if (fine) tm[9] = clock64();
-            // the pairs of a round are disjoint: gather every operand first, then write (pipelined smem)
-            constexpr int NP = KMAX / 2;
-            int pp[NP], qq[NP];
-            double cs[NP], sn[NP];
-#pragma unroll
-            for (int t = 0; t < NP; ++t) {
-                const bool ok = t < npair;
-                pp[t] = ok ? rpq[t] : 0;
-                qq[t] = ok ? rpq[NP + t] : n;
-                cs[t] = ok ? rot[t] : 1.0;
-                sn[t] = ok ? rot[NP + t] : 0.0;
-            }
-            if (lane < n) {                                  // C <- C J and V <- V J (row `lane`)
-                double x0[NP], x1[NP], v0[NP], v1[NP];
-#pragma unroll
-                for (int t = 0; t < NP; ++t)
-                    if (qq[t] < n) {
-                        x0[t] = C[lane * LDK + pp[t]];
-                        x1[t] = C[lane * LDK + qq[t]];
-                        v0[t] = V[lane * LDK + pp[t]];
-                        v1[t] = V[lane * LDK + qq[t]];
-                    }
-#pragma unroll
-                for (int t = 0; t < NP; ++t)
-                    if (qq[t] < n) {
-                        C[lane * LDK + pp[t]] = cs[t] * x0[t] - sn[t] * x1[t];
-                        C[lane * LDK + qq[t]] = sn[t] * x0[t] + cs[t] * x1[t];
-                        V[lane * LDK + pp[t]] = cs[t] * v0[t] - sn[t] * v1[t];
-                        V[lane * LDK + qq[t]] = sn[t] * v0[t] + cs[t] * v1[t];
-                    }
-            }
-            __syncwarp();
-            if (fine) tm[10] = clock64();
-            if (lane < n) {                                  // C <- J^T C (column `lane`)
-                double x0[NP], x1[NP];
-#pragma unroll
-                for (int t = 0; t < NP; ++t)
-                    if (qq[t] < n) {
-                        x0[t] = C[pp[t] * LDK + lane];
-                        x1[t] = C[qq[t] * LDK + lane];
-                    }
-#pragma unroll
-                for (int t = 0; t < NP; ++t)
-                    if (qq[t] < n) {
-                        C[pp[t] * LDK + lane] = cs[t] * x0[t] - sn[t] * x1[t];
-                        C[qq[t] * LDK + lane] = sn[t] * x0[t] + cs[t] * x1[t];
-                    }
-            }
-            __syncwarp();
-            if (fine) tm[11] = clock64();
+    if (n > 1) {
+        switch ((n + 1) & ~1) {
+            case 2: nsw = jacobi_reg<2>(C, V, n); break;
+            case 4: nsw = jacobi_reg<4>(C, V, n); break;
+            case 6: nsw = jacobi_reg<6>(C, V, n); break;
+            case 8: nsw = jacobi_reg<8>(C, V, n); break;
+            case 10: nsw = jacobi_reg<10>(C, V, n); break;
+            case 12: nsw = jacobi_reg<12>(C, V, n); break;
+            case 14: nsw = jacobi_reg<14>(C, V, n); break;
+            default: nsw = jacobi_reg<16>(C, V, n); break;
         }
-        if (!__any_sync(0xffffffffu, rotated)) break;   // every pair below threshold: converged
     }
     if (tm && lane == 0) {
         tm[2] = gtimer();

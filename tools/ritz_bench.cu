@@ -54,11 +54,12 @@ int main() {
         long long c;
         cudaMemcpy(t, tm, sizeof t, cudaMemcpyDeviceToHost);
         cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
+        double cf[KMAX];
+        cudaMemcpy(cf, coef, sizeof cf, cudaMemcpyDeviceToHost);
+        printf("coef0..2 %.15e %.15e %.15e\n", cf[0], cf[1], cf[2]);
         printf("err %s cycles %lld setup %.1f us jacobi %.1f us sweeps %llu final %.1f us\n",
                cudaGetErrorString(cudaGetLastError()), c, (t[1] - t[0]) / 1e3, (t[2] - t[1]) / 1e3, t[4],
                (t[3] - t[2]) / 1e3);
-        printf("  sweep0 offdia %lld cyc; round0: rot %lld  CJ %lld  JtC %lld cyc\n", (long long)(t[12] - t[13]),
-               (long long)(t[9] - t[8]), (long long)(t[10] - t[9]), (long long)(t[11] - t[10]));
     }
     return 0;
 }
