@@ -624,17 +624,19 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
         scl[tid] = 1.0;
     }
     __syncthreads();
-    // ---- s = M^-1 r (exact)
-    elim_coop(grid, a, P.eM, P.rf, scl, P.s, dsm, c, lb, nbc, stamp);
-    // ---- Ms, ||s||_M; q_1 = s / ||s||_M, rhs of the next solve v = M q_1 = Ms / ||s||_M
+    // Basis vectors are stored unnormalised (W_t = sclh_t * Wraw_t, likewise M W_t and L W_t): every
+    // consumer folds sclh_t into its coefficients, so no normalisation pass over the rows is needed.
+    // ---- s = M^-1 r (exact) = Wraw_0
+    elim_coop(grid, a, P.eM, P.rf, scl, P.W, dsm, c, lb, nbc, stamp);
+    // ---- Ms, Ls, ||s||_M; q_1 = s / ||s||_M; rhs of the next solve M q_1 = Ms / ||s||_M
     ZERO_VALS();
     double* gacc = dsm;   // per-thread Gram accumulators [GW][CT] (dsm is free outside face solves / Ritz)
     gram_zero(gacc);
     for (int64_t i = r0; i < hi; i += rs) {
         double m, l, unused_h[1] = {0.0};
-        corr_spmv<true>(P.M, P.L, i, P.s, P.W, nf, unused_h, 0, m, l);
-        const double sv = P.s[i];
-        P.Mw[i] = m;
+        corr_spmv<true>(P.M, P.L, i, P.W, P.W, nf, unused_h, 0, m, l);
+        const double sv = P.W[i];
+        P.MW[i] = m;
         P.LW[i] = l;
         vals[0] += sv * m;
         gacc[0 * CT + tid] += sv * l;            // G_L[0][0] (unscaled)
@@ -655,15 +657,9 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
         sclh[tid][0] = scl[tid];
     }
     __syncthreads();
-    if (act[c])
-        for (int64_t i = r0; i < hi; i += rs) {     // q_1, L q_1, M q_1 (kept for Rayleigh-Ritz)
-            P.W[i] = P.s[i] * scl[c];
-            P.LW[i] *= scl[c];
-            P.MW[i] = P.Mw[i] * scl[c];
-        }
     // ---- inverse Lanczos steps
     for (int j = 1; j < P.kmax; ++j) {
-        elim_coop(grid, a, P.eK, P.Mw, scl, P.w, dsm, c, lb, nbc, stamp);   // w = K^-1 M q_j
+        elim_coop(grid, a, P.eK, j == 1 ? P.MW : P.Mw, scl, P.w, dsm, c, lb, nbc, stamp);   // w = K^-1 M q_j
         const bool part = act[c] && !brk[c];
         const int kc = kcs[c];
         // A: (M w, L w) by one SpMV over the shared pattern; ||w||_M^2 and h_t = W_t . M w
@@ -688,7 +684,7 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
         read_totals(a, pp, 1 + kc, nb, tot);   // every component's first 1+kc (kc uniform enough: use own)
         pp ^= 1;
         if (tid < nc) nb2v[tid] = tot[tid][0];
-        if (tid < KMAX) hsm[c][tid] = tid < kc ? tot[c][1 + tid] : 0.0;
+        if (tid < KMAX) hsm[c][tid] = tid < kc ? tot[c][1 + tid] * sclh[c][tid] * sclh[c][tid] : 0.0;
         __syncthreads();
         // B: w1 = w - W h; M w1 = M w - (M W) h and L w1 = L w - (L W) h by linearity (own rows only);
         // dots h'_t = W_t . M w1
@@ -722,7 +718,7 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
     STAMP(stamp++);
         read_totals(a, pp, kc > 0 ? kc : 1, nb, tot);
         pp ^= 1;
-        if (tid < KMAX) hsm[c][tid] = tid < kc ? tot[c][tid] : 0.0;
+        if (tid < KMAX) hsm[c][tid] = tid < kc ? tot[c][tid] * sclh[c][tid] * sclh[c][tid] : 0.0;
         __syncthreads();
         // C: w2 = w1 - W h' with M w2, L w2 by linearity (M w2 is the next solve's rhs); ||w2||_M^2; row j of
         // the Rayleigh-Ritz Gram matrices before normalisation: w2.(L W_t), w2.(M W_t) (t < j), w2.L w2,
@@ -749,7 +745,8 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
                     m -= hsm[c][t] * mt[t];
                     l -= hsm[c][t] * lt[t];
                 }
-                P.w[i] = x;
+                P.W[size_t(j) * nf + i] = x;
+                P.MW[size_t(j) * nf + i] = m;
                 P.Mw[i] = m;
                 P.LW[size_t(j) * nf + i] = l;
                 vals[0] += x * m;
@@ -791,12 +788,6 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
             }
         }
         __syncthreads();
-        if (part && kcs[c] == j + 1)
-            for (int64_t i = r0; i < hi; i += rs) {
-                P.W[size_t(j) * nf + i] = P.w[i] * scl[c];
-                P.LW[size_t(j) * nf + i] *= scl[c];
-                P.MW[size_t(j) * nf + i] = P.Mw[i] * scl[c];
-            }
     }
     // The combine below reads only own rows (written by this thread), so no barrier is needed before the
     // Ritz step: every Gram row was reduced to per-block partials at its step's last barrier.
@@ -817,7 +808,7 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
             if (kind == 2) {
                 zs.wr[jr] = sj * acc;
             } else {
-                const double g = (t == jr ? sj * sj : sj) * acc;
+                const double g = sj * sclh[cc][t] * acc;   // (sclh_j Wraw_j)^T L (sclh_t Wraw_t)
                 double* G = kind == 0 ? zs.A : zs.B;
                 G[jr * KMAX + t] = g;
                 G[t * KMAX + jr] = g;
@@ -860,13 +851,15 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
     grid.sync();
     __syncwarp();   // lane 0 spun in the barrier: reconverge before warp-synchronous code
     STAMP(stamp++);
-    // z = sum_t coef_t W_t, scattered back to interface order
+    // z = sum_t coef_t W_t = sum_t (coef_t sclh_t) Wraw_t, scattered back to interface order
     {
         const int k = kcs[c];
+        if (tid < KMAX) hsm[c][tid] = tid < k ? P.lz[c].coef[tid] * sclh[c][tid] : 0.0;
+        __syncthreads();
         for (int64_t i = r0; i < hi; i += rs) {
             double acc = 0.0;
             if (act[c])
-                for (int t = 0; t < k; ++t) acc += P.lz[c].coef[t] * P.W[size_t(t) * nf + i];
+                for (int t = 0; t < k; ++t) acc += hsm[c][t] * P.W[size_t(t) * nf + i];
             a.z[P.cmap[i]] = acc;
         }
     }

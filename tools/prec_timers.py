@@ -5,6 +5,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 from synthetic import make_config
 from paper_1501_06211_b200 import binding as B
+if os.environ.get("AB_LIB"):   # A/B experiments: load another build of libde.so
+    B.LIB_PATH = os.environ["AB_LIB"]
 name = sys.argv[1] if len(sys.argv) > 1 else "c5"
 p = make_config(name)
 S = B.Solver.from_problem(p, device=0)

@@ -4,6 +4,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 from synthetic import make_config
 from paper_1501_06211_b200 import binding as B
+if os.environ.get("AB_LIB"):   # A/B experiments: load another build of libde.so
+    B.LIB_PATH = os.environ["AB_LIB"]
 from oracle.fem import element_stiffness, simp_modulus, element_dofs, true_relres
 
 name = sys.argv[1] if len(sys.argv) > 1 else "c5"
