@@ -121,6 +121,8 @@ typedef struct {
     int32_t iterations_pass1; /* PCG iterations before iterative refinement */
     int32_t schur_explicit;  /* 1 if the PCG loop applies explicit local Schur complements */
     double bytes_schur_explicit; /* algorithmic bytes of one explicit S apply: sum_s n_Gamma,s^2 * 8 + vectors */
+    double bytes_prec;       /* algorithmic bytes of one preconditioner application (k_prec_coop; per-phase
+                                streaming model of DESIGN.md "Kernels and their rooflines"), 0 if none */
 } de_stats_t;
 
 /* Fill *opt with defaults (theta 0.5, k 10, inner_mode 1, max_iter 20000, FR, 1 rank). */
@@ -188,6 +190,9 @@ de_status_t de_nccl_unique_id(void* out128);
 de_status_t de_set_profiling(de_ctx_t* ctx, int32_t on);
 /* Average device time (ms) of one launch of the Schur-apply kernel over the last solve. */
 de_status_t de_get_kernel_time(const de_ctx_t* ctx, double* ms_schur_per_launch, int64_t* launches);
+/* Average device time (ms) of one preconditioner application (k_prec_coop, or the multi-kernel path)
+   over the last solve with profiling on; same event-pair method inside the captured PCG graph. */
+de_status_t de_get_prec_time(const de_ctx_t* ctx, double* ms_prec_per_launch, int64_t* launches);
 
 void de_destroy(de_ctx_t* ctx);
 const char* de_last_error(void);

@@ -52,7 +52,8 @@ class de_stats_t(C.Structure):
                 ("n_gamma_c", C.c_int64 * 3),
                 ("bytes_schur", C.c_double), ("kernels_launched", C.c_int64),
                 ("iterations_pass1", C.c_int32), ("schur_explicit", C.c_int32),
-                ("bytes_schur_explicit", C.c_double)]
+                ("bytes_schur_explicit", C.c_double),
+                ("bytes_prec", C.c_double)]
 
 
 _lib = None
@@ -88,6 +89,7 @@ def lib():
         "de_nccl_unique_id": (I32, [P]),
         "de_set_profiling": (I32, [P, I32]),
         "de_get_kernel_time": (I32, [P, C.POINTER(D), C.POINTER(I64)]),
+        "de_get_prec_time": (I32, [P, C.POINTER(D), C.POINTER(I64)]),
         "de_destroy": (None, [P]),
         "de_last_error": (C.c_char_p, []),
     }
@@ -240,6 +242,12 @@ def de_set_profiling(ctx, on: bool):
 def de_get_kernel_time(ctx):
     ms, n = C.c_double(), C.c_int64()
     _check(lib().de_get_kernel_time(ctx, C.byref(ms), C.byref(n)))
+    return ms.value, n.value
+
+
+def de_get_prec_time(ctx):
+    ms, n = C.c_double(), C.c_int64()
+    _check(lib().de_get_prec_time(ctx, C.byref(ms), C.byref(n)))
     return ms.value, n.value
 
 

@@ -111,8 +111,8 @@ struct de_ctx {
     // profiling
     bool profiling = false;
     std::vector<cudaEvent_t> ev;
-    double prof_ms = 0.0;
-    int64_t prof_n = 0;
+    double prof_ms = 0.0, prof_ms_prec = 0.0;
+    int64_t prof_n = 0, prof_n_prec = 0;
     int64_t launches = 0;
     double* d_ubuf2 = nullptr;
     bool explicit_schur = false;
@@ -231,7 +231,8 @@ de_status_t precond(de_ctx* c, const double* r, double* z, const PcgState* s, in
 }
 
 // one PCG iteration (all on c->st; capturable)
-de_status_t pcg_iteration(de_ctx* c, int* nl, cudaEvent_t e0, cudaEvent_t e1) {
+de_status_t pcg_iteration(de_ctx* c, int* nl, cudaEvent_t e0, cudaEvent_t e1, cudaEvent_t e2 = nullptr,
+                          cudaEvent_t e3 = nullptr) {
     const int64_t nG = c->hs.n_G;
     int n = 0;
     if (e0) cudaEventRecordWithFlags(e0, c->st, cudaEventRecordExternal);   // a real node when captured
@@ -245,7 +246,9 @@ de_status_t pcg_iteration(de_ctx* c, int* nl, cudaEvent_t e0, cudaEvent_t e1) {
     launch_pcg_update_xr(c->d_x, c->d_r, pr ? c->d_rold : nullptr, c->d_p, c->d_q, nG, c->rb, c->d_state, c->st);
     n += 2;
     int np = 0;
+    if (e2) cudaEventRecordWithFlags(e2, c->st, cudaEventRecordExternal);
     TRY(precond(c, c->d_r, c->d_z, c->d_state, &np));
+    if (e3) cudaEventRecordWithFlags(e3, c->st, cudaEventRecordExternal);
     n += np;
     launch_pcg_rz(c->d_r, c->d_z, c->d_rold, nG, pr ? 1 : 0, c->rb, c->d_state, c->st);
     launch_pcg_update_p(c->d_p, c->d_z, nG, c->d_state, c->st);
@@ -261,16 +264,17 @@ de_status_t build_graph(de_ctx* c) {
     }
     const int ni = std::max(1, c->opt.check_every);
     const bool prof = c->profiling;
-    if (prof && int(c->ev.size()) < 2 * ni) {
+    if (prof && int(c->ev.size()) < 4 * ni) {
         for (auto e : c->ev) cudaEventDestroy(e);
-        c->ev.assign(2 * ni, nullptr);
+        c->ev.assign(4 * ni, nullptr);
         for (auto& e : c->ev) DE_CUDA(cudaEventCreate(&e));
     }
     cudaGraph_t g;
     DE_CUDA(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
     de_status_t s = DE_OK;
     for (int i = 0; i < ni && s == DE_OK; ++i)
-        s = pcg_iteration(c, &c->launches_per_iter, prof ? c->ev[2 * i] : nullptr, prof ? c->ev[2 * i + 1] : nullptr);
+        s = pcg_iteration(c, &c->launches_per_iter, prof ? c->ev[4 * i] : nullptr, prof ? c->ev[4 * i + 1] : nullptr,
+                          prof ? c->ev[4 * i + 2] : nullptr, prof ? c->ev[4 * i + 3] : nullptr);
     cudaError_t e = cudaStreamEndCapture(c->st, &g);
     if (s != DE_OK) return s;
     DE_CUDA(e);
@@ -306,9 +310,13 @@ de_status_t run_loop(de_ctx* c, PcgState& hsv) {
             const int ran = std::min(hsv.it - it_before, c->graph_iters);
             for (int i = 0; i < ran; ++i) {
                 float ms = 0.f;
-                if (cudaEventElapsedTime(&ms, c->ev[2 * i], c->ev[2 * i + 1]) == cudaSuccess) {
+                if (cudaEventElapsedTime(&ms, c->ev[4 * i], c->ev[4 * i + 1]) == cudaSuccess) {
                     c->prof_ms += ms;
                     c->prof_n += 1;
+                }
+                if (cudaEventElapsedTime(&ms, c->ev[4 * i + 2], c->ev[4 * i + 3]) == cudaSuccess) {
+                    c->prof_ms_prec += ms;
+                    c->prof_n_prec += 1;
                 }
             }
         }
@@ -473,6 +481,46 @@ de_status_t upload_prec(de_ctx* c) {
         c->use_coop = true;
     }
     return DE_OK;
+}
+
+// Algorithmic bytes of one preconditioner application: every
+// phase reads its operands and writes its results once, neighbour values of an SpMV come from cache
+// (counted once as the vector), k = lanczos_k basis vectors, no breakdown.
+double elim_bytes_model(const HElim& E, bool tri) {
+    const double nfn = double(E.face_nodes.size());
+    double b = 0.0;
+    if (tri)   // per face solve: forward + backward read (node, 1/L_jj, L_j+1,j); rhs read; result write
+        b += 2.0 * nfn * (2.0 * (4 + 8 + 8) + 8 + 8);
+    else       // per face solve: the [L | M] band copies, node ids, rhs read, result write
+        b += 2.0 * (double(E.face_fac.size()) * 8.0 + nfn * (4 + 8 + 8));
+    b += double(E.XFC.val.size()) * 12.0;                                   // X_FC x_C in the second face solve
+    b += double(E.XCF.val.size()) * (12.0 + 8.0) + double(E.ncross) * (4 + 4 + 8 + 8 + 8);   // t_C
+    for (size_t cc = 0; cc + 1 < E.sc_off.size(); ++cc) {
+        const double nc = double(E.cross_comp_off[cc + 1] - E.cross_comp_off[cc]);
+        b += nc * nc * 8.0;                                                 // dense S_C^-1 rows
+    }
+    return b;
+}
+
+double prec_bytes_model(const HostSetup& hs, int k) {
+    const double n = double(hs.comp_off[hs.ncomp]), nnz = double(hs.M.val.size()), d = 8.0;
+    bool tri = true;
+    for (const HElim* E : {&hs.elimK, &hs.elimM})
+        for (int F = 0; F < E->nfaces && tri; ++F) {
+            const int o = E->face_off[F], nf = E->face_off[F + 1] - o;
+            if (E->face_band[F] > 1 || nf > TRI_N) tri = false;
+        }
+    const double spmv = nnz * (4 + 8 + 8) + (n + 1) * 4 + n * d;            // M and L values, shared cols, x
+    double b = n * (4 + d + d);                                             // gather r_c
+    b += elim_bytes_model(hs.elimM, tri) + double(k - 1) * elim_bytes_model(hs.elimK, tri);
+    b += spmv + n * d * 3;                                                  // seed: Ms, Ls, s.r
+    for (int j = 1; j < k; ++j) {
+        b += spmv + n * d * (j + 2);                                        // A: M w, L w, W^T M w
+        b += n * d * (3.0 * j + 3 + 3);                                     // B: w1, M w1, L w1
+        b += n * d * (3.0 * j + 4 + 3);                                     // C: w2, M w2, L w2, Gram row j
+    }
+    b += n * d * k + n * (4 + d);                                           // z = W coef, scatter
+    return b;
 }
 
 de_status_t setup_impl(const de_mesh_t* mesh, const double* density, double E0, double Emin, double p,
@@ -698,6 +746,7 @@ de_status_t setup_impl(const de_mesh_t* mesh, const double* density, double E0, 
                     double(c->n_local_I + c->nsl) * 4.0;
     S.bytes_iter = fb + double(c->n_ig + c->n_gx) * 12.0 + double(c->n_local_G) * 8.0 * 3.0 +
                    double(hs.n_G) * 8.0 * 11.0;
+    S.bytes_prec = c->have_prec ? prec_bytes_model(hs, c->P.kmax) : 0.0;
     return DE_OK;
 }
 
@@ -1161,6 +1210,8 @@ de_status_t de_set_profiling(de_ctx_t* c, int32_t on) {
     c->profiling = on != 0;
     c->prof_ms = 0.0;
     c->prof_n = 0;
+    c->prof_ms_prec = 0.0;
+    c->prof_n_prec = 0;
     return DE_OK;
 }
 
@@ -1178,6 +1229,16 @@ de_status_t de_get_kernel_time(const de_ctx_t* c, double* ms, int64_t* launches)
     }
     if (ms) *ms = c->prof_n ? c->prof_ms / double(c->prof_n) : 0.0;
     if (launches) *launches = c->prof_n;
+    return DE_OK;
+}
+
+de_status_t de_get_prec_time(const de_ctx_t* c, double* ms, int64_t* launches) {
+    if (!c) {
+        set_error("null context");
+        return DE_EINVAL;
+    }
+    if (ms) *ms = c->prof_n_prec ? c->prof_ms_prec / double(c->prof_n_prec) : 0.0;
+    if (launches) *launches = c->prof_n_prec;
     return DE_OK;
 }
 

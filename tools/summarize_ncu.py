@@ -40,7 +40,7 @@ def full(rep, out_md, title, algo_bytes=None):
         f.write(f"# {title}\n\n`ncu --set full --clock-control none --import-source on`, report `{rep}`.\n\n")
         f.write(f"* duration: {t} {tu}\n* dram read: {rd} {rdu}, write: {wr} {wru} -> traffic {traffic/1e9:.3f} GB/launch\n")
         if algo_bytes:
-            f.write(f"* algorithmic bytes (1 pass over the factor band + ring + vectors): {algo_bytes/1e9:.3f} GB "
+            f.write(f"* algorithmic bytes per launch (DESIGN.md model): {algo_bytes/1e9:.3f} GB "
                     f"-> traffic / algorithmic = {traffic/algo_bytes:.2f}\n")
         f.write("\n| section | metric | value | unit |\n|---|---|---:|---|\n")
         for row in d[1:]:
@@ -50,10 +50,19 @@ def full(rep, out_md, title, algo_bytes=None):
 
 
 if __name__ == '__main__':
+    bench = json.loads(open('gpurun_out/bench.json').read().strip().splitlines()[-1])
+    algo = {bench['roofline']['kernel'].split()[0]: bench['roofline']['algorithmic_bytes_per_launch'],
+            bench['roofline_secondary']['kernel'].split()[0]: bench['roofline_secondary']['algorithmic_bytes_per_launch']}
     launches('gpurun_out/launches_bench.csv', 'profiles/round1_launches_bench_c5.md',
              'Round 1 launch list: `bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline` (config c5)')
-    tr = full('gpurun_out/schur_bench.ncu-rep', 'profiles/round1_schur_local_c5.md',
-              'Round 1: k_schur_local (C2 Schur apply), config c5, 2048 subdomains', algo_bytes=2285200320.0)
-    json.dump({"config": "c5", "n_gpus": 1, "kernel": "k_schur_local", "dram_bytes_per_launch": tr,
-               "source": "profiles/round1_schur_local_c5.md"}, open('profiles/schur_traffic.json', 'w'), indent=1)
+    tr = {}
+    tr['k_prec_coop'] = full('gpurun_out/prec_coop.ncu-rep', 'profiles/round1_prec_coop_c5.md',
+                             'Round 1: k_prec_coop (C5 preconditioner, one cooperative launch), config c5',
+                             algo_bytes=algo['k_prec_coop'])
+    tr['k_schur_explicit'] = full('gpurun_out/schur_explicit.ncu-rep', 'profiles/round1_schur_explicit_c5.md',
+                                  'Round 1: k_schur_explicit (C2 explicit local Schur apply), config c5',
+                                  algo_bytes=algo['k_schur_explicit'])
+    json.dump({"config": "c5", "n_gpus": 1, "dram_bytes_per_launch": tr,
+               "source": ["profiles/round1_prec_coop_c5.md", "profiles/round1_schur_explicit_c5.md"]},
+              open('profiles/traffic.json', 'w'), indent=1)
     print('traffic', tr)
