@@ -440,6 +440,47 @@ de_status_t upload_prec(de_ctx* c) {
             TRY(dupload(c, &D.tri_xj, txj));
             TRY(dupload(c, &D.tri_xc, txc));
             TRY(dupload(c, &D.tri_xv, txv));
+            // G_F = X_FF^-1 X_FC column by column (the same tridiagonal factor), per flat skeleton index
+            const size_t nfl = size_t(hs.comp_off[hs.ncomp]);
+            std::vector<int32_t> gc0(nfl, 0), gc1(nfl, 0);
+            std::vector<double> gv0(nfl, 0.0), gv1(nfl, 0.0);
+            std::vector<double> g;
+            for (int F = 0; F < E.nfaces; ++F) {
+                const int o = E.face_off[F], n = E.face_off[F + 1] - o;
+                const size_t grp = F / 32, lane = F % 32;
+                for (int k = 0; k < 2; ++k) {
+                    const int jx = txj[2 * F + k];
+                    if (jx < 0) continue;
+                    g.assign(n, 0.0);
+                    double prev = 0.0, lprev = 0.0;
+                    for (int j = 0; j < n; ++j) {
+                        const size_t at = (grp * TRI_N + j) * 32 + lane;
+                        prev = ((j == jx ? txv[2 * F + k] : 0.0) - lprev * prev) * tinv[at];
+                        g[j] = prev;
+                        lprev = tsub[at];
+                    }
+                    double nxt = 0.0;
+                    for (int j = n - 1; j >= 0; --j) {
+                        const size_t at = (grp * TRI_N + j) * 32 + lane;
+                        nxt = (g[j] - tsub[at] * nxt) * tinv[at];
+                        g[j] = nxt;
+                    }
+                    for (int j = 0; j < n; ++j) {
+                        const int fl = E.face_nodes[o + j];
+                        (k == 0 ? gc0 : gc1)[fl] = txc[2 * F + k];
+                        (k == 0 ? gv0 : gv1)[fl] = g[j];
+                    }
+                }
+            }
+            for (int ci = 0; ci < E.ncross; ++ci) {
+                gc0[E.cross_flat[ci]] = ci;
+                gv0[E.cross_flat[ci]] = -1.0;
+            }
+            TRY(dupload(c, &D.g_c0, gc0));
+            TRY(dupload(c, &D.g_c1, gc1));
+            TRY(dupload(c, &D.g_v0, gv0));
+            TRY(dupload(c, &D.g_v1, gv1));
+            D.fuse = getenv("DE_NO_E3_FUSE") ? 0 : 1;
         }
         return check_launch();
     };
@@ -452,6 +493,7 @@ de_status_t upload_prec(de_ctx* c) {
     TRY(dalloc(c, &P.w, nf));
     TRY(dalloc(c, &P.Mw, nf));
     TRY(dalloc(c, &P.y, 2 * nf + 16));
+    DE_CUDA(cudaMemsetAsync(P.y, 0, (2 * nf + 16) * sizeof(double), c->st));   // y stays 0 on cross points
     TRY(dalloc(c, &P.zf, nf));
     TRY(dalloc(c, &P.W, nf * KMAX));
     TRY(dalloc(c, &P.LW, nf * KMAX));

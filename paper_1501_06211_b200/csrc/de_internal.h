@@ -163,6 +163,12 @@ struct ElimDev {
     int32_t* tri_xj;             // [2*nfaces] node index j of cross coupling k (or -1)
     int32_t* tri_xc;             // [2*nfaces] cross index of coupling k
     double* tri_xv;              // [2*nfaces] X_{F_j, c}
+    // E3 folded into the consumer (tri only): x_i = y_i - g_v0[i] xC[g_c0[i]] - g_v1[i] xC[g_c1[i]] for every
+    // flat skeleton index i, with G_F = X_FF^-1 X_FC on face nodes and (v0, c0) = (-1, own cross index), y_i = 0
+    // on cross points
+    int32_t fuse;
+    int32_t *g_c0, *g_c1;
+    double *g_v0, *g_v1;
 };
 constexpr int TRI_N = 32;
 

@@ -156,6 +156,32 @@ __device__ __forceinline__ void corr_spmv(const CsrDev& M, const CsrDev& L, int6
     yL = al;
 }
 
+// x_i of the last exact elimination when its third phase is folded into the consumer (ElimDev::fuse):
+// face node y_i - G_i x_C, cross point x_C (v0 = -1, y_i = 0)
+__device__ __forceinline__ double elim_value(const ElimDev& E, int64_t i, const double* __restrict__ y,
+                                             const double* __restrict__ xC) {
+    return y[i] - E.g_v0[i] * xC[E.g_c0[i]] - E.g_v1[i] * xC[E.g_c1[i]];
+}
+
+// (M x)_i and (L x)_i with x = elim_value(E, .) (M and L share one sparsity pattern); returns x_i
+__device__ __forceinline__ double spmv_elim(const CsrDev& M, const CsrDev& L, int64_t i, const ElimDev& E,
+                                            const double* __restrict__ y, const double* __restrict__ xC,
+                                            double& yM, double& yL) {
+    const int e0 = M.ptr[i], e1 = M.ptr[i + 1];
+    double am = 0.0, al = 0.0, xi = 0.0;
+    for (int e = e0; e < e1; ++e) {
+        const int col = M.col[e];
+        const double x = elim_value(E, col, y, xC);
+        am += M.val[e] * x;
+        al += L.val[e] * x;
+        if (col == i) xi = x;
+    }
+    if (e0 == e1) xi = elim_value(E, i, y, xC);
+    yM = am;
+    yL = al;
+    return xi;
+}
+
 // sum_t h_t W_t[i] with all loads issued up front
 __device__ __forceinline__ double basis_comb(const double* __restrict__ W, int64_t nflat, int64_t i, const double* h,
                                              int nt) {
@@ -357,6 +383,7 @@ __device__ void elim_coop(cg::grid_group& grid, const CoopArgs& a, const ElimDev
     grid.sync();
     __syncwarp();   // lane 0 spun in the barrier: reconverge before warp-synchronous code
     STAMP(stamp++);
+    if (E.tri && E.fuse) return;   // x_F = y_F - G_F x_C is formed by the consumer phase (elim_value)
     tf0 = clock64();
     if (E.tri) {
         if (w > 0)
@@ -632,10 +659,16 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
     ZERO_VALS();
     double* gacc = dsm;   // per-thread Gram accumulators [GW][CT] (dsm is free outside face solves / Ritz)
     gram_zero(gacc);
+    const bool fuseM = P.eM.tri && P.eM.fuse;
     for (int64_t i = r0; i < hi; i += rs) {
-        double m, l, unused_h[1] = {0.0};
-        corr_spmv<true>(P.M, P.L, i, P.W, P.W, nf, unused_h, 0, m, l);
-        const double sv = P.W[i];
+        double m, l, sv, unused_h[1] = {0.0};
+        if (fuseM) {
+            sv = spmv_elim(P.M, P.L, i, P.eM, P.y, P.y + nf, m, l);
+            P.W[i] = sv;
+        } else {
+            corr_spmv<true>(P.M, P.L, i, P.W, P.W, nf, unused_h, 0, m, l);
+            sv = P.W[i];
+        }
         P.MW[i] = m;
         P.LW[i] = l;
         vals[0] += sv * m;
@@ -658,6 +691,7 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
     }
     __syncthreads();
     // ---- inverse Lanczos steps
+    const bool fuseK = P.eK.tri && P.eK.fuse;
     for (int j = 1; j < P.kmax; ++j) {
         elim_coop(grid, a, P.eK, j == 1 ? P.MW : P.Mw, scl, P.w, dsm, c, lb, nbc, stamp);   // w = K^-1 M q_j
         const bool part = act[c] && !brk[c];
@@ -666,11 +700,17 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
         ZERO_VALS();
         if (part)
             for (int64_t i = r0; i < hi; i += rs) {
-                double m, l, unused_h[1] = {0.0};
-                corr_spmv<true>(P.M, P.L, i, P.w, P.W, nf, unused_h, 0, m, l);
+                double m, l, wi, unused_h[1] = {0.0};
+                if (fuseK) {
+                    wi = spmv_elim(P.M, P.L, i, P.eK, P.y, P.y + nf, m, l);
+                    P.w[i] = wi;
+                } else {
+                    corr_spmv<true>(P.M, P.L, i, P.w, P.W, nf, unused_h, 0, m, l);
+                    wi = P.w[i];
+                }
                 a.mw1[i] = m;
                 a.lw1[i] = l;
-                vals[0] += P.w[i] * m;
+                vals[0] += wi * m;
                 double wt[KMAX];
 #pragma unroll
                 for (int t = 0; t < KMAX; ++t) wt[t] = t < kc ? P.W[size_t(t) * nf + i] : 0.0;
