@@ -408,6 +408,8 @@ de_status_t upload_prec(de_ctx* c) {
             for (int i = 0; i < n; ++i) nx += E.XFC.ptr[o + i + 1] - E.XFC.ptr[o + i];
             if (E.face_band[F] > 1 || n > TRI_N || nx > 2) D.tri = 0;
         }
+        for (int ci = 0; ci < E.ncross && D.tri; ++ci)
+            if (E.XCF.ptr[ci + 1] - E.XCF.ptr[ci] > XCF_W) D.tri = 0;
         if (D.tri && E.nfaces > 0) {
             const int ng = (E.nfaces + 31) / 32;
             std::vector<int32_t> tn(E.nfaces), tnode(size_t(ng) * TRI_N * 32, 0), txj(2 * E.nfaces, -1),
@@ -481,6 +483,15 @@ de_status_t upload_prec(de_ctx* c) {
             TRY(dupload(c, &D.g_v0, gv0));
             TRY(dupload(c, &D.g_v1, gv1));
             D.fuse = getenv("DE_NO_E3_FUSE") ? 0 : 1;
+            std::vector<int32_t> x4c(size_t(XCF_W) * E.ncross, 0);
+            std::vector<double> x4v(size_t(XCF_W) * E.ncross, 0.0);
+            for (int ci = 0; ci < E.ncross; ++ci)
+                for (int e = E.XCF.ptr[ci], k = 0; e < E.XCF.ptr[ci + 1]; ++e, ++k) {
+                    x4c[size_t(k) * E.ncross + ci] = E.XCF.col[e];
+                    x4v[size_t(k) * E.ncross + ci] = E.XCF.val[e];
+                }
+            TRY(dupload(c, &D.xcf4_col, x4c));
+            TRY(dupload(c, &D.xcf4_val, x4v));
         }
         return check_launch();
     };

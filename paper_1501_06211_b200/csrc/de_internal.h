@@ -169,7 +169,11 @@ struct ElimDev {
     int32_t fuse;
     int32_t *g_c0, *g_c1;
     double *g_v0, *g_v1;
+    // X_CF padded to XCF_W entries per cross point ([XCF_W][ncross], col 0 / val 0 padding), tri only
+    int32_t* xcf4_col;
+    double* xcf4_val;
 };
+constexpr int XCF_W = 4;
 constexpr int TRI_N = 32;
 
 struct CsrDev {

@@ -352,26 +352,71 @@ __device__ void elim_coop(cg::grid_group& grid, const CoopArgs& a, const ElimDev
         const int base = E.cross_comp_off[c], ncc = E.cross_comp_off[c + 1] - base;
         if (ncc > 0) {
             double* tC = dsm;
-            for (int i = threadIdx.x; i < ncc; i += CT) {
-                const int ci = base + i;
-                double t = scl[c] * b[E.cross_flat[ci]];
-                for (int e = E.xcf_ptr[ci]; e < E.xcf_ptr[ci + 1]; ++e) t -= E.xcf_val[e] * y[E.xcf_col[e]];
-                tC[i] = t;
+            if (E.tri) {   // padded X_CF: every load of UC cross points issued before the first use
+                constexpr int UC = 4;
+                const double sc = scl[c];
+                for (int i0 = threadIdx.x; i0 < ncc; i0 += CT * UC) {
+                    int fl[UC], col[UC][XCF_W];
+                    double xv[UC][XCF_W];
+#pragma unroll
+                    for (int u = 0; u < UC; ++u) {
+                        const int i = i0 + u * CT;
+                        const bool ok = i < ncc;
+                        const int ci = base + (ok ? i : 0);
+                        fl[u] = E.cross_flat[ci];
+#pragma unroll
+                        for (int k = 0; k < XCF_W; ++k) {
+                            col[u][k] = E.xcf4_col[size_t(k) * E.ncross + ci];
+                            xv[u][k] = E.xcf4_val[size_t(k) * E.ncross + ci];
+                        }
+                    }
+                    double bv[UC], yv[UC][XCF_W];
+#pragma unroll
+                    for (int u = 0; u < UC; ++u) {
+                        bv[u] = b[fl[u]];
+#pragma unroll
+                        for (int k = 0; k < XCF_W; ++k) yv[u][k] = y[col[u][k]];
+                    }
+#pragma unroll
+                    for (int u = 0; u < UC; ++u) {
+                        const int i = i0 + u * CT;
+                        double t = sc * bv[u];
+#pragma unroll
+                        for (int k = 0; k < XCF_W; ++k) t -= xv[u][k] * yv[u][k];
+                        if (i < ncc) tC[i] = t;
+                    }
+                }
+            } else {
+                for (int i = threadIdx.x; i < ncc; i += CT) {
+                    const int ci = base + i;
+                    double t = scl[c] * b[E.cross_flat[ci]];
+                    for (int e = E.xcf_ptr[ci]; e < E.xcf_ptr[ci + 1]; ++e) t -= E.xcf_val[e] * y[E.xcf_col[e]];
+                    tC[i] = t;
+                }
             }
             __syncthreads();
             const double* S = E.Sinv + E.sc_off[c];
             for (int rr = lb * CW + w; rr < ncc; rr += nbc * CW) {
                 const double* __restrict__ row = S + size_t(rr) * ncc;
-                double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;   // independent chains: 4 loads in flight
+                constexpr int NA = 8;                         // independent chains: 8 loads per lane in flight
+                double acc8[NA];
+#pragma unroll
+                for (int q = 0; q < NA; ++q) acc8[q] = 0.0;
                 int j = lane;
-                for (; j + 96 < ncc; j += 128) {
-                    a0 += row[j] * tC[j];
-                    a1 += row[j + 32] * tC[j + 32];
-                    a2 += row[j + 64] * tC[j + 64];
-                    a3 += row[j + 96] * tC[j + 96];
+                for (; j + 32 * (NA - 1) < ncc; j += 32 * NA) {
+                    double rv[NA];
+#pragma unroll
+                    for (int q = 0; q < NA; ++q) rv[q] = row[j + 32 * q];
+#pragma unroll
+                    for (int q = 0; q < NA; ++q) acc8[q] += rv[q] * tC[j + 32 * q];
                 }
-                for (; j < ncc; j += 32) a0 += row[j] * tC[j];
-                double acc = warp_sum((a0 + a1) + (a2 + a3));
+#pragma unroll
+                for (int q = 0; q < NA; ++q) {   // tail: fewer than NA chunks of 32 left
+                    const int jj = j + 32 * q;
+                    if (jj < ncc) acc8[q] += row[jj] * tC[jj];
+                }
+                double acc = warp_sum(((acc8[0] + acc8[1]) + (acc8[2] + acc8[3])) +
+                                     ((acc8[4] + acc8[5]) + (acc8[6] + acc8[7])));
                 if (lane == 0) {
                     xC[base + rr] = acc;
                     out[E.cross_flat[base + rr]] = acc;
