@@ -406,7 +406,7 @@ __device__ void elim_coop(cg::grid_group& grid, const CoopArgs& a, const ElimDev
                 for (; j + 32 * (NA - 1) < ncc; j += 32 * NA) {
                     double rv[NA];
 #pragma unroll
-                    for (int q = 0; q < NA; ++q) rv[q] = row[j + 32 * q];
+                    for (int q = 0; q < NA; ++q) rv[q] = __ldcs(row + j + 32 * q);   // streamed once per step
 #pragma unroll
                     for (int q = 0; q < NA; ++q) acc8[q] += rv[q] * tC[j + 32 * q];
                 }

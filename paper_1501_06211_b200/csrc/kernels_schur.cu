@@ -223,12 +223,12 @@ __global__ void __launch_bounds__(256) k_schur_explicit(const SubDesc* __restric
         double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
         int k = 0;
         for (; k + 3 < nG; k += 4) {
-            a0 += S[size_t(k) * nG + row] * xs[k];
-            a1 += S[size_t(k + 1) * nG + row] * xs[k + 1];
-            a2 += S[size_t(k + 2) * nG + row] * xs[k + 2];
-            a3 += S[size_t(k + 3) * nG + row] * xs[k + 3];
+            a0 += __ldcs(S + size_t(k) * nG + row) * xs[k];
+            a1 += __ldcs(S + size_t(k + 1) * nG + row) * xs[k + 1];
+            a2 += __ldcs(S + size_t(k + 2) * nG + row) * xs[k + 2];
+            a3 += __ldcs(S + size_t(k + 3) * nG + row) * xs[k + 3];
         }
-        for (; k < nG; ++k) a0 += S[size_t(k) * nG + row] * xs[k];
+        for (; k < nG; ++k) a0 += __ldcs(S + size_t(k) * nG + row) * xs[k];
         qloc[d.goff + row] = (a0 + a1) + (a2 + a3);
     }
 }
