@@ -396,31 +396,47 @@ __device__ void elim_coop(cg::grid_group& grid, const CoopArgs& a, const ElimDev
             }
             __syncthreads();
             const double* S = E.Sinv + E.sc_off[c];
-            for (int rr = lb * CW + w; rr < ncc; rr += nbc * CW) {
-                const double* __restrict__ row = S + size_t(rr) * ncc;
-                constexpr int NA = 8;                         // independent chains: 8 loads per lane in flight
-                double acc8[NA];
+            // block lb owns the contiguous rows [rlo, rhi); warp w takes one column slice of all of them (two
+            // rows at a time, NA loads per row per lane in flight); warp partials are summed in fixed order
+            const int rlo = int(int64_t(lb) * ncc / nbc), rhi = int(int64_t(lb + 1) * ncc / nbc), nr = rhi - rlo;
+            const int cw = ((ncc + CW * 32 - 1) / (CW * 32)) * 32;
+            const int c0 = w * cw, c1 = min(ncc, c0 + cw);
+            double* part = tC + ncc;   // [CW][nr]
+            constexpr int NA = 8;
+            for (int r = rlo; r < rhi; r += 2) {
+                const bool two = r + 1 < rhi;
+                const double* __restrict__ row0 = S + size_t(r) * ncc;
+                const double* __restrict__ row1 = S + size_t(two ? r + 1 : r) * ncc;
+                double s0 = 0.0, s1 = 0.0;
+                for (int j = c0 + lane; j < c1; j += 32 * NA) {
+                    double v0[NA], v1[NA], t[NA];
 #pragma unroll
-                for (int q = 0; q < NA; ++q) acc8[q] = 0.0;
-                int j = lane;
-                for (; j + 32 * (NA - 1) < ncc; j += 32 * NA) {
-                    double rv[NA];
+                    for (int q = 0; q < NA; ++q) {
+                        const int jj = j + 32 * q;
+                        const bool ok = jj < c1;
+                        v0[q] = ok ? __ldcs(row0 + jj) : 0.0;   // streamed once per step
+                        v1[q] = (ok && two) ? __ldcs(row1 + jj) : 0.0;
+                        t[q] = ok ? tC[jj] : 0.0;
+                    }
 #pragma unroll
-                    for (int q = 0; q < NA; ++q) rv[q] = __ldcs(row + j + 32 * q);   // streamed once per step
-#pragma unroll
-                    for (int q = 0; q < NA; ++q) acc8[q] += rv[q] * tC[j + 32 * q];
+                    for (int q = 0; q < NA; ++q) {
+                        s0 += v0[q] * t[q];
+                        s1 += v1[q] * t[q];
+                    }
                 }
-#pragma unroll
-                for (int q = 0; q < NA; ++q) {   // tail: fewer than NA chunks of 32 left
-                    const int jj = j + 32 * q;
-                    if (jj < ncc) acc8[q] += row[jj] * tC[jj];
-                }
-                double acc = warp_sum(((acc8[0] + acc8[1]) + (acc8[2] + acc8[3])) +
-                                     ((acc8[4] + acc8[5]) + (acc8[6] + acc8[7])));
+                s0 = warp_sum(s0);
+                s1 = warp_sum(s1);
                 if (lane == 0) {
-                    xC[base + rr] = acc;
-                    out[E.cross_flat[base + rr]] = acc;
+                    part[w * nr + (r - rlo)] = s0;
+                    if (two) part[w * nr + (r + 1 - rlo)] = s1;
                 }
+            }
+            __syncthreads();
+            for (int r = rlo + threadIdx.x; r < rhi; r += CT) {
+                double acc = 0.0;
+                for (int q = 0; q < CW; ++q) acc += part[q * nr + (r - rlo)];
+                xC[base + r] = acc;
+                out[E.cross_flat[base + r]] = acc;
             }
             __syncthreads();
         }
@@ -966,7 +982,10 @@ bool prec_coop_prepare(const PrecDev& P, int device, CoopBuffers& B) {
     const bool stage = size_t(CW) * (3 * mf + mfac) * 8 <= 96 * 1024;
     const int per_warp = stage ? 3 * mf + mfac : 3 * mf;
     size_t smem = size_t(CW) * per_warp * 8;
-    smem = std::max(smem, size_t(ncmax) * 8);
+    {   // t_C plus the per-warp partials of the rows one block owns in the cross-point GEMV (>= 1 block per SM)
+        const int nbc_lo = std::max(1, nsm / std::max(1, P.ncomp));
+        smem = std::max(smem, (size_t(ncmax) + size_t(CW) * ((ncmax + nbc_lo - 1) / nbc_lo)) * 8);
+    }
     smem = std::max(smem, size_t(GW) * CT * 8);      // per-thread Gram accumulators
     smem = std::max(smem, size_t(RW) * TRI_N * 8);   // per-thread forward solutions of tridiagonal faces
     smem = std::max(smem, size_t(CW) * (4 * KMAX * (KMAX + 1) + 2 * KMAX + 4 * KMAX) * 8);
@@ -979,6 +998,11 @@ bool prec_coop_prepare(const PrecDev& P, int device, CoopBuffers& B) {
     if (const char* e = getenv("DE_COOP_BPS")) bps = std::max(1, atoi(e));
     const int nb = nsm * std::min(per_sm, bps);
     if (nb < P.ncomp) return false;
+    {   // guaranteed by the sizing above (nb >= nsm)
+        const int nbc_min = nb / P.ncomp;
+        const size_t need = (size_t(ncmax) + size_t(CW) * ((ncmax + nbc_min - 1) / nbc_min)) * 8;
+        if (need > smem) return false;
+    }
     if (getenv("DE_VERBOSE"))
         fprintf(stderr, "[de] k_prec_coop: %d blocks (%d resident/SM possible), %zu B smem\n", nb, per_sm, smem);
     B.nb = nb;
