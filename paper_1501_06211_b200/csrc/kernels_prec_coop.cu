@@ -758,6 +758,10 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
         const bool part = act[c] && !brk[c];
         const int kc = kcs[c];
         // A: (M w, L w) by one SpMV over the shared pattern; ||w||_M^2 and h_t = W_t . M w
+        const bool dbg = a.timers && blockIdx.x == 0 && tid == 32 && j == 5;
+#define DBGT(k) do { if (dbg) a.timers[k] = gtimer(); } while (0)
+        DBGT(120);
+        const long long tA0 = clock64();
         ZERO_VALS();
         if (part)
             for (int64_t i = r0; i < hi; i += rs) {
@@ -778,17 +782,23 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
 #pragma unroll
                 for (int t = 0; t < KMAX; ++t) vals[1 + t] += wt[t] * m;
             }
+        DBGT(121);
+        if (a.timers && j == 5 && blockIdx.x < 4 && (tid & 31) == 0) a.timers[140 + blockIdx.x * CW + (tid >> 5)] = clock64() - tA0;
         block_partials(a, vals, 1 + KMAX, pp, c, lb, sred);
+        DBGT(122);
         grid.sync();
     __syncwarp();   // lane 0 spun in the barrier: reconverge before warp-synchronous code
     STAMP(stamp++);
+        DBGT(123);
         read_totals(a, pp, 1 + kc, nb, tot);   // every component's first 1+kc (kc uniform enough: use own)
+        DBGT(124);
         pp ^= 1;
         if (tid < nc) nb2v[tid] = tot[tid][0];
         if (tid < KMAX) hsm[c][tid] = tid < kc ? tot[c][1 + tid] * sclh[c][tid] * sclh[c][tid] : 0.0;
         __syncthreads();
         // B: w1 = w - W h; M w1 = M w - (M W) h and L w1 = L w - (L W) h by linearity (own rows only);
         // dots h'_t = W_t . M w1
+        DBGT(130);
         ZERO_VALS();
         if (part)
             for (int64_t i = r0; i < hi; i += rs) {
@@ -813,18 +823,21 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
 #pragma unroll
                 for (int t = 0; t < KMAX; ++t) vals[t] += wt[t] * m;
             }
+        DBGT(131);
         block_partials(a, vals, KMAX, pp, c, lb, sred);
+        DBGT(132);
         grid.sync();
     __syncwarp();   // lane 0 spun in the barrier: reconverge before warp-synchronous code
     STAMP(stamp++);
+        DBGT(133);
         read_totals(a, pp, kc > 0 ? kc : 1, nb, tot);
+        DBGT(134);
         pp ^= 1;
         if (tid < KMAX) hsm[c][tid] = tid < kc ? tot[c][tid] * sclh[c][tid] * sclh[c][tid] : 0.0;
         __syncthreads();
         // C: w2 = w1 - W h' with M w2, L w2 by linearity (M w2 is the next solve's rhs); ||w2||_M^2; row j of
         // the Rayleigh-Ritz Gram matrices before normalisation: w2.(L W_t), w2.(M W_t) (t < j), w2.L w2,
         // w2.M w2, w2.r
-        const bool dbg = a.timers && blockIdx.x == 0 && tid == 32 && j == 5;
         if (dbg) a.timers[110] = gtimer();
         ZERO_VALS();
         gram_zero(gacc);

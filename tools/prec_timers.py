@@ -22,6 +22,9 @@ for rep in range(3):
 t = (C.c_ulonglong * (200 + 8192))()
 L.de_debug_prec_timers(S.ctx, t, 200 + 8192)
 print("ritz_warp us", (t[101] - t[100]) / 1e3, "setup", (t[103]-t[102])/1e3, "jacobi", (t[104]-t[103])/1e3, "sweeps", t[106], "final", (t[105]-t[104])/1e3)
+for nm, b0 in (("A", 120), ("B", 130)):
+    print(f"phase{nm} j=5: rows", (t[b0+1]-t[b0])/1e3, "partials", (t[b0+2]-t[b0+1])/1e3, "sync", (t[b0+3]-t[b0+2])/1e3, "totals", (t[b0+4]-t[b0+3])/1e3)
+print("phaseA per-warp row cycles (blocks 0-3):", list(t)[140:172])
 print("phaseC j=5: rows", (t[111]-t[110])/1e3, "partials", (t[112]-t[111])/1e3, "sync", (t[113]-t[112])/1e3, "totals", (t[114]-t[113])/1e3)
 ts = [x for x in list(t)[:100] if x]
 d = np.diff(np.array(ts, dtype=np.float64)) / 1e3
