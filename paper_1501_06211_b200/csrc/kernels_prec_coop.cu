@@ -332,8 +332,10 @@ __device__ void elim_coop(cg::grid_group& grid, const CoopArgs& a, const ElimDev
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     // warp 0 hosts the grid-barrier thread; it comes out of every barrier late, so face solves run
     // on warps 1..CW-1 only (measured: warp 0 otherwise sets the phase time)
-    const int gw = blockIdx.x * (CW - 1) + (w - 1), nwarps = gridDim.x * (CW - 1);
-    const int gt = blockIdx.x * RW + (threadIdx.x - 32), nthr = gridDim.x * RW;
+    // warp-major over blocks: consecutive face groups land on different SMs (block-major would put every
+    // face on the first few dozen blocks); tridiagonal faces: warp gw takes the 32-face group gw
+    const int gw = (w - 1) * int(gridDim.x) + blockIdx.x, nwarps = gridDim.x * (CW - 1);
+    const int gt = gw * 32 + lane, nthr = nwarps * 32;
     double* y = P.y;
     double* xC = P.y + P.nflat;
     double* wsm = dsm + size_t(w) * a.per_warp;
