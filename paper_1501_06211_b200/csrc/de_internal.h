@@ -294,6 +294,7 @@ struct CoopBuffers {
     int stage = 0, per_warp = 0, mf = 0, ncmax = 0, nbc_max = 0, tridiag = 0;
     double *red = nullptr, *gram = nullptr, *w1 = nullptr, *mw1 = nullptr, *lw1 = nullptr;
     unsigned long long* timers = nullptr;   // phase stamps (diagnostics; env DE_PREC_TIMERS=1)
+    const void* kfn = nullptr;              // k_prec_coop instantiation (basis bound, timers)
 };
 bool prec_coop_prepare(const PrecDev& P, int device, CoopBuffers& B);
 size_t prec_coop_red_doubles(const CoopBuffers& B);

@@ -53,7 +53,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 #define STAMP(k)                                                        \
     do {                                                                \
-        if (a.timers && blockIdx.x == 0 && threadIdx.x == 0) a.timers[k] = gtimer(); \
+        if (TIM && a.timers && blockIdx.x == 0 && threadIdx.x == 0) a.timers[k] = gtimer(); \
     } while (0)
 
 __device__ __forceinline__ int ccomp(const int64_t* off, int nc, int64_t i) {
@@ -69,11 +69,13 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 // block-reduce vals[0..nv) and write this block's partials into red[pp][c][v][lb]
-__device__ void block_partials(const CoopArgs& a, const double (&vals)[NRED], int nv, int pp, int c, int lb,
+template <int NV>
+__device__ void block_partials(const CoopArgs& a, const double (&vals)[NV], int nv, int pp, int c, int lb,
                                double (*sred)[NRED]) {
+    static_assert(NV <= NRED, "partials buffer");
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
-    for (int v = 0; v < NRED; ++v) {
+    for (int v = 0; v < NV; ++v) {
         if (v < nv) {
             const double t = warp_sum(vals[v]);
             if (lane == 0) sred[w][v] = t;
@@ -326,6 +328,7 @@ __device__ void face_thread_tridiag(const CoopArgs& a, const ElimDev& E, int F, 
 }
 
 // x = X^-1 (scl * b) by exact elimination (faces -> cross points -> faces); 3 grid barriers.
+template <bool TIM>
 __device__ void elim_coop(cg::grid_group& grid, const CoopArgs& a, const ElimDev& E, const double* b,
                           const double* scl, double* out, double* dsm, int c, int lb, int nbc, int& stamp) {
     const PrecDev& P = a.P;
@@ -345,7 +348,7 @@ __device__ void elim_coop(cg::grid_group& grid, const CoopArgs& a, const ElimDev
             for (int F = gt; F < E.nfaces; F += nthr) face_thread_tridiag(a, E, F, b, scl, nullptr, y, 0, dsm + (threadIdx.x - 32));
     } else if (w > 0)
         for (int F = gw; F < E.nfaces; F += nwarps) face_warp(a, E, F, b, scl, nullptr, y, 0, wsm, lane);
-    if (a.timers && lane == 0 && w > 0 && gw < 4096) a.timers[200 + gw] = clock64() - tf0;
+    if (TIM && a.timers && lane == 0 && w > 0 && gw < 4096) a.timers[200 + gw] = clock64() - tf0;
     grid.sync();
     __syncwarp();   // lane 0 spun in the barrier: reconverge before warp-synchronous code
     STAMP(stamp++);
@@ -453,7 +456,7 @@ __device__ void elim_coop(cg::grid_group& grid, const CoopArgs& a, const ElimDev
             for (int F = gt; F < E.nfaces; F += nthr) face_thread_tridiag(a, E, F, b, scl, xC, out, 1, dsm + (threadIdx.x - 32));
     } else if (w > 0)
         for (int F = gw; F < E.nfaces; F += nwarps) face_warp(a, E, F, b, scl, xC, out, 1, wsm, lane);
-    if (a.timers && lane == 0 && w > 0 && gw < 4096) a.timers[200 + 4096 + gw] = clock64() - tf0;
+    if (TIM && a.timers && lane == 0 && w > 0 && gw < 4096) a.timers[200 + 4096 + gw] = clock64() - tf0;
     grid.sync();
     __syncwarp();   // lane 0 spun in the barrier: reconverge before warp-synchronous code
     STAMP(stamp++);
@@ -668,7 +671,11 @@ __device__ bool ritz_warp(const double* Ain, const double* Bin, const double* wr
     return true;
 }
 
+// KM: compile-time bound on the basis size (>= lanczos_k) for the register arrays of the row phases;
+// TIM: diagnostic timers compiled in (DE_PREC_TIMERS)
+template <int KM, bool TIM>
 __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
+    static_assert(KM <= KMAX, "basis bound");
     cg::grid_group grid = cg::this_grid();
     if (a.s != nullptr && a.s->done) return;
     int stamp = 0;
@@ -690,9 +697,9 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
     const int64_t r0 = tid >= 32 ? lo + int64_t(lb) * RW + (tid - 32) : hi, rs = int64_t(nbc) * RW;
     const int64_t nf = P.nflat;
     int pp = 0;
-    double vals[NRED];
+    double vals[KM + 2];
 #define ZERO_VALS()                                    \
-    _Pragma("unroll") for (int v_ = 0; v_ < NRED; ++v_) vals[v_] = 0.0
+    _Pragma("unroll") for (int v_ = 0; v_ < KM + 2; ++v_) vals[v_] = 0.0
 
     // ---- r_c gather and zero test
     ZERO_VALS();
@@ -717,7 +724,7 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
     // Basis vectors are stored unnormalised (W_t = sclh_t * Wraw_t, likewise M W_t and L W_t): every
     // consumer folds sclh_t into its coefficients, so no normalisation pass over the rows is needed.
     // ---- s = M^-1 r (exact) = Wraw_0
-    elim_coop(grid, a, P.eM, P.rf, scl, P.W, dsm, c, lb, nbc, stamp);
+    elim_coop<TIM>(grid, a, P.eM, P.rf, scl, P.W, dsm, c, lb, nbc, stamp);
     // ---- Ms, Ls, ||s||_M; q_1 = s / ||s||_M; rhs of the next solve M q_1 = Ms / ||s||_M
     ZERO_VALS();
     double* gacc = dsm;   // per-thread Gram accumulators [GW][CT] (dsm is free outside face solves / Ritz)
@@ -756,11 +763,11 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
     // ---- inverse Lanczos steps
     const bool fuseK = P.eK.tri && P.eK.fuse;
     for (int j = 1; j < P.kmax; ++j) {
-        elim_coop(grid, a, P.eK, j == 1 ? P.MW : P.Mw, scl, P.w, dsm, c, lb, nbc, stamp);   // w = K^-1 M q_j
+        elim_coop<TIM>(grid, a, P.eK, j == 1 ? P.MW : P.Mw, scl, P.w, dsm, c, lb, nbc, stamp);   // w = K^-1 M q_j
         const bool part = act[c] && !brk[c];
         const int kc = kcs[c];
         // A: (M w, L w) by one SpMV over the shared pattern; ||w||_M^2 and h_t = W_t . M w
-        const bool dbg = a.timers && blockIdx.x == 0 && tid == 32 && j == 5;
+        const bool dbg = TIM && a.timers && blockIdx.x == 0 && tid == 32 && j == 5;
 #define DBGT(k) do { if (dbg) a.timers[k] = gtimer(); } while (0)
         DBGT(120);
         const long long tA0 = clock64();
@@ -778,15 +785,15 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
                 a.mw1[i] = m;
                 a.lw1[i] = l;
                 vals[0] += wi * m;
-                double wt[KMAX];
+                double wt[KM];
 #pragma unroll
-                for (int t = 0; t < KMAX; ++t) wt[t] = t < kc ? P.W[size_t(t) * nf + i] : 0.0;
+                for (int t = 0; t < KM; ++t) wt[t] = t < kc ? P.W[size_t(t) * nf + i] : 0.0;
 #pragma unroll
-                for (int t = 0; t < KMAX; ++t) vals[1 + t] += wt[t] * m;
+                for (int t = 0; t < KM; ++t) vals[1 + t] += wt[t] * m;
             }
         DBGT(121);
-        if (a.timers && j == 5 && blockIdx.x < 4 && (tid & 31) == 0) a.timers[140 + blockIdx.x * CW + (tid >> 5)] = clock64() - tA0;
-        block_partials(a, vals, 1 + KMAX, pp, c, lb, sred);
+        if (TIM && a.timers && j == 5 && blockIdx.x < 4 && (tid & 31) == 0) a.timers[140 + blockIdx.x * CW + (tid >> 5)] = clock64() - tA0;
+        block_partials(a, vals, 1 + KM, pp, c, lb, sred);
         DBGT(122);
         grid.sync();
     __syncwarp();   // lane 0 spun in the barrier: reconverge before warp-synchronous code
@@ -804,9 +811,9 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
         ZERO_VALS();
         if (part)
             for (int64_t i = r0; i < hi; i += rs) {
-                double wt[KMAX], mt[KMAX], lt[KMAX];
+                double wt[KM], mt[KM], lt[KM];
 #pragma unroll
-                for (int t = 0; t < KMAX; ++t) {
+                for (int t = 0; t < KM; ++t) {
                     const bool ok = t < kc;
                     wt[t] = ok ? P.W[size_t(t) * nf + i] : 0.0;
                     mt[t] = ok ? P.MW[size_t(t) * nf + i] : 0.0;
@@ -814,7 +821,7 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
                 }
                 double x = P.w[i], m = a.mw1[i], l = a.lw1[i];
 #pragma unroll
-                for (int t = 0; t < KMAX; ++t) {
+                for (int t = 0; t < KM; ++t) {
                     x -= hsm[c][t] * wt[t];
                     m -= hsm[c][t] * mt[t];
                     l -= hsm[c][t] * lt[t];
@@ -823,10 +830,10 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
                 a.mw1[i] = m;
                 a.lw1[i] = l;
 #pragma unroll
-                for (int t = 0; t < KMAX; ++t) vals[t] += wt[t] * m;
+                for (int t = 0; t < KM; ++t) vals[t] += wt[t] * m;
             }
         DBGT(131);
-        block_partials(a, vals, KMAX, pp, c, lb, sred);
+        block_partials(a, vals, KM, pp, c, lb, sred);
         DBGT(132);
         grid.sync();
     __syncwarp();   // lane 0 spun in the barrier: reconverge before warp-synchronous code
@@ -845,9 +852,9 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
         gram_zero(gacc);
         if (part)
             for (int64_t i = r0; i < hi; i += rs) {
-                double wt[KMAX], mt[KMAX], lt[KMAX];
+                double wt[KM], mt[KM], lt[KM];
 #pragma unroll
-                for (int t = 0; t < KMAX; ++t) {
+                for (int t = 0; t < KM; ++t) {
                     const bool ok = t < kc;
                     wt[t] = ok ? P.W[size_t(t) * nf + i] : 0.0;
                     mt[t] = ok ? P.MW[size_t(t) * nf + i] : 0.0;
@@ -856,7 +863,7 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
                 double x = a.w1[i], m = a.mw1[i], l = a.lw1[i];
                 const double rv = P.rf[i];
 #pragma unroll
-                for (int t = 0; t < KMAX; ++t) {
+                for (int t = 0; t < KM; ++t) {
                     x -= hsm[c][t] * wt[t];
                     m -= hsm[c][t] * mt[t];
                     l -= hsm[c][t] * lt[t];
@@ -867,7 +874,7 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
                 P.LW[size_t(j) * nf + i] = l;
                 vals[0] += x * m;
 #pragma unroll
-                for (int t = 0; t < KMAX; ++t)
+                for (int t = 0; t < KM; ++t)
                     if (t < kc) {
                         gacc[t * CT + tid] += x * lt[t];
                         gacc[(KMAX + t) * CT + tid] += x * mt[t];
@@ -948,10 +955,10 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
                 double* X = V + KMAX * (KMAX + 1);
                 double* rot = X + KMAX * (KMAX + 1);
                 int* rpq = reinterpret_cast<int*>(rot + KMAX);
-                if (a.timers && w == 0 && lane == 0) a.timers[100] = gtimer();
+                if (TIM && a.timers && w == 0 && lane == 0) a.timers[100] = gtimer();
                 const bool ok = ritz_warp(zs.A, zs.B, zs.wr, k, P.singular[w] != 0, P.theta, zs.coef, R, Cm, V, X,
-                                          rot, rpq, (a.timers && w == 0) ? a.timers + 102 : nullptr);
-                if (a.timers && w == 0 && lane == 0) a.timers[101] = gtimer();
+                                          rot, rpq, (TIM && a.timers && w == 0) ? a.timers + 102 : nullptr);
+                if (TIM && a.timers && w == 0 && lane == 0) a.timers[101] = gtimer();
                 if (!ok && lane == 0) {
                     zs.status = DE_EBREAKDOWN;
                     for (int e = 0; e < KMAX; ++e) zs.coef[e] = 0.0;
@@ -1005,9 +1012,13 @@ bool prec_coop_prepare(const PrecDev& P, int device, CoopBuffers& B) {
     smem = std::max(smem, size_t(RW) * TRI_N * 8);   // per-thread forward solutions of tridiagonal faces
     smem = std::max(smem, size_t(CW) * (4 * KMAX * (KMAX + 1) + 2 * KMAX + 4 * KMAX) * 8);
     if (smem > 200 * 1024) return false;
-    cudaFuncSetAttribute(k_prec_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    typedef void (*coop_fn)(CoopArgs);
+    const bool tim = getenv("DE_PREC_TIMERS") != nullptr;
+    coop_fn kfn = P.kmax <= 10 ? (tim ? k_prec_coop<10, true> : k_prec_coop<10, false>) : k_prec_coop<KMAX, false>;
+    if (tim && P.kmax > 10) kfn = k_prec_coop<KMAX, true>;
+    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_prec_coop, CT, smem) != cudaSuccess || per_sm < 1)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, CT, smem) != cudaSuccess || per_sm < 1)
         return false;
     int bps = 2;   // blocks per SM; DE_COOP_BPS overrides (tuning experiments only)
     if (const char* e = getenv("DE_COOP_BPS")) bps = std::max(1, atoi(e));
@@ -1021,6 +1032,7 @@ bool prec_coop_prepare(const PrecDev& P, int device, CoopBuffers& B) {
     if (getenv("DE_VERBOSE"))
         fprintf(stderr, "[de] k_prec_coop: %d blocks (%d resident/SM possible), %zu B smem\n", nb, per_sm, smem);
     B.nb = nb;
+    B.kfn = reinterpret_cast<const void*>(kfn);
     B.smem = smem;
     B.stage = stage ? 1 : 0;
     B.per_warp = per_warp;
@@ -1063,7 +1075,7 @@ int prec_apply_coop(const PrecDev& P, const CoopBuffers& B, const double* r, dou
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    const cudaError_t e = cudaLaunchKernelEx(&cfg, k_prec_coop, a);
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, reinterpret_cast<void (*)(CoopArgs)>(const_cast<void*>(B.kfn)), a);
     return e == cudaSuccess ? 1 : -1;
 }
 
