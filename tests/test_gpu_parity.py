@@ -128,6 +128,28 @@ def _check_precond(p, T, comps, impl):
         S.close()
 
 
+@pytest.mark.parametrize("k,theta", [(4, 0.5), (12, 0.25), (16, 0.5)])
+@pytest.mark.parametrize("name,kw", [SMALL[2], SMALL[4]], ids=_ids([SMALL[2], SMALL[4]]))
+def test_preconditioner_lanczos_k_theta(name, kw, k, theta):
+    """Basis sizes on both sides of the cooperative kernel's compile-time bound (10) and theta != 1/2
+    (SPEC.md:374-413), cooperative kernel vs oracle O8."""
+    from paper_1501_06211_b200 import binding as B
+    p = make_config(name, **kw)
+    T = build_topology(p)
+    comps = build_components(p, T)
+    S = _solver(p, lanczos_k=k, theta=theta)
+    try:
+        r = np.random.default_rng(13).normal(size=T.n_G)
+        ref = apply_precond(comps, r, "lanczos", theta, k, "X")
+        dr = torch.tensor(r, dtype=torch.float64, device="cuda")
+        dz = torch.empty_like(dr)
+        B.de_precond_apply_device(S.ctx, dr.data_ptr(), dz.data_ptr())
+        z = dz.cpu().numpy()
+        assert np.linalg.norm(z - ref) <= 1e-9 * np.linalg.norm(ref), np.linalg.norm(z - ref) / np.linalg.norm(ref)
+    finally:
+        S.close()
+
+
 WELL_POSED = [c for c in SMALL if c[0] != "c3"] + [("c2", {}), ("c4", dict(nel=(24, 12, 12), sub=(6, 6, 6)))]
 
 
