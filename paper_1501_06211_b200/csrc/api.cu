@@ -363,7 +363,7 @@ de_status_t upload_prec(de_ctx* c) {
     for (const HElim* E : {&hs.elimK, &hs.elimM})
         for (int cc = 0; cc < hs.ncomp; ++cc) maxsc = std::max(maxsc, E->sc_off[cc + 1] - E->sc_off[cc]);
     TRY(dalloc(c, &gjbuf, size_t(std::max<int64_t>(maxsc, 1))));
-    auto up_elim = [&](const HElim& E, ElimDev& D) -> de_status_t {
+    auto up_elim = [&](const HElim& E, const HCsr& X, ElimDev& D) -> de_status_t {
         D.nfaces = E.nfaces;
         D.ncross = E.ncross;
         D.ncomp = hs.ncomp;
@@ -492,11 +492,57 @@ de_status_t upload_prec(de_ctx* c) {
                 }
             TRY(dupload(c, &D.xcf4_col, x4c));
             TRY(dupload(c, &D.xcf4_val, x4v));
+            {   // PCR coefficients of every face block X_FF (tridiagonal along face_nodes)
+                std::vector<double> pq(size_t(E.nfaces) * PCR_Q * 32, 0.0);
+                std::vector<int32_t> pn(size_t(E.nfaces) * 32, 0);
+                auto entry = [&](int r, int col) {
+                    for (int e = X.ptr[r]; e < X.ptr[r + 1]; ++e)
+                        if (X.col[e] == col) return X.val[e];
+                    return 0.0;
+                };
+                for (int F = 0; F < E.nfaces; ++F) {
+                    const int o = E.face_off[F], n = E.face_off[F + 1] - o;
+                    double av[32], dv[32], cv[32];
+                    for (int j = 0; j < 32; ++j) {
+                        av[j] = cv[j] = 0.0;
+                        dv[j] = 1.0;
+                        if (j < n) {
+                            const int fj = E.face_nodes[o + j];
+                            pn[size_t(F) * 32 + j] = fj;
+                            dv[j] = entry(fj, fj);
+                            if (j > 0) av[j] = entry(fj, E.face_nodes[o + j - 1]);
+                            if (j + 1 < n) cv[j] = entry(fj, E.face_nodes[o + j + 1]);
+                        }
+                    }
+                    double* q = &pq[size_t(F) * PCR_Q * 32];
+                    for (int l = 0; l < PCR_L; ++l) {
+                        const int sg = 1 << l;
+                        double na[32], nd[32], nc[32];
+                        for (int j = 0; j < 32; ++j) {
+                            const double al = j - sg >= 0 ? -av[j] / dv[j - sg] : 0.0;
+                            const double ga = j + sg < 32 ? -cv[j] / dv[j + sg] : 0.0;
+                            q[(2 * l) * 32 + j] = al;
+                            q[(2 * l + 1) * 32 + j] = ga;
+                            na[j] = j - sg >= 0 ? al * av[j - sg] : 0.0;
+                            nc[j] = j + sg < 32 ? ga * cv[j + sg] : 0.0;
+                            nd[j] = dv[j] + (j - sg >= 0 ? al * cv[j - sg] : 0.0) + (j + sg < 32 ? ga * av[j + sg] : 0.0);
+                        }
+                        for (int j = 0; j < 32; ++j) {
+                            av[j] = na[j];
+                            cv[j] = nc[j];
+                            dv[j] = nd[j];
+                        }
+                    }
+                    for (int j = 0; j < 32; ++j) q[(2 * PCR_L) * 32 + j] = 1.0 / dv[j];
+                }
+                TRY(dupload(c, &D.pcr, pq));
+                TRY(dupload(c, &D.pcr_node, pn));
+            }
         }
         return check_launch();
     };
-    TRY(up_elim(hs.elimK, P.eK));
-    TRY(up_elim(hs.elimM, P.eM));
+    TRY(up_elim(hs.elimK, hs.K, P.eK));
+    TRY(up_elim(hs.elimM, hs.M, P.eM));
     const size_t nf = size_t(P.nflat);
     TRY(dalloc(c, &P.rf, nf));
     TRY(dalloc(c, &P.s, nf));

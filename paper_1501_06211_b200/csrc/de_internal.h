@@ -172,7 +172,14 @@ struct ElimDev {
     // X_CF padded to XCF_W entries per cross point ([XCF_W][ncross], col 0 / val 0 padding), tri only
     int32_t* xcf4_col;
     double* xcf4_val;
+    // warp-per-face parallel cyclic reduction of X_FF y = b (tri only): lane j = face node j, 32 lanes per face
+    // (identity rows past the face end); per face [PCR_Q][32] doubles: (alpha, gamma) of the 5 reduction
+    // levels, then 1/d after the last level; pcr_node[F*32 + j] = flat index (0 past the end)
+    double* pcr;
+    int32_t* pcr_node;
 };
+constexpr int PCR_L = 5;             // log2(32) reduction levels
+constexpr int PCR_Q = 2 * PCR_L + 1;
 constexpr int XCF_W = 4;
 constexpr int TRI_N = 32;
 

@@ -92,16 +92,42 @@ __device__ void block_partials(const CoopArgs& a, const double (&vals)[NV], int 
 
 // totals of all components (fixed order over lb) into tot[c][v]
 __device__ void read_totals(const CoopArgs& a, int pp, int nv, int nb, double (*tot)[NRED]) {
+    // task (c, v) = sum over the component's nbc block partials: lane l adds b = l, l+32, ... in order, then a
+    // warp tree (fixed order); TU tasks per warp and QU partials per lane are loaded together
+    constexpr int TU = 3, QU = 8;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int nc = a.P.ncomp;
-    for (int t = w; t < nc * nv; t += CW) {
-        const int c = t / nv, v = t - c * nv;
-        const int nbc = (nb - c + nc - 1) / nc;
-        const double* p = a.red + ((size_t(pp) * MAXC + c) * NRED + v) * a.nbc_max;
-        double acc = 0.0;
-        for (int b = lane; b < nbc; b += 32) acc += *((volatile const double*)(p + b));
-        acc = warp_sum(acc);
-        if (lane == 0) tot[c][v] = acc;
+    const int nc = a.P.ncomp, ntask = nc * nv;
+    for (int t0 = w; t0 < ntask; t0 += CW * TU) {
+        double acc[TU];
+        const double* p[TU];
+        int nbc[TU];
+#pragma unroll
+        for (int u = 0; u < TU; ++u) {
+            const int t = min(t0 + u * CW, ntask - 1), c = t / nv, v = t - c * nv;
+            nbc[u] = (t0 + u * CW < ntask) ? (nb - c + nc - 1) / nc : 0;
+            p[u] = a.red + ((size_t(pp) * MAXC + c) * NRED + v) * a.nbc_max;
+            acc[u] = 0.0;
+        }
+        for (int b0 = 0; b0 < a.nbc_max; b0 += 32 * QU) {
+            double x[TU][QU];
+#pragma unroll
+            for (int u = 0; u < TU; ++u)
+#pragma unroll
+                for (int q = 0; q < QU; ++q) {
+                    const int bb = b0 + lane + 32 * q;
+                    x[u][q] = bb < nbc[u] ? *((volatile const double*)(p[u] + bb)) : 0.0;
+                }
+#pragma unroll
+            for (int u = 0; u < TU; ++u)
+#pragma unroll
+                for (int q = 0; q < QU; ++q) acc[u] += x[u][q];
+        }
+#pragma unroll
+        for (int u = 0; u < TU; ++u) {
+            const double sum = warp_sum(acc[u]);
+            const int t = t0 + u * CW;
+            if (lane == 0 && t < ntask) tot[t / nv][t - (t / nv) * nv] = sum;
+        }
     }
     __syncthreads();
 }
@@ -327,6 +353,28 @@ __device__ void face_thread_tridiag(const CoopArgs& a, const ElimDev& E, int F, 
     }
 }
 
+// Warp solve of one tridiagonal face block by parallel cyclic reduction (lane j = node j; coefficients
+// precomputed per level, ElimDev::pcr): y_F = X_FF^-1 (scale * b_F). Same result as the Cholesky sweeps up to
+// rounding (X_FF is diagonally dominant: K = L (+ M) and M on a path).
+__device__ __forceinline__ void face_warp_pcr(const ElimDev& E, int F, const double* __restrict__ b, double sc,
+                                              double* __restrict__ y, int lane) {
+    const int n = E.tri_n[F];
+    const double* __restrict__ q = E.pcr + size_t(F) * PCR_Q * 32;
+    const int node = E.pcr_node[size_t(F) * 32 + lane];
+    double co[PCR_Q];
+#pragma unroll
+    for (int k = 0; k < PCR_Q; ++k) co[k] = q[k * 32 + lane];
+    double x = lane < n ? sc * b[node] : 0.0;
+#pragma unroll
+    for (int l = 0; l < PCR_L; ++l) {
+        const int sg = 1 << l;
+        const double xm = __shfl_up_sync(0xffffffffu, x, sg), xp = __shfl_down_sync(0xffffffffu, x, sg);
+        x += co[2 * l] * xm + co[2 * l + 1] * xp;   // out-of-range neighbours carry zero coefficients
+    }
+    x *= co[2 * PCR_L];
+    if (lane < n) y[node] = x;
+}
+
 // x = X^-1 (scl * b) by exact elimination (faces -> cross points -> faces); 3 grid barriers.
 template <bool TIM>
 __device__ void elim_coop(cg::grid_group& grid, const CoopArgs& a, const ElimDev& E, const double* b,
@@ -343,7 +391,11 @@ __device__ void elim_coop(cg::grid_group& grid, const CoopArgs& a, const ElimDev
     double* xC = P.y + P.nflat;
     double* wsm = dsm + size_t(w) * a.per_warp;
     long long tf0 = clock64();
-    if (E.tri) {
+    if (E.tri && E.fuse) {   // warp per face (PCR); each face lies in one component
+        if (w > 0)
+            for (int F = gw; F < E.nfaces; F += nwarps)
+                face_warp_pcr(E, F, b, scl[ccomp(P.comp_off, P.ncomp, E.pcr_node[size_t(F) * 32])], y, lane);
+    } else if (E.tri) {
         if (w > 0)
             for (int F = gt; F < E.nfaces; F += nthr) face_thread_tridiag(a, E, F, b, scl, nullptr, y, 0, dsm + (threadIdx.x - 32));
     } else if (w > 0)
