@@ -356,23 +356,41 @@ __device__ void face_thread_tridiag(const CoopArgs& a, const ElimDev& E, int F, 
 // Warp solve of one tridiagonal face block by parallel cyclic reduction (lane j = node j; coefficients
 // precomputed per level, ElimDev::pcr): y_F = X_FF^-1 (scale * b_F). Same result as the Cholesky sweeps up to
 // rounding (X_FF is diagonally dominant: K = L (+ M) and M on a path).
-__device__ __forceinline__ void face_warp_pcr(const ElimDev& E, int F, const double* __restrict__ b, double sc,
+// NF faces per call (F0 + f * stride, f < NF; F >= nfaces skipped) with every load issued before the first use.
+template <int NF>
+__device__ __forceinline__ void face_warp_pcr(const PrecDev& P, const ElimDev& E, int F0, int stride,
+                                              const double* __restrict__ b, const double* scl,
                                               double* __restrict__ y, int lane) {
-    const int n = E.tri_n[F];
-    const double* __restrict__ q = E.pcr + size_t(F) * PCR_Q * 32;
-    const int node = E.pcr_node[size_t(F) * 32 + lane];
-    double co[PCR_Q];
+    int n[NF], node[NF];
+    double co[NF][PCR_Q], x[NF];
 #pragma unroll
-    for (int k = 0; k < PCR_Q; ++k) co[k] = q[k * 32 + lane];
-    double x = lane < n ? sc * b[node] : 0.0;
+    for (int f = 0; f < NF; ++f) {
+        const int F = F0 + f * stride;
+        const bool ok = F < E.nfaces;
+        const int Fc = ok ? F : 0;
+        n[f] = ok ? E.tri_n[Fc] : 0;
+        node[f] = E.pcr_node[size_t(Fc) * 32 + lane];
+        const double* __restrict__ q = E.pcr + size_t(Fc) * PCR_Q * 32;
+#pragma unroll
+        for (int k = 0; k < PCR_Q; ++k) co[f][k] = q[k * 32 + lane];
+    }
+#pragma unroll
+    for (int f = 0; f < NF; ++f) {
+        const double sc = scl[ccomp(P.comp_off, P.ncomp, __shfl_sync(0xffffffffu, node[f], 0))];
+        x[f] = lane < n[f] ? sc * b[node[f]] : 0.0;
+    }
 #pragma unroll
     for (int l = 0; l < PCR_L; ++l) {
         const int sg = 1 << l;
-        const double xm = __shfl_up_sync(0xffffffffu, x, sg), xp = __shfl_down_sync(0xffffffffu, x, sg);
-        x += co[2 * l] * xm + co[2 * l + 1] * xp;   // out-of-range neighbours carry zero coefficients
+#pragma unroll
+        for (int f = 0; f < NF; ++f) {
+            const double xm = __shfl_up_sync(0xffffffffu, x[f], sg), xp = __shfl_down_sync(0xffffffffu, x[f], sg);
+            x[f] += co[f][2 * l] * xm + co[f][2 * l + 1] * xp;   // out-of-range neighbours: zero coefficients
+        }
     }
-    x *= co[2 * PCR_L];
-    if (lane < n) y[node] = x;
+#pragma unroll
+    for (int f = 0; f < NF; ++f)
+        if (lane < n[f]) y[node[f]] = x[f] * co[f][2 * PCR_L];
 }
 
 // x = X^-1 (scl * b) by exact elimination (faces -> cross points -> faces); 3 grid barriers.
@@ -393,8 +411,7 @@ __device__ void elim_coop(cg::grid_group& grid, const CoopArgs& a, const ElimDev
     long long tf0 = clock64();
     if (E.tri && E.fuse) {   // warp per face (PCR); each face lies in one component
         if (w > 0)
-            for (int F = gw; F < E.nfaces; F += nwarps)
-                face_warp_pcr(E, F, b, scl[ccomp(P.comp_off, P.ncomp, E.pcr_node[size_t(F) * 32])], y, lane);
+            for (int F = gw; F < E.nfaces; F += 2 * nwarps) face_warp_pcr<2>(P, E, F, nwarps, b, scl, y, lane);
     } else if (E.tri) {
         if (w > 0)
             for (int F = gt; F < E.nfaces; F += nthr) face_thread_tridiag(a, E, F, b, scl, nullptr, y, 0, dsm + (threadIdx.x - 32));
