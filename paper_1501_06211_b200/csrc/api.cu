@@ -538,6 +538,28 @@ de_status_t upload_prec(de_ctx* c) {
                 TRY(dupload(c, &D.pcr, pq));
                 TRY(dupload(c, &D.pcr_node, pn));
             }
+            {   // G^T rows per cross point from the per-node couplings (face nodes only; ascending column)
+                std::vector<int32_t> gp(E.ncross + 1, 0), gcol;
+                std::vector<double> gval;
+                std::vector<std::vector<std::pair<int32_t, double>>> rows(E.ncross);
+                std::vector<char> isc(nfl, 0);
+                for (int ci = 0; ci < E.ncross; ++ci) isc[E.cross_flat[ci]] = 1;
+                for (size_t fl = 0; fl < nfl; ++fl) {
+                    if (isc[fl]) continue;   // cross points carry (-1, own index): not part of G^T
+                    if (gv0[fl] != 0.0) rows[gc0[fl]].push_back({int32_t(fl), gv0[fl]});
+                    if (gv1[fl] != 0.0) rows[gc1[fl]].push_back({int32_t(fl), gv1[fl]});
+                }
+                for (int ci = 0; ci < E.ncross; ++ci) {
+                    gp[ci + 1] = gp[ci] + int32_t(rows[ci].size());
+                    for (auto& q : rows[ci]) {
+                        gcol.push_back(q.first);
+                        gval.push_back(q.second);
+                    }
+                }
+                TRY(dupload(c, &D.gt_ptr, gp));
+                TRY(dupload(c, &D.gt_col, gcol));
+                TRY(dupload(c, &D.gt_val, gval));
+            }
         }
         return check_launch();
     };

@@ -177,6 +177,10 @@ struct ElimDev {
     // levels, then 1/d after the last level; pcr_node[F*32 + j] = flat index (0 past the end)
     double* pcr;
     int32_t* pcr_node;
+    // G^T = X_CF X_FF^-1 as CSR over cross points (face-node columns): t_C = scale (b_C - G^T b_F) needs only
+    // the right-hand side, so the first face phase forms it once per component (fuse only)
+    int32_t *gt_ptr, *gt_col;
+    double* gt_val;
 };
 constexpr int PCR_L = 5;             // log2(32) reduction levels
 constexpr int PCR_Q = 2 * PCR_L + 1;

@@ -53,7 +53,8 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 #define STAMP(k)                                                        \
     do {                                                                \
-        if (TIM && a.timers && blockIdx.x == 0 && threadIdx.x == 0) a.timers[k] = gtimer(); \
+        const int k_ = (k);   /* every thread advances its stamp counter */          \
+        if (TIM && a.timers && blockIdx.x == 0 && threadIdx.x == 0) a.timers[k_] = gtimer(); \
     } while (0)
 
 __device__ __forceinline__ int ccomp(const int64_t* off, int nc, int64_t i) {
@@ -412,6 +413,44 @@ __device__ void elim_coop(cg::grid_group& grid, const CoopArgs& a, const ElimDev
     if (E.tri && E.fuse) {   // warp per face (PCR); each face lies in one component
         if (w > 0)
             for (int F = gw; F < E.nfaces; F += 2 * nwarps) face_warp_pcr<2>(P, E, F, nwarps, b, scl, y, lane);
+        // t_C = scale (b_C - G^T b_F) once per cross point (needs only b), two cross points per warp in flight
+        if (w > 0) {
+            double* tCg = P.y + P.nflat + E.ncross;
+            for (int ci0 = gw; ci0 < E.ncross; ci0 += 2 * nwarps) {
+                double acc[2] = {0.0, 0.0};
+                int e0[2], e1[2], cf[2];
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const int ci = ci0 + u * nwarps;
+                    const bool ok = ci < E.ncross;
+                    e0[u] = ok ? E.gt_ptr[ci] : 0;
+                    e1[u] = ok ? E.gt_ptr[ci + 1] : 0;
+                    cf[u] = ok ? E.cross_flat[ci] : 0;
+                }
+                const int len = max(e1[0] - e0[0], e1[1] - e0[1]);
+                for (int k = lane; k < len; k += 64) {
+                    double v[2][2], x[2][2];
+#pragma unroll
+                    for (int u = 0; u < 2; ++u)
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int e = e0[u] + k + 32 * h;
+                            const bool ok = e < e1[u];
+                            v[u][h] = ok ? E.gt_val[e] : 0.0;
+                            x[u][h] = ok ? b[E.gt_col[e]] : 0.0;
+                        }
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) acc[u] += v[u][0] * x[u][0] + v[u][1] * x[u][1];
+                }
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const int ci = ci0 + u * nwarps;
+                    const double sgt = warp_sum(acc[u]);
+                    if (lane == 0 && ci < E.ncross)
+                        tCg[ci] = scl[ccomp(P.comp_off, P.ncomp, cf[u])] * (b[cf[u]] - sgt);
+                }
+            }
+        }
     } else if (E.tri) {
         if (w > 0)
             for (int F = gt; F < E.nfaces; F += nthr) face_thread_tridiag(a, E, F, b, scl, nullptr, y, 0, dsm + (threadIdx.x - 32));
@@ -422,21 +461,30 @@ __device__ void elim_coop(cg::grid_group& grid, const CoopArgs& a, const ElimDev
     __syncwarp();   // lane 0 spun in the barrier: reconverge before warp-synchronous code
     STAMP(stamp++);
     // cross points of this block's component: t_C = scl*b_C - X_CF y in smem, then rows of S_C^-1 t_C
+    const bool dbg2 = TIM && a.timers && blockIdx.x == 0 && threadIdx.x == 32 && stamp == 26;   // E2 of Lanczos step 5 (fused path)
+    if (dbg2) a.timers[180] = gtimer();
     {
         const int base = E.cross_comp_off[c], ncc = E.cross_comp_off[c + 1] - base;
         if (ncc > 0) {
             double* tC = dsm;
-            if (E.tri) {   // padded X_CF: every load of UC cross points issued before the first use
+            if (E.tri && E.fuse) {   // formed once in the first face phase
+                const double* tCg = P.y + P.nflat + E.ncross;
+                for (int i = threadIdx.x; i < ncc; i += CT) tC[i] = tCg[base + i];
+            } else if (E.tri) {   // padded X_CF: every load of UC cross points issued before the first use
                 constexpr int UC = 4;
                 const double sc = scl[c];
-                for (int i0 = threadIdx.x; i0 < ncc; i0 += CT * UC) {
+                // every block of the component reads the same inputs: start each block at a different offset so
+                // the blocks do not queue on the same L2 lines at the same time
+                const int rot = int((int64_t(lb) * 224) % ncc);
+                for (int i0 = threadIdx.x - 32; i0 < ncc; i0 += RW * UC) {   // warps 1.. (warp 0: barrier host)
+                    if (threadIdx.x < 32) break;
                     int fl[UC], col[UC][XCF_W];
                     double xv[UC][XCF_W];
 #pragma unroll
                     for (int u = 0; u < UC; ++u) {
-                        const int i = i0 + u * CT;
+                        const int i = i0 + u * RW;
                         const bool ok = i < ncc;
-                        const int ci = base + (ok ? i : 0);
+                        const int ci = base + (ok ? (i + rot < ncc ? i + rot : i + rot - ncc) : 0);
                         fl[u] = E.cross_flat[ci];
 #pragma unroll
                         for (int k = 0; k < XCF_W; ++k) {
@@ -453,11 +501,11 @@ __device__ void elim_coop(cg::grid_group& grid, const CoopArgs& a, const ElimDev
                     }
 #pragma unroll
                     for (int u = 0; u < UC; ++u) {
-                        const int i = i0 + u * CT;
+                        const int i = i0 + u * RW;
                         double t = sc * bv[u];
 #pragma unroll
                         for (int k = 0; k < XCF_W; ++k) t -= xv[u][k] * yv[u][k];
-                        if (i < ncc) tC[i] = t;
+                        if (i < ncc) tC[i + rot < ncc ? i + rot : i + rot - ncc] = t;
                     }
                 }
             } else {
@@ -469,6 +517,7 @@ __device__ void elim_coop(cg::grid_group& grid, const CoopArgs& a, const ElimDev
                 }
             }
             __syncthreads();
+            if (dbg2) a.timers[181] = gtimer();
             const double* S = E.Sinv + E.sc_off[c];
             // block lb owns the contiguous rows [rlo, rhi); warp w takes one column slice of all of them (two
             // rows at a time, NA loads per row per lane in flight); warp partials are summed in fixed order
@@ -505,7 +554,9 @@ __device__ void elim_coop(cg::grid_group& grid, const CoopArgs& a, const ElimDev
                     if (two) part[w * nr + (r + 1 - rlo)] = s1;
                 }
             }
+            if (dbg2) a.timers[182] = gtimer();
             __syncthreads();
+            if (dbg2) a.timers[183] = gtimer();
             for (int r = rlo + threadIdx.x; r < rhi; r += CT) {
                 double acc = 0.0;
                 for (int q = 0; q < CW; ++q) acc += part[q * nr + (r - rlo)];
@@ -515,8 +566,10 @@ __device__ void elim_coop(cg::grid_group& grid, const CoopArgs& a, const ElimDev
             __syncthreads();
         }
     }
+    if (dbg2) a.timers[184] = gtimer();
     grid.sync();
     __syncwarp();   // lane 0 spun in the barrier: reconverge before warp-synchronous code
+    if (dbg2) a.timers[185] = gtimer();
     STAMP(stamp++);
     if (E.tri && E.fuse) return;   // x_F = y_F - G_F x_C is formed by the consumer phase (elim_value)
     tf0 = clock64();

@@ -25,6 +25,7 @@ print("ritz_warp us", (t[101] - t[100]) / 1e3, "setup", (t[103]-t[102])/1e3, "ja
 for nm, b0 in (("A", 120), ("B", 130)):
     print(f"phase{nm} j=5: rows", (t[b0+1]-t[b0])/1e3, "partials", (t[b0+2]-t[b0+1])/1e3, "sync", (t[b0+3]-t[b0+2])/1e3, "totals", (t[b0+4]-t[b0+3])/1e3)
 print("phaseA per-warp row cycles (blocks 0-3):", list(t)[140:172])
+print("E2 (step 5): tC", (t[181]-t[180])/1e3, "gemv", (t[182]-t[181])/1e3, "syncthreads", (t[183]-t[182])/1e3, "sums", (t[184]-t[183])/1e3, "grid.sync", (t[185]-t[184])/1e3)
 print("phaseC j=5: rows", (t[111]-t[110])/1e3, "partials", (t[112]-t[111])/1e3, "sync", (t[113]-t[112])/1e3, "totals", (t[114]-t[113])/1e3)
 ts = [x for x in list(t)[:100] if x]
 d = np.diff(np.array(ts, dtype=np.float64)) / 1e3
