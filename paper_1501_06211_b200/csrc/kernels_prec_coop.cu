@@ -896,6 +896,9 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
         ZERO_VALS();
         if (part)
             for (int64_t i = r0; i < hi; i += rs) {
+                double wt[KM];   // basis loads first (the stores below may alias them for the compiler)
+#pragma unroll
+                for (int t = 0; t < KM; ++t) wt[t] = t < kc ? P.W[size_t(t) * nf + i] : 0.0;
                 double m, l, wi, unused_h[1] = {0.0};
                 if (fuseK) {
                     wi = spmv_elim(P.M, P.L, i, P.eK, P.y, P.y + nf, m, l);
@@ -907,9 +910,6 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
                 a.mw1[i] = m;
                 a.lw1[i] = l;
                 vals[0] += wi * m;
-                double wt[KM];
-#pragma unroll
-                for (int t = 0; t < KM; ++t) wt[t] = t < kc ? P.W[size_t(t) * nf + i] : 0.0;
 #pragma unroll
                 for (int t = 0; t < KM; ++t) vals[1 + t] += wt[t] * m;
             }
