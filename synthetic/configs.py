@@ -193,6 +193,42 @@ def make_config(name: str, nel=None, sub=None, seed=None, **kw) -> Problem:
     return Problem(name=tag, dim=dim, nel=nel, sub=sub, seed=seed, **d)
 
 
+def paper_problem(inv_h: int, nsub: int) -> Problem:
+    """The paper's test problem (Table 1 at PAPER.md:201-232):
+    cantilever on Omega = (0,2) x (0,1), Q1 squares of edge h = 1/inv_h, clamped on x = 2 (all components),
+    body force f = 0.75 downward, traction g = 1 on the free end x = 0 along its outward normal (-x)
+    (reading R18: the text says "outward traction"; its extent is not stated), uniform material E = 1,
+    nu = 0.3 (VTS with rho = 1: p = 1, Emin = 0), N = nsub subdomains as a sqrt(N) x sqrt(N) grid (R18),
+    rtol 1e-6 (the paper's GMRES tolerance). Consistent nodal loads: body force f h^2/4 per element node,
+    traction g h/2 per edge node."""
+    q = int(round(nsub ** 0.5))
+    if q * q != nsub:
+        raise ValueError("nsub must be a perfect square")
+    nel = (2 * inv_h, inv_h)
+    nx, ny = nel
+    if nx % q or ny % q:
+        raise ValueError("sqrt(nsub) must divide the mesh")
+    h = 1.0 / inv_h
+    nn = 2 * (nx + 1) * (ny + 1)
+    fixed = np.zeros(nn, dtype=np.uint8)
+    for j in range(ny + 1):
+        nd = _node(nel, nx, j)
+        fixed[2 * nd:2 * nd + 2] = 1
+    f = np.zeros(nn)
+    cnt = np.zeros((ny + 1, nx + 1))          # elements touching each node
+    cnt[:-1, :-1] += 1
+    cnt[1:, :-1] += 1
+    cnt[:-1, 1:] += 1
+    cnt[1:, 1:] += 1
+    f[1::2] = -0.75 * h * h / 4.0 * cnt.ravel()
+    for j in range(ny + 1):
+        w = 0.5 if j in (0, ny) else 1.0
+        f[2 * _node(nel, 0, j)] += -1.0 * h * w
+    return Problem(name=f"paper[h=1/{inv_h},N={nsub}]", dim=2, nel=nel, sub=(nx // q, ny // q), fixed=fixed,
+                   density=np.ones(nx * ny), rhs=f, E0=1.0, Emin=0.0, p=1.0, nu=0.3, h=h, rtol=1e-6,
+                   meta=dict(inv_h=inv_h, nsub=nsub))
+
+
 def density_sequence_step(rho: np.ndarray, t: int, base_seed: int = 5000) -> np.ndarray:
     """Config-5 density evolution: rho <- clip(rho*(1+0.05*U[-1,1]), 1e-3, 1)
     with U drawn from default_rng(base_seed + t)."""
