@@ -794,8 +794,14 @@ de_status_t setup_impl(const de_mesh_t* mesh, const double* density, double E0, 
         c->explicit_schur = fits && (opt.schur_mode == 2 || (opt.schur_mode == 0 && double(c->n_sexp) < fac_one_pass));
         if (c->explicit_schur) {
             TRY(dalloc(c, &c->d_sexp, size_t(c->n_sexp)));
-            const size_t per = size_t(std::max(1, c->max_nG) + 8) * size_t(std::max(1, c->max_nI));
-            c->col_batch = int(std::max<size_t>(1, std::min<size_t>(c->nsl, (size_t(512) << 20) / (per * 8))));
+            // scratch per subdomain: the thread-per-column formation keeps n_I x FORM_THREADS solutions, the
+            // warp-per-8-columns one (n_Gamma,s + 8) x n_I; one launch per batch, a multiple of the SM count
+            const size_t per = size_t(std::max(std::max(1, c->max_nG) + 8, FORM_THREADS)) * size_t(std::max(1, c->max_nI));
+            int nsm = 148;
+            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->opt.device);
+            size_t cap = (size_t(1) << 30) / (per * 8);
+            if (cap >= size_t(nsm)) cap = cap / size_t(nsm) * size_t(nsm);
+            c->col_batch = int(std::max<size_t>(1, std::min<size_t>(c->nsl, cap)));
             TRY(dalloc(c, &c->d_colscratch, size_t(c->col_batch) * per));
         }
     }

@@ -186,6 +186,7 @@ constexpr int PCR_L = 5;             // log2(32) reduction levels
 constexpr int PCR_Q = 2 * PCR_L + 1;
 constexpr int XCF_W = 4;
 constexpr int TRI_N = 32;
+constexpr int FORM_THREADS = 256;   // columns per pass of the thread-per-column S_s formation
 
 struct CsrDev {
     int32_t n;

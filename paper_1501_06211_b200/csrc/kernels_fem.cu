@@ -116,48 +116,8 @@ void launch_assemble_pairs(const MeshDev& m, const int32_t* da, const int32_t* d
 
 // ---------------------------------------------------------------- B2: band Cholesky
 
-// 2D: the active window of columns [j, j+bw] lives in shared memory (slot = col % (bw+1)).
-__global__ void __launch_bounds__(256) k_band_chol_smem(const SubDesc* __restrict__ sd, double* __restrict__ band,
-                                                        int ld, int bw, int* __restrict__ fail) {
-    extern __shared__ double sm[];
-    const int W = bw + 1;
-    double* win = sm;                 // W * ld
-    double* l = win + W * ld;         // ld
-    const SubDesc d = sd[blockIdx.x];
-    const int n = d.nI;
-    double* base = band + d.band_off;
-    double* Mb = base + int64_t(n) * ld;
-    const int tid = threadIdx.x, nt = blockDim.x;
-    for (int i = tid; i < W * ld; i += nt) {
-        const int c = i / ld;
-        win[i] = c < n ? base[int64_t(c) * ld + (i - c * ld)] : 0.0;
-    }
-    __syncthreads();
-    for (int j = 0; j < n; ++j) {
-        double* cj = win + (j % W) * ld;
-        const double dj = cj[0];
-        const bool bad = !(dj > 0.0);
-        const double inv = bad ? 1.0 : 1.0 / sqrt(dj);
-        if (bad && tid == 0) atomicCAS(fail, 0, d.gid + 1);
-        for (int k = tid; k < ld; k += nt) l[k] = (k == 0) ? inv : (k <= bw ? cj[k] * inv : 0.0);
-        __syncthreads();
-        for (int k = tid; k < ld; k += nt) {
-            base[int64_t(j) * ld + k] = l[k];
-            if (k <= bw && j + k < n) Mb[int64_t(n - 1 - j - k) * ld + k] = l[k];   // M = P L^T P
-        }
-        // rank-1 update of columns j+1..j+bw: (m, r) with m in [1,bw], r in [0, bw-m]
-        for (int t = tid; t < bw * W; t += nt) {
-            const int mm = 1 + t / W, rem = t - (mm - 1) * W;
-            if (rem <= bw - mm && j + mm < n) win[((j + mm) % W) * ld + rem] -= l[mm + rem] * l[mm];
-        }
-        __syncthreads();
-        const int cn = j + W;   // next column enters the freed slot
-        for (int k = tid; k < ld; k += nt) cj[k] = cn < n ? base[int64_t(cn) * ld + k] : 0.0;
-        __syncthreads();
-    }
-}
-
-// 3D: 32-column panels factored in shared memory; trailing update in global memory.
+// 32-column panels factored in shared memory; trailing update in global memory (2D and 3D; measured on c5:
+// 16 ms against 39 ms for a column-at-a-time shared-memory window).
 constexpr int NBP = 32;
 __global__ void __launch_bounds__(512) k_band_chol_panel(const SubDesc* __restrict__ sd, double* __restrict__ band,
                                                          int ld, int bw, int* __restrict__ fail) {
@@ -217,15 +177,9 @@ __global__ void __launch_bounds__(512) k_band_chol_panel(const SubDesc* __restri
 int launch_band_cholesky(const SubDesc* sd, int nsl, double* band, int ld, int band_w, int* d_fail,
                          cudaStream_t st) {
     if (nsl == 0) return 0;
-    const size_t smem_win = (size_t(band_w + 1) * ld + ld) * sizeof(double);
-    if (smem_win <= 100 * 1024) {
-        cudaFuncSetAttribute(k_band_chol_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_win));
-        k_band_chol_smem<<<nsl, 256, smem_win, st>>>(sd, band, ld, band_w, d_fail);
-    } else {
-        const size_t smem = size_t(NBP) * ld * sizeof(double);
-        cudaFuncSetAttribute(k_band_chol_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        k_band_chol_panel<<<nsl, 512, smem, st>>>(sd, band, ld, band_w, d_fail);
-    }
+    const size_t smem = size_t(NBP) * ld * sizeof(double);
+    cudaFuncSetAttribute(k_band_chol_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    k_band_chol_panel<<<nsl, 512, smem, st>>>(sd, band, ld, band_w, d_fail);
     return 1;
 }
 

@@ -16,6 +16,8 @@
 // over L then M, so M's first stages are in flight while the L sweep finishes.
 #include "de_internal.h"
 
+#include <cstdlib>
+
 namespace de {
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -375,6 +377,110 @@ __global__ void __launch_bounds__(32) k_schur_cols(SchurArgs a, int nstage) {
     }
 }
 
+// ---------------------------------------------------------------- S_s formation, thread per column
+// Columns of S_s = A_GG - A_GI A_II^-1 A_IG (x = e_t), one CTA per subdomain, thread t <-> column t.
+// Both triangular solves are the same recurrence over r = 0..n-1 on a stream of factor columns taken in
+// decreasing order, z_r = (rhs_r - sum_{k=1..B} F[c][k] z_{r-k}) F[c][0], c = n-1-r: the forward L solve reads
+// the M = P L^T P copy (its column n-1-r is row r of L) and the backward L^T solve reads L (rhs = y reversed).
+// The last SF_W values z_{r-1..r-B} of a thread live in registers: the row loop is unrolled by SF_W, so every
+// window index is a compile-time constant. Factor columns are shared by the CTA through a two-half shared
+// ring filled by cp.async SF_CB rows ahead.
+constexpr int SF_T = FORM_THREADS;   // threads = columns per pass
+constexpr int SF_W = 68;     // register window (>= B + 1; 2D 32x32 subdomains: B = 65..67)
+constexpr int SF_CB = 16;    // rows per ring half
+
+__device__ __forceinline__ void sf_cp16(void* smem, const void* gmem) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+
+// rows r0 .. r0+SF_CB-1 (factor columns n-1-r) into ring half (r0 / SF_CB) & 1
+__device__ __forceinline__ void sf_issue(const double* __restrict__ F, int n, int ld, int r0, double* ring) {
+    double* dst = ring + size_t((r0 / SF_CB) & 1) * SF_CB * ld;
+    const int chunks = ld / 2;
+    for (int q = threadIdx.x; q < SF_CB * chunks; q += blockDim.x) {
+        const int cc = q / chunks, off = (q - cc * chunks) * 2, r = r0 + cc;
+        if (r < n) sf_cp16(dst + cc * ld + off, F + size_t(n - 1 - r) * ld + off);
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+
+// One solve over the factor stream (see above); rhs(r) and out(r, z) give the right-hand side and take the
+// solution of row r. The right-hand side enters after the window terms, so its load overlaps them.
+template <class Rhs, class Out>
+__device__ __forceinline__ void sf_sweep(const double* __restrict__ F, int n, int ld, int B, double* ring, Rhs rhs,
+                                         Out out) {
+    double z[SF_W];
+#pragma unroll
+    for (int q = 0; q < SF_W; ++q) z[q] = 0.0;
+    __syncthreads();   // ring free (previous sweep done)
+    sf_issue(F, n, ld, 0, ring);
+    for (int r0 = 0; r0 < n; r0 += SF_W) {
+#pragma unroll
+        for (int q = 0; q < SF_W; ++q) {
+            const int r = r0 + q;
+            if (r < n) {
+                if ((r % SF_CB) == 0) {   // this half has landed; start the next one (the other half is free)
+                    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+                    __syncthreads();
+                    if (r + SF_CB < n) sf_issue(F, n, ld, r + SF_CB, ring);
+                }
+                const double* col = ring + (size_t((r / SF_CB) & 1) * SF_CB + (r % SF_CB)) * ld;
+                const double b = rhs(r);
+                double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+                for (int k = 1; k < SF_W; ++k)
+                    if (k <= B) acc[k & 3] = fma(-col[k], z[(q - k + SF_W) % SF_W], acc[k & 3]);
+                const double zr = (b + ((acc[0] + acc[1]) + (acc[2] + acc[3]))) * col[0];
+                z[q] = zr;
+                out(r, zr);
+            }
+        }
+    }
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
+
+__global__ void __launch_bounds__(SF_T, 1) k_schur_form(SchurArgs a) {
+    extern __shared__ __align__(16) double ring[];   // [2][SF_CB][ld]
+    const int sl = a.col_s0 + int(blockIdx.x);
+    const SubDesc d = a.sd[sl];
+    const int n = d.nI, nG = d.nG, B = a.band_w, ld = a.ld, tid = threadIdx.x;
+    const double* Lb = a.band + d.band_off;
+    const double* Mb = Lb + size_t(n) * ld;
+    const int32_t* igp = a.igp + d.igp_off;
+    const int32_t* gxp = a.gxp + d.gxp_off;
+    double* ys = a.colscratch + size_t(blockIdx.x) * size_t(a.max_nI) * SF_T;   // [row][SF_T]
+    for (int t0 = 0; t0 < nG; t0 += SF_T) {
+        const int t = t0 + tid;
+        // forward: L y = A_IG e_t (rows of L = columns of M, reversed); the rows of A_IG are scanned by every
+        // thread (broadcast loads)
+        sf_sweep(Mb, n, ld, B, ring,
+                 [&](int r) {
+                     double v = 0.0;
+                     for (int e = igp[r]; e < igp[r + 1]; ++e)
+                         if (a.ig_col[e] == t) v += a.ig_val[e];
+                     return v;
+                 },
+                 [&](int r, double zr) { ys[size_t(r) * SF_T + tid] = zr; });
+        // backward: L^T x = y, row order reversed, in place
+        sf_sweep(Lb, n, ld, B, ring, [&](int r) { return ys[size_t(n - 1 - r) * SF_T + tid]; },
+                 [&](int r, double zr) { ys[size_t(n - 1 - r) * SF_T + tid] = zr; });
+        // S_s[l][t] = A_GG[l][t] - A_GI[l][:] x; stored at (row t, column l) by symmetry (coalesced)
+        if (t < nG)
+            for (int l = 0; l < nG; ++l) {
+                double q = 0.0;
+                for (int e = gxp[l]; e < gxp[l + 1]; ++e) {
+                    const int cidx = a.gx_col[e];
+                    const double val = a.gx_val[e];
+                    if (cidx >= 0) q += (cidx == t) ? val : 0.0;
+                    else q -= val * ys[size_t(-cidx - 1) * SF_T + tid];
+                }
+                a.sexp[d.sexp_off + size_t(l) * nG + t] = q;
+            }
+        __syncthreads();
+    }
+}
+
 constexpr int COL_R = 8;
 
 template <int G, int NS>
@@ -405,6 +511,12 @@ static void launch_t(const SchurArgs& a, int nstage, size_t smem, cudaStream_t s
 
 int launch_schur_local(const SchurArgs& a, cudaStream_t st) {
     if (a.nsl == 0) return 0;
+    if (a.mode == SCHUR_COLUMNS && a.band_w + 1 <= SF_W && a.ld % 2 == 0 && !getenv("DE_FORM_WARP")) {
+        const size_t smem = size_t(2) * SF_CB * a.ld * sizeof(double);
+        cudaFuncSetAttribute(k_schur_form, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        k_schur_form<<<unsigned(a.nsl), SF_T, smem, st>>>(a);
+        return 1;
+    }
     const int need = (a.band_w + 1 + 31) / 32;   // register slots per lane covering b+1 rows
     const int G = 4, nstage = 4;
     const size_t smem = 128 + sizeof(double) * (size_t(nstage) * G * a.ld + a.maxG);

@@ -67,7 +67,19 @@ def test_bands_match_oracle(name, kw):
             b = blocks[sl]
             kb = b.band
             ref = b.chol.T          # scipy lower band: chol[k, j] = L[j+k, j]
-            assert np.abs(L[:, :kb + 1] - ref).max() <= 1e-11 * np.abs(ref).max()
+            # backward error of the GPU factor (independent of the summation order): Cholesky gives
+            # |L L^T - A| <= (b+2) eps |L||L^T| elementwise (Higham, Thm 10.3); checked normwise with a x4 margin
+            n = L.shape[0]
+            Ld = np.zeros((n, n))
+            for k in range(kb + 1):
+                idx = np.arange(n - k)
+                Ld[idx + k, idx] = L[:n - k, k]
+            Ad = b.AII.toarray()
+            bound = 4 * (kb + 2) * np.finfo(float).eps * (np.abs(Ld) @ np.abs(Ld).T).max()
+            assert np.abs(Ld @ Ld.T - Ad).max() <= bound
+            # forward agreement with scipy's factor: each side has the backward error above, so they differ by
+            # about kappa * (b+2) eps; 1e-9 covers the high-contrast c3 instance (densities 1e-3 .. 1)
+            assert np.abs(L[:, :kb + 1] - ref).max() <= 1e-9 * np.abs(ref).max()
             assert np.all(L[:, kb + 1:] == 0)
     finally:
         S.close()
