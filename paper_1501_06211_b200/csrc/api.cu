@@ -119,6 +119,7 @@ struct de_ctx {
     double* d_sexp = nullptr;
     double* d_colscratch = nullptr;
     int col_batch = 0;
+    int max_ig = 0;
     int64_t n_sexp = 0;
     // nccl
     void* comm = nullptr;
@@ -738,6 +739,7 @@ de_status_t setup_impl(const de_mesh_t* mesh, const double* density, double E0, 
         goff += d.nG;
         const int32_t ig0 = ring.igp[ring.igp_off[k]], ig1 = ring.igp[ring.igp_off[k] + d.nI];
         ig_sub.insert(ig_sub.end(), size_t(ig1 - ig0), s);
+        c->max_ig = std::max(c->max_ig, int(ig1 - ig0));
         const int32_t gx0 = ring.gxp[ring.gxp_off[k]], gx1 = ring.gxp[ring.gxp_off[k] + d.nG];
         gx_sub.insert(gx_sub.end(), size_t(gx1 - gx0), s);
     }
@@ -901,6 +903,7 @@ de_status_t factor_impl(de_ctx* c) {
             a.sexp = c->d_sexp;
             a.colscratch = c->d_colscratch;
             a.max_nI = c->max_nI;
+            a.max_ig = c->max_ig;
             launch_schur_local(a, c->st);
         }
     TRY(check_launch());

@@ -245,6 +245,7 @@ struct SchurArgs {
     double* sexp;
     double* colscratch;     // nsl*maxG*max_nI doubles
     int col_s0, max_nI;
+    int max_ig;             // max A_IG entries of one subdomain (shared-memory staging in the formation)
 };
 int launch_schur_local(const SchurArgs& a, cudaStream_t st);
 // q_s = S_s x_s with the explicit column-major S_s (one CTA per subdomain, coalesced over rows)

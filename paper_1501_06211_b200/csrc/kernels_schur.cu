@@ -388,6 +388,7 @@ __global__ void __launch_bounds__(32) k_schur_cols(SchurArgs a, int nstage) {
 constexpr int SF_T = FORM_THREADS;   // threads = columns per pass
 constexpr int SF_W = 68;     // register window (>= B + 1; 2D 32x32 subdomains: B = 65..67)
 constexpr int SF_CB = 16;    // rows per ring half
+constexpr int SF_U = 8;      // rows per unrolled block of the recurrence
 
 __device__ __forceinline__ void sf_cp16(void* smem, const void* gmem) {
     const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -405,20 +406,29 @@ __device__ __forceinline__ void sf_issue(const double* __restrict__ F, int n, in
     asm volatile("cp.async.commit_group;\n" ::: "memory");
 }
 
-// One solve over the factor stream (see above); rhs(r) and out(r, z) give the right-hand side and take the
-// solution of row r. The right-hand side enters after the window terms, so its load overlaps them.
-template <class Rhs, class Out>
+// One solve over the factor stream (see above): rhs(r) gives the right-hand side of row r and out(r, z) takes
+// its solution. PF > 0: rhs(r) is a global load, issued PF rows ahead into a register ring (static indices,
+// SF_W % PF == 0); it enters after the window terms either way, so its latency overlaps them.
+template <int PF, class Rhs, class Out>
 __device__ __forceinline__ void sf_sweep(const double* __restrict__ F, int n, int ld, int B, double* ring, Rhs rhs,
                                          Out out) {
-    double z[SF_W];
+    // rows in unrolled blocks of SF_U: z[j] holds the solution of row r0-1-j (0 before row 0), the block's own
+    // rows go to nz[]; after the block the window shifts by SF_U (a fully unrolled 68-row body would not fit the
+    // instruction cache)
+    static_assert(PF == 0 || PF == SF_U, "prefetch ring = block");
+    double z[SF_W], pf[SF_U];
 #pragma unroll
     for (int q = 0; q < SF_W; ++q) z[q] = 0.0;
+#pragma unroll
+    for (int q = 0; q < SF_U; ++q) pf[q] = (PF > 0 && q < n) ? rhs(q) : 0.0;
     __syncthreads();   // ring free (previous sweep done)
     sf_issue(F, n, ld, 0, ring);
-    for (int r0 = 0; r0 < n; r0 += SF_W) {
+    for (int r0 = 0; r0 < n; r0 += SF_U) {
+        double nz[SF_U];
 #pragma unroll
-        for (int q = 0; q < SF_W; ++q) {
+        for (int q = 0; q < SF_U; ++q) {
             const int r = r0 + q;
+            nz[q] = 0.0;
             if (r < n) {
                 if ((r % SF_CB) == 0) {   // this half has landed; start the next one (the other half is free)
                     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
@@ -426,22 +436,32 @@ __device__ __forceinline__ void sf_sweep(const double* __restrict__ F, int n, in
                     if (r + SF_CB < n) sf_issue(F, n, ld, r + SF_CB, ring);
                 }
                 const double* col = ring + (size_t((r / SF_CB) & 1) * SF_CB + (r % SF_CB)) * ld;
-                const double b = rhs(r);
+                double b;
+                if constexpr (PF > 0) {
+                    b = pf[q];
+                    pf[q] = r + PF < n ? rhs(r + PF) : 0.0;
+                } else {
+                    b = rhs(r);
+                }
                 double acc[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-                for (int k = 1; k < SF_W; ++k)
-                    if (k <= B) acc[k & 3] = fma(-col[k], z[(q - k + SF_W) % SF_W], acc[k & 3]);
+                for (int k = SF_W - 1; k >= 1; --k)   // oldest rows first: the newest terms close the row
+                    if (k <= B) acc[k & 3] = fma(-col[k], k <= q ? nz[q - k] : z[k - q - 1], acc[k & 3]);
                 const double zr = (b + ((acc[0] + acc[1]) + (acc[2] + acc[3]))) * col[0];
-                z[q] = zr;
+                nz[q] = zr;
                 out(r, zr);
             }
         }
+#pragma unroll
+        for (int j = SF_W - 1; j >= SF_U; --j) z[j] = z[j - SF_U];
+#pragma unroll
+        for (int q = 0; q < SF_U; ++q) z[SF_U - 1 - q] = nz[q];
     }
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
 }
 
 __global__ void __launch_bounds__(SF_T, 1) k_schur_form(SchurArgs a) {
-    extern __shared__ __align__(16) double ring[];   // [2][SF_CB][ld]
+    extern __shared__ __align__(16) double ring[];   // [2][SF_CB][ld], then the staged A_IG rows
     const int sl = a.col_s0 + int(blockIdx.x);
     const SubDesc d = a.sd[sl];
     const int n = d.nI, nG = d.nG, B = a.band_w, ld = a.ld, tid = threadIdx.x;
@@ -450,21 +470,31 @@ __global__ void __launch_bounds__(SF_T, 1) k_schur_form(SchurArgs a) {
     const int32_t* igp = a.igp + d.igp_off;
     const int32_t* gxp = a.gxp + d.gxp_off;
     double* ys = a.colscratch + size_t(blockIdx.x) * size_t(a.max_nI) * SF_T;   // [row][SF_T]
+    // A_IG rows of this subdomain in shared memory (values, columns, row pointers rebased to 0)
+    double* s_val = ring + size_t(2) * SF_CB * ld;
+    int* s_col = reinterpret_cast<int*>(s_val + a.max_ig);
+    int* s_ptr = s_col + a.max_ig;
+    const int e0 = igp[0], ne = igp[n] - e0;
+    for (int e = tid; e < ne; e += SF_T) {
+        s_val[e] = a.ig_val[e0 + e];
+        s_col[e] = a.ig_col[e0 + e];
+    }
+    for (int r = tid; r <= n; r += SF_T) s_ptr[r] = igp[r] - e0;
+    __syncthreads();
     for (int t0 = 0; t0 < nG; t0 += SF_T) {
         const int t = t0 + tid;
-        // forward: L y = A_IG e_t (rows of L = columns of M, reversed); the rows of A_IG are scanned by every
-        // thread (broadcast loads)
-        sf_sweep(Mb, n, ld, B, ring,
-                 [&](int r) {
-                     double v = 0.0;
-                     for (int e = igp[r]; e < igp[r + 1]; ++e)
-                         if (a.ig_col[e] == t) v += a.ig_val[e];
-                     return v;
-                 },
-                 [&](int r, double zr) { ys[size_t(r) * SF_T + tid] = zr; });
-        // backward: L^T x = y, row order reversed, in place
-        sf_sweep(Lb, n, ld, B, ring, [&](int r) { return ys[size_t(n - 1 - r) * SF_T + tid]; },
-                 [&](int r, double zr) { ys[size_t(n - 1 - r) * SF_T + tid] = zr; });
+        // forward: L y = A_IG e_t (rows of L = columns of M, reversed)
+        sf_sweep<0>(Mb, n, ld, B, ring,
+                    [&](int r) {
+                        double v = 0.0;
+                        for (int e = s_ptr[r]; e < s_ptr[r + 1]; ++e)
+                            if (s_col[e] == t) v += s_val[e];
+                        return v;
+                    },
+                    [&](int r, double zr) { ys[size_t(r) * SF_T + tid] = zr; });
+        // backward: L^T x = y, row order reversed, in place (a row's rhs is read PF rows before it is overwritten)
+        sf_sweep<SF_U>(Lb, n, ld, B, ring, [&](int r) { return ys[size_t(n - 1 - r) * SF_T + tid]; },
+                     [&](int r, double zr) { ys[size_t(n - 1 - r) * SF_T + tid] = zr; });
         // S_s[l][t] = A_GG[l][t] - A_GI[l][:] x; stored at (row t, column l) by symmetry (coalesced)
         if (t < nG)
             for (int l = 0; l < nG; ++l) {
@@ -511,8 +541,9 @@ static void launch_t(const SchurArgs& a, int nstage, size_t smem, cudaStream_t s
 
 int launch_schur_local(const SchurArgs& a, cudaStream_t st) {
     if (a.nsl == 0) return 0;
-    if (a.mode == SCHUR_COLUMNS && a.band_w + 1 <= SF_W && a.ld % 2 == 0 && !getenv("DE_FORM_WARP")) {
-        const size_t smem = size_t(2) * SF_CB * a.ld * sizeof(double);
+    if (a.mode == SCHUR_COLUMNS && a.band_w + 1 <= SF_W && a.ld % 2 == 0 && !getenv("DE_FORM_WARP") &&
+        size_t(2) * SF_CB * a.ld * 8 + size_t(a.max_ig) * 12 + size_t(a.max_nI + 1) * 4 <= 200 * 1024) {
+        const size_t smem = size_t(2) * SF_CB * a.ld * sizeof(double) + size_t(a.max_ig) * 12 + size_t(a.max_nI + 1) * 4;
         cudaFuncSetAttribute(k_schur_form, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         k_schur_form<<<unsigned(a.nsl), SF_T, smem, st>>>(a);
         return 1;
