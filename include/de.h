@@ -95,6 +95,10 @@ typedef struct {
                                 bytes than one pass over the factors, i.e. 2D), 1 = implicit through interior
                                 solves, 2 = explicit local Schur complements S_s formed at
                                 de_factor; condense/back-substitution always use the solves */
+    int32_t weighted_trace;  /* 1: coefficient-weighted trace norm (R19): every trace
+                                facet element of M and L is scaled by the mean SIMP modulus of its two adjacent
+                                elements; the preconditioner is rebuilt by de_factor after each density update.
+                                0 (default): the unweighted norm of PAPER.md:172 (R6) */
 } de_options_t;
 
 typedef struct {

@@ -129,10 +129,10 @@ class ComponentData:
         return x
 
 
-def build_components(prob, topo):
+def build_components(prob, topo, weighted=False):
     comps = []
     for skel in component_skeletons(prob, topo):
-        M, L, singular = component_trace_matrices(prob, skel)
+        M, L, singular = component_trace_matrices(prob, skel, weighted)
         K = (L + M).tocsr() if singular else L
         cd = ComponentData(skel, M, L, singular, K)
         cd.inner_its = []

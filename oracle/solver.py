@@ -43,10 +43,11 @@ class DDResult:
 class DDOracle:
     """Setup/factor/solve split mirroring de_setup / de_factor / de_solve."""
 
-    def __init__(self, prob, mode="lanczos", theta=0.5, k=10, inner="X", beta="FR"):
+    def __init__(self, prob, mode="lanczos", theta=0.5, k=10, inner="X", beta="FR", weighted=False):
         self.prob = prob
         self.topo = build_topology(prob)
-        self.comps = build_components(prob, self.topo) if mode != "identity" else []
+        self.weighted = weighted
+        self.comps = build_components(prob, self.topo, weighted) if mode != "identity" else []
         self.mode, self.theta, self.k, self.inner, self.beta = mode, theta, k, inner, beta
         self.blocks = None
         self.uG_prev = None
@@ -54,6 +55,8 @@ class DDOracle:
     def factor(self, prob=None):
         if prob is not None:
             self.prob = prob
+            if self.weighted and self.mode != "identity":   # R19: the weighted norm follows the densities
+                self.comps = build_components(self.prob, self.topo, True)
         self.blocks = factor_subdomains(subdomain_blocks(self.prob, self.topo))
 
     def S(self, x):

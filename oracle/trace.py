@@ -5,7 +5,12 @@ respectively assembled on the interface Gamma"), Eq.(9)
 (applied component-wise).  Readings: R6 trace elements are the
 element facets (edges in 2D, faces in 3D) whose two adjacent elements lie in
 different subdomains; linear (2D) / bilinear (3D) facet elements; Dirichlet
-rows/columns of component c eliminated; no coefficient weighting.  R7: a
+rows/columns of component c eliminated; no coefficient weighting by default.
+NEXT(3) / R19 (weighted=True): every facet element is scaled by the mean modulus
+(E_a + E_b)/2 of its two adjacent elements (SIMP moduli of the current densities),
+the coefficient-weighted trace norm of SURVEY.md §8(f); pinned by uniform density
+(weighted = E x unweighted, preconditioner / E) and by one face between two uniform
+subdomains (weight (E_a + E_b)/2), tests/test_weighted_trace.py.  R7: a
 component whose skeleton has a connected piece without Dirichlet contact is
 "singular" (L_c has constants in its kernel).
 
@@ -37,15 +42,16 @@ def facet_matrices(dim: int, h: float):
     return M, L
 
 
-def trace_facets(prob):
+def trace_facets(prob, with_elements=False):
     """Node ids [nf, 2^(d-1)] of every facet shared by two elements of different
-    subdomains (facet-local lexicographic node order)."""
+    subdomains (facet-local lexicographic node order); with_elements: also the two
+    adjacent element ids [nf, 2]."""
     dim, nel = prob.dim, tuple(prob.nel)
     esub = element_subdomain(dim, nel, prob.sub)
     enodes = element_dofs(dim, nel)[:, ::dim] // dim
     offs = local_nodes(dim)
     coords = np.stack(np.unravel_index(np.arange(np.prod(nel)), tuple(reversed(nel))), 1)[:, ::-1]
-    out = []
+    out, els = [], []
     for a in range(dim):
         stride = int(np.prod(nel[:a]))
         has_nb = coords[:, a] < nel[a] - 1
@@ -53,20 +59,30 @@ def trace_facets(prob):
         e = e[esub[e] != esub[e + stride]]
         cols = [i for i, o in enumerate(offs) if o[a] == 1]   # lexicographic in remaining axes
         out.append(enodes[e][:, cols])
-    return np.concatenate(out, axis=0) if out else np.zeros((0, 2 ** (dim - 1)), dtype=np.int64)
+        els.append(np.stack([e, e + stride], axis=1))
+    F = np.concatenate(out, axis=0) if out else np.zeros((0, 2 ** (dim - 1)), dtype=np.int64)
+    if with_elements:
+        return F, (np.concatenate(els, axis=0) if els else np.zeros((0, 2), dtype=np.int64))
+    return F
 
 
-def component_trace_matrices(prob, skel):
-    """(M_c, L_c, singular_c) as CSR over positions in skel.nodes."""
+def component_trace_matrices(prob, skel, weighted=False):
+    """(M_c, L_c, singular_c) as CSR over positions in skel.nodes; weighted: facet elements scaled by the
+    mean SIMP modulus of their two adjacent elements (R19)."""
+    from .fem import simp_modulus
     dim = prob.dim
     Mf, Lf = facet_matrices(dim, prob.h)
-    F = trace_facets(prob)
+    F, FE = trace_facets(prob, with_elements=True)
     nn = prob.nnodes
     m = F.shape[1]
     rows = np.repeat(F, m, axis=1).ravel()
     cols = np.tile(F, (1, m)).ravel()
-    Mfull = sp.coo_matrix((np.tile(Mf.ravel(), len(F)), (rows, cols)), shape=(nn, nn)).tocsr()
-    Lfull = sp.coo_matrix((np.tile(Lf.ravel(), len(F)), (rows, cols)), shape=(nn, nn)).tocsr()
+    w = np.ones(len(F))
+    if weighted:
+        E = simp_modulus(prob.density, prob.E0, prob.Emin, prob.p)
+        w = 0.5 * (E[FE[:, 0]] + E[FE[:, 1]])
+    Mfull = sp.coo_matrix(((w[:, None] * Mf.ravel()[None, :]).ravel(), (rows, cols)), shape=(nn, nn)).tocsr()
+    Lfull = sp.coo_matrix(((w[:, None] * Lf.ravel()[None, :]).ravel(), (rows, cols)), shape=(nn, nn)).tocsr()
     tn = np.unique(F)
     fixed_c = prob.fixed[dim * tn + skel.c] != 0
     keep = tn[~fixed_c]

@@ -82,6 +82,9 @@ struct de_ctx {
     int64_t n_local_I = 0, n_local_G = 0;
     // device memory
     std::vector<void*> allocs;
+    std::vector<void*> prec_allocs;   // preconditioner buffers (freed and rebuilt for the weighted norm)
+    bool in_prec = false;             // dalloc records into prec_allocs
+    bool dens_dirty = false;          // densities changed since the preconditioner was built
     SubDesc* d_sd = nullptr;
     double *d_rho = nullptr, *d_Ee = nullptr;
     int8_t* d_cls = nullptr;
@@ -137,7 +140,7 @@ de_status_t dalloc(de_ctx* c, T** p, size_t n) {
         set_error("cudaMalloc(%zu bytes) failed: %s", n * sizeof(T), cudaGetErrorString(e));
         return e == cudaErrorMemoryAllocation ? DE_ENOMEM : DE_ECUDA;
     }
-    c->allocs.push_back(*p);
+    (c->in_prec ? c->prec_allocs : c->allocs).push_back(*p);
     return DE_OK;
 }
 
@@ -336,7 +339,41 @@ de_status_t masked_norm2(de_ctx* c, const double* f, double* out_host) {
     return DE_OK;
 }
 
+de_status_t upload_prec_impl(de_ctx* c);
+
+// Every preconditioner buffer is recorded in c->prec_allocs, so the weighted norm (R19) can rebuild it.
 de_status_t upload_prec(de_ctx* c) {
+    c->in_prec = true;
+    const de_status_t s = upload_prec_impl(c);
+    c->in_prec = false;
+    return s;
+}
+
+// Weighted trace norm after a density update (R19): host rebuild of M, L, K and the eliminations from the new
+// element moduli, then a fresh device upload (the PCG graph holds the old pointers: rebuilt on next use).
+de_status_t rebuild_weighted_prec(de_ctx* c) {
+    HostSetup& hs = c->hs;
+    std::vector<double> rho(hs.nelem);
+    DE_CUDA(cudaMemcpyAsync(rho.data(), c->d_rho, sizeof(double) * hs.nelem, cudaMemcpyDeviceToHost, c->st));
+    DE_CUDA(cudaStreamSynchronize(c->st));
+    hs.trace_E.resize(hs.nelem);
+    for (int64_t e = 0; e < hs.nelem; ++e) hs.trace_E[e] = c->Emin + std::pow(rho[e], c->p) * (c->E0 - c->Emin);
+    TRY(build_trace(hs, hs.trace_E.data()));
+    if (c->gexec) {
+        cudaGraphExecDestroy(c->gexec);
+        c->gexec = nullptr;
+    }
+    for (void* p : c->prec_allocs) cudaFree(p);
+    c->prec_allocs.clear();
+    c->P = PrecDev{};
+    c->coop = CoopBuffers{};
+    c->have_prec = c->use_coop = false;
+    TRY(upload_prec(c));
+    c->dens_dirty = false;
+    return DE_OK;
+}
+
+de_status_t upload_prec_impl(de_ctx* c) {
     HostSetup& hs = c->hs;
     PrecDev& P = c->P;
     P.ncomp = hs.ncomp;
@@ -678,6 +715,12 @@ de_status_t setup_impl(const de_mesh_t* mesh, const double* density, double E0, 
     c->nu = nu;
     c->rank = opt.rank;
     c->nranks = opt.nranks;
+    if (opt.weighted_trace) {   // R19: element moduli of the setup densities
+        int64_t ne = 1;
+        for (int a = 0; a < mesh->dim; ++a) ne *= mesh->nel[a];
+        c->hs.trace_E.resize(ne);
+        for (int64_t e = 0; e < ne; ++e) c->hs.trace_E[e] = Emin + std::pow(density[e], p) * (E0 - Emin);
+    }
     TRY(host_setup(mesh, part, nu, c->hs));
     HostSetup& hs = c->hs;
     for (int64_t e = 0; e < hs.nelem; ++e)
@@ -885,6 +928,7 @@ de_status_t factor_impl(de_ctx* c) {
         set_error("context was created with host_only = 1");
         return DE_ESTATE;
     }
+    if (c->opt.weighted_trace && c->dens_dirty && c->have_prec) TRY(rebuild_weighted_prec(c));
     cudaEvent_t e0, e1;
     DE_CUDA(cudaEventCreate(&e0));
     DE_CUDA(cudaEventCreate(&e1));
@@ -1140,6 +1184,7 @@ de_status_t de_update_densities(de_ctx_t* c, const double* density) {
     DE_CUDA(cudaSetDevice(c->opt.device));
     DE_CUDA(cudaMemcpyAsync(c->d_rho, density, sizeof(double) * c->hs.nelem, cudaMemcpyHostToDevice, c->st));
     c->factored = false;
+    c->dens_dirty = true;
     return DE_OK;
 }
 
@@ -1152,6 +1197,7 @@ de_status_t de_update_densities_device(de_ctx_t* c, const double* d_density) {
     DE_CUDA(cudaSetDevice(c->opt.device));
     DE_CUDA(cudaMemcpyAsync(c->d_rho, d_density, sizeof(double) * c->hs.nelem, cudaMemcpyDeviceToDevice, c->st));
     c->factored = false;
+    c->dens_dirty = true;
     return DE_OK;
 }
 
@@ -1385,6 +1431,7 @@ void de_destroy(de_ctx_t* c) {
         if (e) cudaEventDestroy(e);
     if (c->comm && nccl().destroy) nccl().destroy(c->comm);
     for (void* p : c->allocs) cudaFree(p);
+    for (void* p : c->prec_allocs) cudaFree(p);
     if (c->own_stream && c->st) cudaStreamDestroy(c->st);
     delete c;
 }

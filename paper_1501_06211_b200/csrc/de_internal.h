@@ -90,6 +90,8 @@ struct HostSetup {
     std::vector<int32_t> face_of;     // flat -> face id within component, -1 cross
     int64_t n_faces_c[MAXC] = {0, 0, 0}, n_cross_c[MAXC] = {0, 0, 0};
     int singular_mask = 0;
+    std::vector<int32_t> flat_of;     // Gamma dof -> flattened skeleton index (-1 otherwise)
+    std::vector<double> trace_E;      // element moduli of the weighted trace norm (R19); empty = unweighted
     HCsr M, L, K;                     // block diagonal over components (flattened)
     HElim elimK, elimM;
     double KE0[24 * 24];              // unit-E element stiffness, local order lexicographic
@@ -99,6 +101,7 @@ struct HostSetup {
 // Build everything density-independent. Returns DE_OK or DE_EINVAL with the error set.
 de_status_t host_setup(const de_mesh_t* mesh, const de_partition_t* part, double nu,
                        HostSetup& hs);
+de_status_t build_trace(HostSetup& hs, const double* Ee);
 
 // Per-subdomain ring structures (A_IG rows over interior, A_GG/A_GI rows over Gamma).
 struct HRing {

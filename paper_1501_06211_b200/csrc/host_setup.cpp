@@ -459,7 +459,8 @@ de_status_t host_setup(const de_mesh_t* mesh, const de_partition_t* part, double
     hs.cnode.clear();
     hs.face_of.clear();
     hs.comp_off[0] = 0;
-    std::vector<int32_t> flat_of(hs.ndof, -1);   // Gamma dof -> flat index
+    hs.flat_of.assign(hs.ndof, -1);   // Gamma dof -> flat index
+    std::vector<int32_t>& flat_of = hs.flat_of;
     for (int c = 0; c < dim; ++c) {
         std::map<std::pair<int32_t, int32_t>, int32_t> fid;
         // first pass: face keys in ascending key order
@@ -488,6 +489,15 @@ de_status_t host_setup(const de_mesh_t* mesh, const de_partition_t* part, double
         hs.comp_off[c + 1] = int64_t(hs.cmap.size());
     }
     for (int c = dim; c < MAXC; ++c) hs.comp_off[c + 1] = hs.comp_off[dim];
+    return build_trace(hs, hs.trace_E.empty() ? nullptr : hs.trace_E.data());
+}
+
+// Trace matrices M, L (and K), singular components, and the exact-elimination structures of K and M.
+// Ee == nullptr: unweighted (R6); else every facet element is scaled by (E_a + E_b)/2 of its two adjacent
+// elements (NEXT(3), R19). Re-run by de_factor when the weighted norm must follow new densities.
+de_status_t build_trace(HostSetup& hs, const double* Ee) {
+    const int dim = hs.dim;
+    const std::vector<int32_t>& flat_of = hs.flat_of;
     const int32_t nflat = int32_t(hs.comp_off[dim]);
 
     // ---- trace facets (R6): element facets whose two elements lie in different subdomains
@@ -529,6 +539,9 @@ de_status_t host_setup(const de_mesh_t* mesh, const de_partition_t* part, double
             int e2[3] = {e[0], e[1], e[2]};
             e2[a]++;
             if (esub(e) == esub(e2)) continue;
+            int64_t stride = 1;
+            for (int t2 = 0; t2 < a; ++t2) stride *= hs.nel[t2];
+            const double wgt = Ee ? 0.5 * (Ee[el] + Ee[el + stride]) : 1.0;
             // facet nodes: offsets with o_a = 1, lexicographic in remaining axes
             int64_t fn[4];
             int t = 0;
@@ -549,8 +562,8 @@ de_status_t host_setup(const de_mesh_t* mesh, const de_partition_t* part, double
                     for (int j = 0; j < nfn; ++j) {
                         const int32_t fj = flat_of[dim * fn[j] + c];
                         if (fj < 0) continue;
-                        tM.push_back({fi, fj, Mf[i][j]});
-                        tL.push_back({fi, fj, Lf[i][j]});
+                        tM.push_back({fi, fj, wgt * Mf[i][j]});
+                        tL.push_back({fi, fj, wgt * Lf[i][j]});
                     }
                 }
         }
@@ -575,6 +588,8 @@ de_status_t host_setup(const de_mesh_t* mesh, const de_partition_t* part, double
     }
     hs.M = csr_from_trips(nflat, tM);
     hs.L = csr_from_trips(nflat, tL);
+    hs.elimK = HElim();
+    hs.elimM = HElim();
     if (hs.M.ptr != hs.L.ptr || hs.M.col != hs.L.col) {   // the preconditioner fuses M and L SpMVs
         set_error("internal: trace M and L sparsity patterns differ");
         return DE_EINVAL;
