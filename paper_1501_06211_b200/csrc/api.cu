@@ -772,7 +772,7 @@ de_status_t setup_impl(const de_mesh_t* mesh, const double* density, double E0, 
         d.igp_off = ring.igp_off[k];
         d.gxp_off = ring.gxp_off[k];
         d.sexp_off = c->n_sexp;
-        c->n_sexp += int64_t(hs.nGs[s]) * hs.nGs[s];
+        c->n_sexp += sexp_packed_doubles(hs.nGs[s]);
         c->hsd.push_back(d);
         idofs.insert(idofs.end(), hs.idofs.begin() + hs.ioff[s], hs.idofs.begin() + hs.ioff[s + 1]);
         for (int l = 0; l < d.nG; ++l) Rg.push_back(hs.gpos[hs.gdofs[hs.goff[s] + l]]);
@@ -839,6 +839,8 @@ de_status_t setup_impl(const de_mesh_t* mesh, const double* density, double E0, 
         c->explicit_schur = fits && (opt.schur_mode == 2 || (opt.schur_mode == 0 && double(c->n_sexp) < fac_one_pass));
         if (c->explicit_schur) {
             TRY(dalloc(c, &c->d_sexp, size_t(c->n_sexp)));
+            DE_CUDA(cudaMemsetAsync(c->d_sexp, 0, size_t(c->n_sexp) * sizeof(double), c->st));   // tile padding
+            prepare_schur_explicit(c->max_nG);
             // scratch per subdomain: the thread-per-column formation keeps n_I x FORM_THREADS solutions, the
             // warp-per-8-columns one (n_Gamma,s + 8) x n_I; one launch per batch, a multiple of the SM count
             const size_t per = size_t(std::max(std::max(1, c->max_nG) + 8, FORM_THREADS)) * size_t(std::max(1, c->max_nI));

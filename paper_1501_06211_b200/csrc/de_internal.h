@@ -190,6 +190,17 @@ constexpr int PCR_Q = 2 * PCR_L + 1;
 constexpr int XCF_W = 4;
 constexpr int TRI_N = 32;
 constexpr int FORM_THREADS = 256;   // columns per pass of the thread-per-column S_s formation
+// Explicit S_s storage: the lower triangle of 16 x 16 tiles, tile (I, J) (I >= J) at (I(I+1)/2 + J) * 256,
+// row-major inside the tile, zero padding past n_Gamma,s; diagonal tiles are stored whole.
+constexpr int STS = 16;
+inline int64_t sexp_packed_doubles(int nG) {
+    const int64_t nt = (nG + STS - 1) / STS;
+    return nt * (nt + 1) / 2 * STS * STS;
+}
+__host__ __device__ inline int64_t sexp_packed_index(int r, int c) {   // requires r / STS >= c / STS
+    const int64_t I = r / STS, J = c / STS;
+    return (I * (I + 1) / 2 + J) * (STS * STS) + (r % STS) * STS + (c % STS);
+}
 
 struct CsrDev {
     int32_t n;
@@ -254,6 +265,7 @@ int launch_schur_local(const SchurArgs& a, cudaStream_t st);
 // q_s = S_s x_s with the explicit column-major S_s (one CTA per subdomain, coalesced over rows)
 void launch_schur_explicit(const SubDesc* sd, int nsl, const double* sexp, const int32_t* Rg, const double* xin,
                            double* qloc, int maxG, const PcgState* s, cudaStream_t st);
+void prepare_schur_explicit(int maxG);
 
 void launch_gather(const int32_t* gptr, const int32_t* gsrc, const double* qloc,
                    const double* add, double* q, int64_t nG, const PcgState* st_done,

@@ -204,42 +204,90 @@ __global__ void __launch_bounds__(32) k_schur_local(SchurArgs a, int nstage) {
                 q -= a.gx_val[e] * w[-cidx - 1];
             }
         }
-        if (cols) a.sexp[d.sexp_off + size_t(tcol) * nG + l] = q;   // column tcol of S_sl
+        if (cols && l / STS >= tcol / STS) a.sexp[d.sexp_off + sexp_packed_index(l, tcol)] = q;   // S_s[l][tcol]
         else a.qloc[d.goff + l] = q;
     }
 }
 
 // q_s = S_s x_s, S_s column-major (= row-major by symmetry): thread t accumulates row t over columns k,
 // so each step is one coalesced read of column k. One CTA per subdomain.
-__global__ void __launch_bounds__(256) k_schur_explicit(const SubDesc* __restrict__ sd, const double* __restrict__ sexp,
-                                                        const int32_t* __restrict__ Rg, const double* __restrict__ xin,
-                                                        double* __restrict__ qloc, const PcgState* s) {
+// q_s = S_s x_s from the packed lower tiles (STS x STS, see de_internal.h): every tile is read once and used twice
+// (T x_J for its row block, T^T x_I for its column block), so only half the dense bytes stream from HBM.
+// Warp w owns tile rows dealt in zig-zag order (0, nt-1, 1, nt-2, ...) for balance; lane l holds rows h + 2k
+// (h = l / 16, k < 8) and column l % 16 of a tile. Per-warp partial vectors are summed in a fixed order.
+constexpr int SE_T = 256, SE_W = SE_T / 32;
+__global__ void __launch_bounds__(SE_T) k_schur_explicit(const SubDesc* __restrict__ sd, const double* __restrict__ sexp,
+                                                         const int32_t* __restrict__ Rg, const double* __restrict__ xin,
+                                                         double* __restrict__ qloc, const PcgState* s) {
     if (s != nullptr && s->done) return;
-    __shared__ double xs[1024];
+    extern __shared__ double se_sm[];
     const SubDesc d = sd[blockIdx.x];
-    const int nG = d.nG, t = threadIdx.x;
-    for (int l = t; l < nG; l += blockDim.x) xs[l] = xin[Rg[d.goff + l]];
+    const int nG = d.nG, nt = (nG + STS - 1) / STS, np = nt * STS, tid = threadIdx.x;
+    const int lane = tid & 31, w = tid >> 5, h = lane >> 4, j = lane & 15;
+    double* xs = se_sm;            // [np], zero past nG
+    double* yw = se_sm + np;       // [SE_W][np]
+    for (int l = tid; l < np; l += SE_T) xs[l] = l < nG ? xin[Rg[d.goff + l]] : 0.0;
+    for (int l = tid; l < SE_W * np; l += SE_T) yw[l] = 0.0;
     __syncthreads();
     const double* S = sexp + d.sexp_off;
-    for (int row = t; row < nG; row += blockDim.x) {
-        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-        int k = 0;
-        for (; k + 3 < nG; k += 4) {
-            a0 += __ldcs(S + size_t(k) * nG + row) * xs[k];
-            a1 += __ldcs(S + size_t(k + 1) * nG + row) * xs[k + 1];
-            a2 += __ldcs(S + size_t(k + 2) * nG + row) * xs[k + 2];
-            a3 += __ldcs(S + size_t(k + 3) * nG + row) * xs[k + 3];
+    double* y = yw + w * np;
+    for (int m = w; m < nt; m += SE_W) {
+        const int I = (m & 1) ? nt - 1 - m / 2 : m / 2;
+        const double* Trow = S + int64_t(I) * (I + 1) / 2 * (STS * STS);
+        double xi[STS / 2], acc[STS / 2];
+#pragma unroll
+        for (int k = 0; k < STS / 2; ++k) {
+            xi[k] = xs[I * STS + h + 2 * k];
+            acc[k] = 0.0;
         }
-        for (; k < nG; ++k) a0 += __ldcs(S + size_t(k) * nG + row) * xs[k];
-        qloc[d.goff + row] = (a0 + a1) + (a2 + a3);
+        for (int J = 0; J <= I; ++J) {
+            const double* T = Trow + J * (STS * STS);
+            double tv[STS / 2];
+#pragma unroll
+            for (int k = 0; k < STS / 2; ++k) tv[k] = __ldcs(T + (h + 2 * k) * STS + j);
+            const double xj = xs[J * STS + j];
+            double tt = 0.0;
+#pragma unroll
+            for (int k = 0; k < STS / 2; ++k) {
+                acc[k] = fma(tv[k], xj, acc[k]);
+                tt = fma(tv[k], xi[k], tt);
+            }
+            if (J < I) {   // T^T x_I -> rows of block J
+                tt += __shfl_xor_sync(0xffffffffu, tt, 16);
+                if (h == 0) y[J * STS + j] += tt;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < STS / 2; ++k)
+#pragma unroll
+            for (int o = 8; o > 0; o >>= 1) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], o);
+        if (j == 0)
+#pragma unroll
+            for (int k = 0; k < STS / 2; ++k) y[I * STS + h + 2 * k] += acc[k];
+        __syncwarp();
+    }
+    __syncthreads();
+    for (int l = tid; l < nG; l += SE_T) {
+        double q = 0.0;
+#pragma unroll
+        for (int ww = 0; ww < SE_W; ++ww) q += yw[ww * np + l];
+        qloc[d.goff + l] = q;
     }
 }
 
 void launch_schur_explicit(const SubDesc* sd, int nsl, const double* sexp, const int32_t* Rg, const double* xin,
                            double* qloc, int maxG, const PcgState* s, cudaStream_t st) {
     if (nsl == 0) return;
-    const int threads = std::min(256, std::max(32, (maxG + 31) / 32 * 32));
-    k_schur_explicit<<<nsl, threads, 0, st>>>(sd, sexp, Rg, xin, qloc, s);
+    const int np = (maxG + STS - 1) / STS * STS;
+    const size_t smem = size_t(1 + SE_W) * np * sizeof(double);
+    k_schur_explicit<<<nsl, SE_T, smem, st>>>(sd, sexp, Rg, xin, qloc, s);
+}
+
+// once per context, outside any graph capture
+void prepare_schur_explicit(int maxG) {
+    const int np = (maxG + STS - 1) / STS * STS;
+    cudaFuncSetAttribute(k_schur_explicit, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(size_t(1 + SE_W) * np * sizeof(double)));
 }
 
 // ------------------------------------------------------------------ explicit S_s formation, R columns per warp
@@ -372,8 +420,8 @@ __global__ void __launch_bounds__(32) k_schur_cols(SchurArgs a, int nstage) {
             }
         }
 #pragma unroll
-        for (int k = 0; k < R; ++k)
-            if (t0 + k < nG) a.sexp[d.sexp_off + size_t(t0 + k) * nG + l] = q[k];
+        for (int k = 0; k < R; ++k)   // S_s[l][t0+k] into the packed lower tiles
+            if (t0 + k < nG && l / STS >= (t0 + k) / STS) a.sexp[d.sexp_off + sexp_packed_index(l, t0 + k)] = q[k];
     }
 }
 
@@ -505,7 +553,7 @@ __global__ void __launch_bounds__(SF_T, 1) k_schur_form(SchurArgs a) {
                     if (cidx >= 0) q += (cidx == t) ? val : 0.0;
                     else q -= val * ys[size_t(-cidx - 1) * SF_T + tid];
                 }
-                a.sexp[d.sexp_off + size_t(l) * nG + t] = q;
+                if (l / STS >= t / STS) a.sexp[d.sexp_off + sexp_packed_index(l, t)] = q;   // S_s[l][t]
             }
         __syncthreads();
     }
