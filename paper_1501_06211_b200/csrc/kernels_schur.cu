@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(32) k_schur_local(SchurArgs a, int nstage) {
 // (T x_J for its row block, T^T x_I for its column block), so only half the dense bytes stream from HBM.
 // Warp w owns tile rows dealt in zig-zag order (0, nt-1, 1, nt-2, ...) for balance; lane l holds rows h + 2k
 // (h = l / 16, k < 8) and column l % 16 of a tile. Per-warp partial vectors are summed in a fixed order.
-constexpr int SE_T = 256, SE_W = SE_T / 32;
+constexpr int SE_T = 256, SE_W = SE_T / 32, SE_U = 4;
 __global__ void __launch_bounds__(SE_T) k_schur_explicit(const SubDesc* __restrict__ sd, const double* __restrict__ sexp,
                                                          const int32_t* __restrict__ Rg, const double* __restrict__ xin,
                                                          double* __restrict__ qloc, const PcgState* s) {
@@ -240,21 +240,29 @@ __global__ void __launch_bounds__(SE_T) k_schur_explicit(const SubDesc* __restri
             xi[k] = xs[I * STS + h + 2 * k];
             acc[k] = 0.0;
         }
-        for (int J = 0; J <= I; ++J) {
-            const double* T = Trow + J * (STS * STS);
-            double tv[STS / 2];
+        for (int J0 = 0; J0 <= I; J0 += SE_U) {   // SE_U tiles per step: 8 SE_U loads per lane in flight
+            double tv[SE_U][STS / 2];
 #pragma unroll
-            for (int k = 0; k < STS / 2; ++k) tv[k] = __ldcs(T + (h + 2 * k) * STS + j);
-            const double xj = xs[J * STS + j];
-            double tt = 0.0;
+            for (int u = 0; u < SE_U; ++u) {
+                const double* T = Trow + (J0 + u) * (STS * STS);
 #pragma unroll
-            for (int k = 0; k < STS / 2; ++k) {
-                acc[k] = fma(tv[k], xj, acc[k]);
-                tt = fma(tv[k], xi[k], tt);
+                for (int k = 0; k < STS / 2; ++k) tv[u][k] = J0 + u <= I ? __ldcs(T + (h + 2 * k) * STS + j) : 0.0;
             }
-            if (J < I) {   // T^T x_I -> rows of block J
-                tt += __shfl_xor_sync(0xffffffffu, tt, 16);
-                if (h == 0) y[J * STS + j] += tt;
+#pragma unroll
+            for (int u = 0; u < SE_U; ++u) {
+                const int J = J0 + u;
+                if (J > I) break;
+                const double xj = xs[J * STS + j];
+                double tt = 0.0;
+#pragma unroll
+                for (int k = 0; k < STS / 2; ++k) {
+                    acc[k] = fma(tv[u][k], xj, acc[k]);
+                    tt = fma(tv[u][k], xi[k], tt);
+                }
+                if (J < I) {   // T^T x_I -> rows of block J
+                    tt += __shfl_xor_sync(0xffffffffu, tt, 16);
+                    if (h == 0) y[J * STS + j] += tt;
+                }
             }
         }
 #pragma unroll
