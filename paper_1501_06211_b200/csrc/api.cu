@@ -1262,9 +1262,13 @@ de_status_t de_get_skeleton(const de_ctx_t* c, int32_t comp, int32_t* nodes, int
         return DE_EINVAL;
     }
     const HostSetup& hs = c->hs;
-    for (int64_t f = hs.comp_off[comp]; f < hs.comp_off[comp + 1]; ++f) {
-        if (nodes) nodes[f - hs.comp_off[comp]] = hs.cnode[f];
-        if (face_of_node) face_of_node[f - hs.comp_off[comp]] = hs.face_of[f];
+    // ascending node order (the internal flattened order is face-major)
+    std::vector<std::pair<int32_t, int32_t>> nf;
+    for (int64_t f = hs.comp_off[comp]; f < hs.comp_off[comp + 1]; ++f) nf.push_back({hs.cnode[f], hs.face_of[f]});
+    std::sort(nf.begin(), nf.end());
+    for (size_t q = 0; q < nf.size(); ++q) {
+        if (nodes) nodes[q] = nf[q].first;
+        if (face_of_node) face_of_node[q] = nf[q].second;
     }
     return DE_OK;
 }

@@ -487,6 +487,26 @@ de_status_t host_setup(const de_mesh_t* mesh, const de_partition_t* part, double
             }
         }
         hs.comp_off[c + 1] = int64_t(hs.cmap.size());
+        {   // face-major flattened order inside the component: faces by id (nodes ascending, i.e. along the
+            // face), then the cross points; the nodes of a face are then contiguous (coalesced face-mapped work)
+            const int64_t lo = hs.comp_off[c], n = hs.comp_off[c + 1] - lo;
+            std::vector<int64_t> ord(n);
+            std::iota(ord.begin(), ord.end(), 0);
+            auto key = [&](int64_t q) { return hs.face_of[lo + q] < 0 ? INT32_MAX : hs.face_of[lo + q]; };
+            std::stable_sort(ord.begin(), ord.end(), [&](int64_t a, int64_t b) { return key(a) < key(b); });
+            std::vector<int32_t> cm(n), cn(n), fo(n);
+            for (int64_t q = 0; q < n; ++q) {
+                cm[q] = hs.cmap[lo + ord[q]];
+                cn[q] = hs.cnode[lo + ord[q]];
+                fo[q] = hs.face_of[lo + ord[q]];
+            }
+            for (int64_t q = 0; q < n; ++q) {
+                hs.cmap[lo + q] = cm[q];
+                hs.cnode[lo + q] = cn[q];
+                hs.face_of[lo + q] = fo[q];
+                flat_of[int64_t(dim) * cn[q] + c] = int32_t(lo + q);
+            }
+        }
     }
     for (int c = dim; c < MAXC; ++c) hs.comp_off[c + 1] = hs.comp_off[dim];
     return build_trace(hs, hs.trace_E.empty() ? nullptr : hs.trace_E.data());
