@@ -630,6 +630,7 @@ de_status_t upload_prec_impl(de_ctx* c) {
     if (c->opt.prec_kernels == 0 && prec_coop_prepare(P, c->opt.device, c->coop)) {
         TRY(dalloc(c, &c->coop.red, prec_coop_red_doubles(c->coop)));
         TRY(dalloc(c, &c->coop.gram, prec_coop_gram_doubles(c->coop)));
+        TRY(dalloc(c, &c->coop.gram_tot, size_t(MAXC) * KMAX * (2 * KMAX + 1)));
         TRY(dalloc(c, &c->coop.w1, nf));
         TRY(dalloc(c, &c->coop.mw1, nf));
         TRY(dalloc(c, &c->coop.lw1, nf));

@@ -320,7 +320,7 @@ struct CoopBuffers {
     int nb = 0;
     size_t smem = 0;
     int stage = 0, per_warp = 0, mf = 0, ncmax = 0, nbc_max = 0, tridiag = 0;
-    double *red = nullptr, *gram = nullptr, *w1 = nullptr, *mw1 = nullptr, *lw1 = nullptr;
+    double *red = nullptr, *gram = nullptr, *gram_tot = nullptr, *w1 = nullptr, *mw1 = nullptr, *lw1 = nullptr;
     unsigned long long* timers = nullptr;   // phase stamps (diagnostics; env DE_PREC_TIMERS=1)
     const void* kfn = nullptr;              // k_prec_coop instantiation (basis bound, timers)
 };

@@ -34,6 +34,7 @@ struct CoopArgs {
     const PcgState* s;
     double* red;        // [2][MAXC][NRED][nbc_max]
     double* gram;       // [MAXC][KMAX rows][GW][nbc_max] per-block Gram partials
+    double* gram_tot;   // [MAXC][KMAX rows][GW] their fixed-order sums
     double* w1;         // second Lanczos work vector (nflat)
     double* mw1;        // M w1 (nflat)
     double* lw1;        // L w1 (nflat)
@@ -151,6 +152,38 @@ __device__ void gram_partials(const CoopArgs& a, const double* gacc, int c, int 
         if (lane == 0) a.gram[((size_t(c) * KMAX + j) * GW + v) * a.nbc_max + lb] = t;
     }
     __syncthreads();
+}
+
+// Fixed-order sums of Gram row jr (every accepted component), one entry per warp: entry tasks
+// tau = first, first + stride, ...; lanes add the block partials b = lane, lane+32, .. in order, then a warp tree.
+__device__ void gram_row_sums(const CoopArgs& a, int jr, const int* kcs, int first, int stride, int nb) {
+    constexpr int TU = 6;   // entries per warp in flight
+    const int lane = threadIdx.x & 31, nc = a.P.ncomp, per = 2 * (jr + 1) + 1;
+    for (int tau0 = first; tau0 < nc * per; tau0 += stride * TU) {
+        const double* pg[TU];
+        size_t dst[TU];
+        int nbcc[TU];
+#pragma unroll
+        for (int u = 0; u < TU; ++u) {
+            const int tau = tau0 + u * stride, cc = min(tau / per, nc - 1), q = tau - cc * per;
+            const int v = q <= jr ? q : (q < 2 * (jr + 1) ? KMAX + (q - jr - 1) : 2 * KMAX);
+            const bool ok = tau < nc * per && jr < kcs[cc];
+            nbcc[u] = ok ? (nb - cc + nc - 1) / nc : 0;
+            pg[u] = a.gram + ((size_t(cc) * KMAX + jr) * GW + v) * a.nbc_max;
+            dst[u] = ok ? (size_t(cc) * KMAX + jr) * GW + v : ~size_t(0);
+        }
+        double acc[TU];
+#pragma unroll
+        for (int u = 0; u < TU; ++u) acc[u] = 0.0;
+        for (int b = lane; b < a.nbc_max; b += 32)
+#pragma unroll
+            for (int u = 0; u < TU; ++u) acc[u] += b < nbcc[u] ? pg[u][b] : 0.0;
+#pragma unroll
+        for (int u = 0; u < TU; ++u) {
+            const double t = warp_sum(acc[u]);
+            if (lane == 0 && dst[u] != ~size_t(0)) a.gram_tot[dst[u]] = t;
+        }
+    }
 }
 
 __device__ __forceinline__ double spmv_row(const CsrDev& A, int64_t i, const double* __restrict__ x) {
@@ -882,6 +915,9 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
         sclh[tid][0] = scl[tid];
     }
     __syncthreads();
+    // Gram row 0 is complete: warp 0 of the first blocks sums it while the next phase runs (warp 0 does no
+    // face or row work there); the last row is left to block 0 before the Ritz step
+    if (P.kmax > 1 && tid < 32) gram_row_sums(a, 0, kcs, blockIdx.x, nb, nb);
     // ---- inverse Lanczos steps
     const bool fuseK = P.eK.tri && P.eK.fuse;
     for (int j = 1; j < P.kmax; ++j) {
@@ -1033,21 +1069,21 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
             }
         }
         __syncthreads();
+        if (j + 1 < P.kmax && tid < 32) gram_row_sums(a, j, kcs, blockIdx.x, nb, nb);
     }
     // The combine below reads only own rows (written by this thread), so no barrier is needed before the
     // Ritz step: every Gram row was reduced to per-block partials at its step's last barrier.
     // block 0: fixed-order reduction of the Gram partials (one thread per entry, scaled by the
     // normalisation of its row), then one warp per component solves the k x k Ritz problem
     if (blockIdx.x == 0) {
+        gram_row_sums(a, P.kmax - 1, kcs, tid >> 5, CW, nb);   // rows < kmax-1 were summed in the loop
+        __syncthreads();
         for (int e = tid; e < nc * KMAX * GW; e += CT) {
             const int cc = e / (KMAX * GW), rem = e - cc * (KMAX * GW), jr = rem / GW, v = rem - jr * GW;
             if (jr >= kcs[cc]) continue;
             const int kind = v < KMAX ? 0 : (v < 2 * KMAX ? 1 : 2), t = kind == 0 ? v : v - KMAX;
             if (kind < 2 && t > jr) continue;
-            const int nbcc = (nb - cc + nc - 1) / nc;
-            const double* pg = a.gram + ((size_t(cc) * KMAX + jr) * GW + v) * a.nbc_max;
-            double acc = 0.0;
-            for (int b = 0; b < nbcc; ++b) acc += pg[b];
+            const double acc = *((volatile const double*)(a.gram_tot + (size_t(cc) * KMAX + jr) * GW + v));
             const double sj = sclh[cc][jr];
             LzState& zs = P.lz[cc];
             if (kind == 2) {
@@ -1177,6 +1213,7 @@ int prec_apply_coop(const PrecDev& P, const CoopBuffers& B, const double* r, dou
     a.s = s;
     a.red = B.red;
     a.gram = B.gram;
+    a.gram_tot = B.gram_tot;
     a.w1 = B.w1;
     a.mw1 = B.mw1;
     a.lw1 = B.lw1;

@@ -35,7 +35,7 @@ print(" ".join(f"{x:.1f}" for x in d))
 f0 = np.array(list(t)[200:200 + 4096], dtype=np.float64); f1 = np.array(list(t)[200 + 4096:200 + 8192], dtype=np.float64)
 f0 = f0[f0 > 0]; f1 = f1[f1 > 0]
 print("face mode0 warp cycles: n", len(f0), "mean", f0.mean(), "max", f0.max(), "p50", np.median(f0))
-print("face mode1 warp cycles: n", len(f1), "mean", f1.mean(), "max", f1.max(), "p50", np.median(f1))
+if len(f1): print("face mode1 warp cycles: n", len(f1), "mean", f1.mean(), "max", f1.max(), "p50", np.median(f1))
 f1all = np.array(list(t)[200 + 4096:200 + 4096 + 2368], dtype=np.float64)
 slow = np.argsort(-f1all)[:12]
 print("slowest mode1 warps (gw, cycles, block, warp):", [(int(g), int(f1all[g]), int(g) // 8, int(g) % 8) for g in slow])
