@@ -224,7 +224,7 @@ de_status_t precond(de_ctx* c, const double* r, double* z, const PcgState* s, in
             set_error("cooperative preconditioner launch failed: %s", cudaGetErrorString(cudaGetLastError()));
             return DE_ECUDA;
         }
-        if (nl) *nl = 1;
+        if (nl) *nl = 3;   // k_prec_coop, k_prec_ritz, k_prec_combine
     } else if (c->have_prec) {
         prec_apply(c->P, r, z, s, c->st, nl);
     } else {

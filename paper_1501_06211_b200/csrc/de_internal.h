@@ -216,6 +216,7 @@ struct LzState {                    // per component inverse-Lanczos bookkeeping
     double wr[KMAX];
     double coef[KMAX];
     double theta_ritz[KMAX];
+    double sc[KMAX];                 // scale of each stored (unnormalised) basis vector (cooperative path)
 };
 
 // kernel launchers (implemented in *.cu); all asynchronous on `st`
@@ -317,7 +318,7 @@ void prec_prepare(const PrecDev& P);   // one-time kernel attributes (outside gr
 
 // persistent cooperative preconditioner (kernels_prec_coop.cu)
 struct CoopBuffers {
-    int nb = 0;
+    int nb = 0, nsm = 148;
     size_t smem = 0;
     int stage = 0, per_warp = 0, mf = 0, ncmax = 0, nbc_max = 0, tridiag = 0;
     double *red = nullptr, *gram = nullptr, *gram_tot = nullptr, *w1 = nullptr, *mw1 = nullptr, *lw1 = nullptr;

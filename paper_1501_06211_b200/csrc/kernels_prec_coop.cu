@@ -1071,10 +1071,8 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
         __syncthreads();
         if (j + 1 < P.kmax && tid < 32) gram_row_sums(a, j, kcs, blockIdx.x, nb, nb);
     }
-    // The combine below reads only own rows (written by this thread), so no barrier is needed before the
-    // Ritz step: every Gram row was reduced to per-block partials at its step's last barrier.
-    // block 0: fixed-order reduction of the Gram partials (one thread per entry, scaled by the
-    // normalisation of its row), then one warp per component solves the k x k Ritz problem
+    // block 0: the last Gram row's fixed-order sums, then the Gram matrices (scaled by the normalisation of
+    // each row) into the components' LzState for k_prec_ritz
     if (blockIdx.x == 0) {
         gram_row_sums(a, P.kmax - 1, kcs, tid >> 5, CW, nb);   // rows < kmax-1 were summed in the loop
         __syncthreads();
@@ -1097,54 +1095,75 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
         }
         __syncthreads();
         STAMP(stamp++);
-        const int w = tid >> 5, lane = tid & 31;
-        double* ws = dsm + size_t(w) * (4 * KMAX * (KMAX + 1) + 2 * KMAX + 4 * KMAX);
-        if (w < nc) {
-            LzState& zs = P.lz[w];
-            const int k = kcs[w];
-            if (lane < KMAX) zs.coef[lane] = 0.0;
-            zs.kc = k;
-            zs.active = act[w];
-            __syncwarp();
-            if (act[w]) {
-                double* R = ws;
-                double* Cm = R + KMAX * (KMAX + 1);
-                double* V = Cm + KMAX * (KMAX + 1);
-                double* X = V + KMAX * (KMAX + 1);
-                double* rot = X + KMAX * (KMAX + 1);
-                int* rpq = reinterpret_cast<int*>(rot + KMAX);
-                if (TIM && a.timers && w == 0 && lane == 0) a.timers[100] = gtimer();
-                const bool ok = ritz_warp(zs.A, zs.B, zs.wr, k, P.singular[w] != 0, P.theta, zs.coef, R, Cm, V, X,
-                                          rot, rpq, (TIM && a.timers && w == 0) ? a.timers + 102 : nullptr);
-                if (TIM && a.timers && w == 0 && lane == 0) a.timers[101] = gtimer();
-                if (!ok && lane == 0) {
-                    zs.status = DE_EBREAKDOWN;
-                    for (int e = 0; e < KMAX; ++e) zs.coef[e] = 0.0;
-                    if (a.s) {
-                        PcgState* sm = const_cast<PcgState*>(a.s);
-                        sm->status = DE_EBREAKDOWN;
-                        sm->done = 1;
-                    }
-                }
+        if (tid < nc * KMAX) {   // per component: basis size, activity and the scales for the combine
+            const int cc = tid / KMAX, t = tid - cc * KMAX;
+            LzState& zs = P.lz[cc];
+            zs.sc[t] = t < kcs[cc] ? sclh[cc][t] : 0.0;
+            if (t == 0) {
+                zs.kc = kcs[cc];
+                zs.active = act[cc];
             }
         }
     }
-    grid.sync();
-    __syncwarp();   // lane 0 spun in the barrier: reconverge before warp-synchronous code
-    STAMP(stamp++);
-    // z = sum_t coef_t W_t = sum_t (coef_t sclh_t) Wraw_t, scattered back to interface order
-    {
-        const int k = kcs[c];
-        if (tid < KMAX) hsm[c][tid] = tid < k ? P.lz[c].coef[tid] * sclh[c][tid] : 0.0;
-        __syncthreads();
-        for (int64_t i = r0; i < hi; i += rs) {
-            double acc = 0.0;
-            if (act[c])
-                for (int t = 0; t < k; ++t) acc += hsm[c][t] * P.W[size_t(t) * nf + i];
-            a.z[P.cmap[i]] = acc;
+    // the k x k Ritz problems (k_prec_ritz) and the combine (k_prec_combine) follow as two small launches: the
+    // Ritz code runs there without this kernel's register cap, and one grid barrier is saved
+}
+
+#undef ZERO_VALS
+
+// One warp per component: the k x k Ritz problem of the Gram matrices left by k_prec_coop -> coefficients
+// (no register cap: the Jacobi and the triangular solves stay in registers).
+template <bool TIM>
+__global__ void __launch_bounds__(32 * MAXC) k_prec_ritz(PrecDev P, const PcgState* s, unsigned long long* timers) {
+    if (s != nullptr && s->done) return;
+    extern __shared__ double rsm[];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (w >= P.ncomp) return;
+    constexpr int WSZ = 4 * KMAX * (KMAX + 1) + 2 * KMAX + 4 * KMAX;
+    LzState& zs = P.lz[w];
+    if (lane < KMAX) zs.coef[lane] = 0.0;
+    __syncwarp();
+    if (!zs.active) return;
+    double* R = rsm + size_t(w) * WSZ;
+    double* Cm = R + KMAX * (KMAX + 1);
+    double* V = Cm + KMAX * (KMAX + 1);
+    double* X = V + KMAX * (KMAX + 1);
+    double* rot = X + KMAX * (KMAX + 1);
+    int* rpq = reinterpret_cast<int*>(rot + KMAX);
+    if (TIM && timers && w == 0 && lane == 0) timers[100] = gtimer();
+    const bool ok = ritz_warp(zs.A, zs.B, zs.wr, zs.kc, P.singular[w] != 0, P.theta, zs.coef, R, Cm, V, X, rot, rpq,
+                              (TIM && timers && w == 0) ? timers + 102 : nullptr);
+    if (TIM && timers && w == 0 && lane == 0) timers[101] = gtimer();
+    if (!ok && lane == 0) {
+        zs.status = DE_EBREAKDOWN;
+        for (int e = 0; e < KMAX; ++e) zs.coef[e] = 0.0;
+        if (s) {
+            PcgState* sm = const_cast<PcgState*>(s);
+            sm->status = DE_EBREAKDOWN;
+            sm->done = 1;
         }
     }
-#undef ZERO_VALS
+}
+
+// z = sum_t coef_t W_t = sum_t (coef_t sc_t) Wraw_t, scattered back to interface order
+__global__ void __launch_bounds__(256) k_prec_combine(PrecDev P, double* __restrict__ z, const PcgState* s) {
+    if (s != nullptr && s->done) return;
+    __shared__ double cs[MAXC][KMAX];
+    __shared__ int kc[MAXC];
+    if (threadIdx.x < P.ncomp * KMAX) {
+        const int c = threadIdx.x / KMAX, t = threadIdx.x - c * KMAX;
+        const LzState& zs = P.lz[c];
+        cs[c][t] = zs.active ? zs.coef[t] * zs.sc[t] : 0.0;
+        if (t == 0) kc[c] = zs.active ? zs.kc : 0;
+    }
+    __syncthreads();
+    const size_t nf = size_t(P.nflat);
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < P.nflat; i += int64_t(gridDim.x) * blockDim.x) {
+        const int c = ccomp(P.comp_off, P.ncomp, i);
+        double acc = 0.0;
+        for (int t = 0; t < kc[c]; ++t) acc += cs[c][t] * P.W[size_t(t) * nf + i];
+        z[P.cmap[i]] = acc;
+    }
 }
 
 // ------------------------------------------------------------------ host side
@@ -1190,6 +1209,7 @@ bool prec_coop_prepare(const PrecDev& P, int device, CoopBuffers& B) {
     if (getenv("DE_VERBOSE"))
         fprintf(stderr, "[de] k_prec_coop: %d blocks (%d resident/SM possible), %zu B smem\n", nb, per_sm, smem);
     B.nb = nb;
+    B.nsm = nsm;
     B.kfn = reinterpret_cast<const void*>(kfn);
     B.smem = smem;
     B.stage = stage ? 1 : 0;
@@ -1234,8 +1254,14 @@ int prec_apply_coop(const PrecDev& P, const CoopBuffers& B, const double* r, dou
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    const cudaError_t e = cudaLaunchKernelEx(&cfg, reinterpret_cast<void (*)(CoopArgs)>(const_cast<void*>(B.kfn)), a);
-    return e == cudaSuccess ? 1 : -1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, reinterpret_cast<void (*)(CoopArgs)>(const_cast<void*>(B.kfn)), a);
+    if (e != cudaSuccess) return -1;
+    const size_t rsm = size_t(MAXC) * (4 * KMAX * (KMAX + 1) + 6 * KMAX) * sizeof(double);
+    if (B.timers) k_prec_ritz<true><<<1, 32 * MAXC, rsm, st>>>(P, s, B.timers);
+    else k_prec_ritz<false><<<1, 32 * MAXC, rsm, st>>>(P, s, nullptr);
+    k_prec_combine<<<B.nsm * 4, 256, 0, st>>>(P, z, s);
+    e = cudaGetLastError();
+    return e == cudaSuccess ? 3 : -1;
 }
 
 }  // namespace de
