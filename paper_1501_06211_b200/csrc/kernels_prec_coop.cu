@@ -1114,17 +1114,16 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
 // One warp per component: the k x k Ritz problem of the Gram matrices left by k_prec_coop -> coefficients
 // (no register cap: the Jacobi and the triangular solves stay in registers).
 template <bool TIM>
-__global__ void __launch_bounds__(32 * MAXC) k_prec_ritz(PrecDev P, const PcgState* s, unsigned long long* timers) {
+__global__ void __launch_bounds__(32) k_prec_ritz(PrecDev P, const PcgState* s, unsigned long long* timers) {
     if (s != nullptr && s->done) return;
     extern __shared__ double rsm[];
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int w = blockIdx.x, lane = threadIdx.x & 31;   // one single-warp CTA per component
     if (w >= P.ncomp) return;
-    constexpr int WSZ = 4 * KMAX * (KMAX + 1) + 2 * KMAX + 4 * KMAX;
     LzState& zs = P.lz[w];
     if (lane < KMAX) zs.coef[lane] = 0.0;
     __syncwarp();
     if (!zs.active) return;
-    double* R = rsm + size_t(w) * WSZ;
+    double* R = rsm;
     double* Cm = R + KMAX * (KMAX + 1);
     double* V = Cm + KMAX * (KMAX + 1);
     double* X = V + KMAX * (KMAX + 1);
@@ -1256,9 +1255,9 @@ int prec_apply_coop(const PrecDev& P, const CoopBuffers& B, const double* r, dou
     cfg.numAttrs = 1;
     cudaError_t e = cudaLaunchKernelEx(&cfg, reinterpret_cast<void (*)(CoopArgs)>(const_cast<void*>(B.kfn)), a);
     if (e != cudaSuccess) return -1;
-    const size_t rsm = size_t(MAXC) * (4 * KMAX * (KMAX + 1) + 6 * KMAX) * sizeof(double);
-    if (B.timers) k_prec_ritz<true><<<1, 32 * MAXC, rsm, st>>>(P, s, B.timers);
-    else k_prec_ritz<false><<<1, 32 * MAXC, rsm, st>>>(P, s, nullptr);
+    const size_t rsm = size_t(4 * KMAX * (KMAX + 1) + 6 * KMAX) * sizeof(double);
+    if (B.timers) k_prec_ritz<true><<<P.ncomp, 32, rsm, st>>>(P, s, B.timers);
+    else k_prec_ritz<false><<<P.ncomp, 32, rsm, st>>>(P, s, nullptr);
     k_prec_combine<<<B.nsm * 4, 256, 0, st>>>(P, z, s);
     e = cudaGetLastError();
     return e == cudaSuccess ? 3 : -1;
