@@ -242,13 +242,18 @@ de_status_t pcg_iteration(de_ctx* c, int* nl, cudaEvent_t e0, cudaEvent_t e1, cu
     if (e0) cudaEventRecordWithFlags(e0, c->st, cudaEventRecordExternal);   // a real node when captured
     launch_apply(c, c->d_p, c->d_state);
     if (e1) cudaEventRecordWithFlags(e1, c->st, cudaEventRecordExternal);
-    launch_gather(c->d_gptr, c->d_gsrc, c->d_qloc, nullptr, c->d_q, nG, c->d_state, c->st);
-    n += 2;
-    TRY(allreduce(c, c->d_q, size_t(nG)));
     const bool pr = c->opt.beta_variant == 1;
-    launch_pcg_pq(c->d_p, c->d_q, nG, c->rb, c->d_state, c->st);
+    if (c->nranks == 1) {   // assembly and p.q in one pass
+        launch_gather_pq(c->d_gptr, c->d_gsrc, c->d_qloc, c->d_p, c->d_q, nG, c->rb, c->d_state, c->st);
+        n += 2;
+    } else {
+        launch_gather(c->d_gptr, c->d_gsrc, c->d_qloc, nullptr, c->d_q, nG, c->d_state, c->st);
+        TRY(allreduce(c, c->d_q, size_t(nG)));
+        launch_pcg_pq(c->d_p, c->d_q, nG, c->rb, c->d_state, c->st);
+        n += 3;
+    }
     launch_pcg_update_xr(c->d_x, c->d_r, pr ? c->d_rold : nullptr, c->d_p, c->d_q, nG, c->rb, c->d_state, c->st);
-    n += 2;
+    n += 1;
     int np = 0;
     if (e2) cudaEventRecordWithFlags(e2, c->st, cudaEventRecordExternal);
     TRY(precond(c, c->d_r, c->d_z, c->d_state, &np));

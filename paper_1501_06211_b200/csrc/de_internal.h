@@ -279,6 +279,8 @@ struct RedBuf {
 };
 void launch_pcg_pq(const double* p, const double* q, int64_t n, RedBuf rb, PcgState* s,
                    cudaStream_t st);
+void launch_gather_pq(const int32_t* gptr, const int32_t* gsrc, const double* qloc, const double* p, double* q,
+                      int64_t n, RedBuf rb, PcgState* s, cudaStream_t st);
 void launch_pcg_update_xr(double* x, double* r, double* r_old, const double* p, const double* q,
                           int64_t n, RedBuf rb, PcgState* s, cudaStream_t st);
 void launch_pcg_rz(const double* r, const double* z, const double* r_old, int64_t n, int beta_pr,

@@ -101,6 +101,34 @@ void launch_pcg_pq(const double* p, const double* q, int64_t n, RedBuf rb, PcgSt
     k_pcg_pq<<<red_blocks(n, rb), RB, 0, st>>>(p, q, n, rb, s);
 }
 
+// single rank: q = sum of the local contributions (k_gather) and p.q in one pass (k_pcg_pq's reduction and tail)
+__global__ void k_gather_pq(const int32_t* __restrict__ gptr, const int32_t* __restrict__ gsrc,
+                            const double* __restrict__ qloc, const double* __restrict__ p, double* __restrict__ q,
+                            int64_t n, RedBuf rb, PcgState* s) {
+    if (s->done) return;
+    double v[1] = {0.0}, tot[1];
+    for (int64_t g = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; g < n; g += int64_t(gridDim.x) * blockDim.x) {
+        double acc = 0.0;
+        for (int k = gptr[g]; k < gptr[g + 1]; ++k) acc += qloc[gsrc[k]];
+        q[g] = acc;
+        v[0] += p[g] * acc;
+    }
+    if (grid_reduce<1>(v, tot, rb)) {
+        s->pq = tot[0];
+        if (!(tot[0] > 0.0)) {
+            s->status = DE_EBREAKDOWN;
+            s->done = 1;
+        } else {
+            s->alpha = s->rz / tot[0];
+        }
+    }
+}
+
+void launch_gather_pq(const int32_t* gptr, const int32_t* gsrc, const double* qloc, const double* p, double* q,
+                      int64_t n, RedBuf rb, PcgState* s, cudaStream_t st) {
+    k_gather_pq<<<red_blocks(n, rb), RB, 0, st>>>(gptr, gsrc, qloc, p, q, n, rb, s);
+}
+
 // x += alpha p; r -= alpha q; ||r||^2 -> convergence / iteration cap
 __global__ void k_pcg_update_xr(double* __restrict__ x, double* __restrict__ r, double* __restrict__ r_old,
                                 const double* __restrict__ p, const double* __restrict__ q, int64_t n,
