@@ -1,15 +1,17 @@
-// kernels_prec_coop.cu — the interface preconditioner z = H^_theta^-1 r as ONE
-// persistent cooperative kernel per application: the same algorithm as kernels_precond.cu
-// (R7, R9, R10), but ~60 grid-wide barriers
-// instead of ~110 kernel launches.
+// kernels_prec_coop.cu — the interface preconditioner z = H^_theta^-1 r as one
+// persistent cooperative kernel per application (k_prec_coop: seed, inverse-Lanczos steps, Gram matrices)
+// followed by two small launches (k_prec_ritz: the k x k Ritz problems; k_prec_combine: z = W coef).
+// Same algorithm as kernels_precond.cu (R7, R9, R10).
 //
 // Work distribution: block b serves component c = b % ncomp for row-parallel phases (rows
-// lo_c + lb*CT + tid, stride nbc*CT); face solves are warp-per-face over all components; the cross-
-// point GEMV is split over the component's blocks. Every scalar (norms, Gram-Schmidt coefficients)
-// is a fixed-order sum of per-block partials that EVERY block recomputes after the barrier, so all
-// blocks hold bitwise identical copies and no extra barrier is needed to broadcast them.
-// Per Lanczos step: exact K-solve (3 barriers) + M w & dots (1) + CGS pass 1 with M(w - W h) formed
-// on the fly (1) + CGS pass 2 and ||w||_M (1).
+// lo_c + lb*RW + (tid-32), stride nbc*RW; warp 0 hosts the grid-barrier thread and does no row work);
+// face solves are warp-per-face over all components; the cross-point GEMV is split over the component's
+// blocks. Every scalar (norms, Gram-Schmidt coefficients) is a fixed-order sum of per-block partials that
+// EVERY block recomputes after the barrier, so all blocks hold bitwise identical copies and no extra
+// barrier is needed to broadcast them.
+// Per Lanczos step (2D): exact K-solve (2 barriers: faces by parallel cyclic reduction + t_C; cross-point
+// GEMV; the face correction x_F = y_F - G x_C is folded into the next phase) + phase A (M w, L w, dots) +
+// phase B (CGS pass 1, images by linearity) + phase C (CGS pass 2, ||w||_M, Gram row) = 5 barriers.
 #include "de_internal.h"
 
 #include <cooperative_groups.h>
@@ -186,33 +188,15 @@ __device__ void gram_row_sums(const CoopArgs& a, int jr, const int* kcs, int fir
     }
 }
 
-__device__ __forceinline__ double spmv_row(const CsrDev& A, int64_t i, const double* __restrict__ x) {
-    double acc = 0.0;
-    for (int e = A.ptr[i]; e < A.ptr[i + 1]; ++e) acc += A.val[e] * x[A.col[e]];
-    return acc;
-}
-
-// y_M = sum_e M_ie v_e and (optionally) y_L = sum_e L_ie v_e with v = x - sum_{t<nt} h_t W_t (M and L share
-// one sparsity pattern: both are assembled on the same trace facets). The basis loop is unrolled to KMAX
-// with predication so every load of a row is issued before the first use (latency-bound otherwise).
-template <bool WITH_L>
-__device__ __forceinline__ void corr_spmv(const CsrDev& M, const CsrDev& L, int64_t i, const double* __restrict__ x,
-                                          const double* __restrict__ W, int64_t nflat, const double* h, int nt,
-                                          double& yM, double& yL) {
-    const int e0 = M.ptr[i], e1 = M.ptr[i + 1];
+// (M x)_i and (L x)_i by one pass over the shared sparsity pattern (M and L are assembled on the same trace
+// facets; host_setup checks that the patterns agree)
+__device__ __forceinline__ void spmv_ml(const CsrDev& M, const CsrDev& L, int64_t i, const double* __restrict__ x,
+                                        double& yM, double& yL) {
     double am = 0.0, al = 0.0;
-    for (int e = e0; e < e1; ++e) {
-        const int col = M.col[e];
-        const double mv = M.val[e];
-        const double lv = WITH_L ? L.val[e] : 0.0;
-        double w[KMAX];
-#pragma unroll
-        for (int t = 0; t < KMAX; ++t) w[t] = t < nt ? W[size_t(t) * nflat + col] : 0.0;
-        double v = x[col];
-#pragma unroll
-        for (int t = 0; t < KMAX; ++t) v -= h[t] * w[t];
-        am += mv * v;
-        if (WITH_L) al += lv * v;
+    for (int e = M.ptr[i]; e < M.ptr[i + 1]; ++e) {
+        const double v = x[M.col[e]];
+        am += M.val[e] * v;
+        al += L.val[e] * v;
     }
     yM = am;
     yL = al;
@@ -242,18 +226,6 @@ __device__ __forceinline__ double spmv_elim(const CsrDev& M, const CsrDev& L, in
     yM = am;
     yL = al;
     return xi;
-}
-
-// sum_t h_t W_t[i] with all loads issued up front
-__device__ __forceinline__ double basis_comb(const double* __restrict__ W, int64_t nflat, int64_t i, const double* h,
-                                             int nt) {
-    double w[KMAX];
-#pragma unroll
-    for (int t = 0; t < KMAX; ++t) w[t] = t < nt ? W[size_t(t) * nflat + i] : 0.0;
-    double acc = 0.0;
-#pragma unroll
-    for (int t = 0; t < KMAX; ++t) acc += h[t] * w[t];
-    return acc;
 }
 
 // Warp solve of one face block (L then M = P L^T P forward sweeps, b <= 31, row window in registers).
@@ -886,12 +858,12 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
     gram_zero(gacc);
     const bool fuseM = P.eM.tri && P.eM.fuse;
     for (int64_t i = r0; i < hi; i += rs) {
-        double m, l, sv, unused_h[1] = {0.0};
+        double m, l, sv;
         if (fuseM) {
             sv = spmv_elim(P.M, P.L, i, P.eM, P.y, P.y + nf, m, l);
             P.W[i] = sv;
         } else {
-            corr_spmv<true>(P.M, P.L, i, P.W, P.W, nf, unused_h, 0, m, l);
+            spmv_ml(P.M, P.L, i, P.W, m, l);
             sv = P.W[i];
         }
         P.MW[i] = m;
@@ -935,12 +907,12 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
                 double wt[KM];   // basis loads first (the stores below may alias them for the compiler)
 #pragma unroll
                 for (int t = 0; t < KM; ++t) wt[t] = t < kc ? P.W[size_t(t) * nf + i] : 0.0;
-                double m, l, wi, unused_h[1] = {0.0};
+                double m, l, wi;
                 if (fuseK) {
                     wi = spmv_elim(P.M, P.L, i, P.eK, P.y, P.y + nf, m, l);
                     P.w[i] = wi;
                 } else {
-                    corr_spmv<true>(P.M, P.L, i, P.w, P.W, nf, unused_h, 0, m, l);
+                    spmv_ml(P.M, P.L, i, P.w, m, l);
                     wi = P.w[i];
                 }
                 a.mw1[i] = m;
