@@ -200,6 +200,7 @@ SchurArgs schur_args(de_ctx* c, int mode, const double* xin, const double* f, do
     a.state = s;
     a.mode = mode;
     a.maxG = c->max_nG;
+    a.max_nI = c->max_nI;
     return a;
 }
 
@@ -859,6 +860,7 @@ de_status_t setup_impl(const de_mesh_t* mesh, const double* density, double E0, 
         }
     }
     TRY(dalloc(c, &c->d_scratch, size_t(c->n_local_I) + 32));
+    prepare_schur_blk(hs.ld, hs.band, c->max_nI, c->max_nG);
     TRY(dalloc(c, &c->d_qloc, size_t(c->n_local_G) + 32));
     TRY(dupload(c, &c->d_gptr, gcnt));
     TRY(dupload(c, &c->d_gsrc, gsrc));

@@ -267,6 +267,7 @@ int launch_schur_local(const SchurArgs& a, cudaStream_t st);
 void launch_schur_explicit(const SubDesc* sd, int nsl, const double* sexp, const int32_t* Rg, const double* xin,
                            double* qloc, int maxG, const PcgState* s, cudaStream_t st);
 void prepare_schur_explicit(int maxG);
+void prepare_schur_blk(int ld, int band_w, int max_nI, int maxG);
 
 void launch_gather(const int32_t* gptr, const int32_t* gsrc, const double* qloc,
                    const double* add, double* q, int64_t nG, const PcgState* st_done,

@@ -209,8 +209,6 @@ __global__ void __launch_bounds__(32) k_schur_local(SchurArgs a, int nstage) {
     }
 }
 
-// q_s = S_s x_s, S_s column-major (= row-major by symmetry): thread t accumulates row t over columns k,
-// so each step is one coalesced read of column k. One CTA per subdomain.
 // q_s = S_s x_s from the packed lower tiles (STS x STS, see de_internal.h): every tile is read once and used twice
 // (T x_J for its row block, T^T x_I for its column block), so only half the dense bytes stream from HBM.
 // Warp w owns tile rows dealt in zig-zag order (0, nt-1, 1, nt-2, ...) for balance; lane l holds rows h + 2k
@@ -567,6 +565,144 @@ __global__ void __launch_bounds__(SF_T, 1) k_schur_form(SchurArgs a) {
     }
 }
 
+// ---------------------------------------------------------------- wide bands (3D): blocked solves
+// One CTA per subdomain for APPLY / CONDENSE / BACKSUB when b+1 exceeds the register window of the warp
+// sweep: L is streamed in BK_P-column panels (two-stage TMA ring, one bulk copy per panel). Forward L y = rhs:
+// one warp solves the panel's diagonal block (lane = row, one shuffle per column), then the CTA updates the
+// <= b rows below it. Backward L^T x = y reads the same L panels in descending order: the CTA forms each panel
+// column's dot product with the solved x below the panel, then one warp solves the diagonal block. The chain
+// per row is one shuffle + FMA instead of a full band row, and the M copy is not read.
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+constexpr int BK_T = 256, BK_P = 16, BK_S = 2;   // threads, panel columns, ring stages
+__global__ void __launch_bounds__(BK_T, 1) k_schur_blk(SchurArgs a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    if (a.state != nullptr && a.state->done) return;
+    const unsigned FULL = 0xffffffffu;
+    const SubDesc d = a.sd[blockIdx.x];
+    const int n = d.nI, nG = d.nG, B = a.band_w, ld = a.ld, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int mode = a.mode;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
+    double* pan = reinterpret_cast<double*>(smem + 128);   // [BK_S][BK_P][ld]
+    double* v = pan + BK_S * BK_P * ld;                    // [n]: rhs, then y, then x
+    double* xl = v + a.max_nI;                             // [nG]
+    const double* Lb = a.band + d.band_off;
+    const int np = (n + BK_P - 1) / BK_P;
+    auto panel_of = [&](int q) { return q < np ? q : 2 * np - 1 - q; };   // forward ascending, backward descending
+    auto issue = [&](int q) {
+        const int p = panel_of(q), c0 = p * BK_P, nc = min(BK_P, n - c0);
+        const uint32_t bytes = uint32_t(nc) * uint32_t(ld) * 8u;
+        mbar_expect_tx(bar + (q % BK_S), bytes);
+        tma_load_1d(pan + size_t(q % BK_S) * BK_P * ld, Lb + size_t(c0) * ld, bytes, bar + (q % BK_S));
+    };
+    if (tid == 0) {
+        for (int i = 0; i < BK_S; ++i) mbar_init(bar + i, 1);
+        fence_mbar_init();
+        for (int q = 0; q < min(BK_S, 2 * np); ++q) issue(q);
+    }
+    if (mode != SCHUR_CONDENSE)
+        for (int l = tid; l < nG; l += BK_T) xl[l] = a.xin[a.Rg[d.goff + l]];
+    __syncthreads();
+    const int32_t* igp = a.igp + d.igp_off;
+    const int32_t* idofs = a.idofs + d.ioff;
+    for (int r = tid; r < n; r += BK_T) {          // dense interior right-hand side
+        double val = (mode == SCHUR_APPLY) ? 0.0 : a.f[idofs[r]];
+        if (mode != SCHUR_CONDENSE) {
+            double acc = 0.0;
+            for (int e = igp[r]; e < igp[r + 1]; ++e) acc += a.ig_val[e] * xl[a.ig_col[e]];
+            val = (mode == SCHUR_APPLY) ? acc : val - acc;
+        }
+        v[r] = val;
+    }
+    __syncthreads();
+    for (int q = 0; q < 2 * np; ++q) {
+        mbar_wait(bar + (q % BK_S), uint32_t((q / BK_S) & 1));
+        const double* P = pan + size_t(q % BK_S) * BK_P * ld;
+        const int p = panel_of(q), j0 = p * BK_P, nc = min(BK_P, n - j0);
+        if (q < np) {   // forward: diagonal block, then the rows below
+            if (wid == 0) {   // unrolled: every coefficient load is off the shuffle-FMA chain
+                double vr = lane < nc ? v[j0 + lane] : 0.0;
+                double cf[BK_P], dg[BK_P];
+#pragma unroll
+                for (int jj = 0; jj < BK_P; ++jj) {
+                    cf[jj] = (jj < nc && lane > jj && lane < nc) ? P[jj * ld + (lane - jj)] : 0.0;
+                    dg[jj] = jj < nc ? P[jj * ld] : 0.0;   // slot 0 holds 1 / L_jj
+                }
+#pragma unroll
+                for (int jj = 0; jj < BK_P; ++jj) {
+                    const double yj = __shfl_sync(FULL, vr, jj) * dg[jj];
+                    vr = lane == jj ? yj : fma(-cf[jj], yj, vr);
+                }
+                if (lane < nc) v[j0 + lane] = vr;
+            }
+            __syncthreads();
+            const int ihi = min(n, j0 + nc + B);
+            for (int i = j0 + nc + tid; i < ihi; i += BK_T) {
+                double acc = 0.0;
+#pragma unroll
+                for (int jj = 0; jj < BK_P; ++jj) {
+                    const int k = i - (j0 + jj);
+                    if (jj < nc && k <= B) acc = fma(P[jj * ld + k], v[j0 + jj], acc);
+                }
+                v[i] -= acc;
+            }
+        } else {        // backward: dots with the solved rows below, then the diagonal block
+            for (int jj = wid; jj < nc; jj += BK_T / 32) {
+                const int j = j0 + jj;
+                double acc = 0.0;
+                for (int k = (j0 + nc - j) + lane; k <= B && j + k < n; k += 32) acc = fma(P[jj * ld + k], v[j + k], acc);
+                acc = warp_sum_d(acc);
+                if (lane == 0) v[j] -= acc;
+            }
+            __syncthreads();
+            if (wid == 0) {
+                double tr = lane < nc ? v[j0 + lane] : 0.0;
+                double cf[BK_P], dg[BK_P];
+#pragma unroll
+                for (int jj = 0; jj < BK_P; ++jj) {
+                    cf[jj] = (jj < nc && lane < jj) ? P[lane * ld + (jj - lane)] : 0.0;
+                    dg[jj] = jj < nc ? P[jj * ld] : 0.0;
+                }
+#pragma unroll
+                for (int jj = BK_P - 1; jj >= 0; --jj) {
+                    const double xj = __shfl_sync(FULL, tr, jj) * dg[jj];
+                    tr = lane == jj ? xj : fma(-cf[jj], xj, tr);
+                }
+                if (lane < nc) v[j0 + lane] = tr;
+            }
+        }
+        __syncthreads();
+        if (tid == 0 && q + BK_S < 2 * np) issue(q + BK_S);   // every reader is past this panel
+    }
+    if (mode == SCHUR_BACKSUB) {
+        for (int i = tid; i < n; i += BK_T) a.u[idofs[i]] = v[i];
+        return;
+    }
+    const int32_t* gxp = a.gxp + d.gxp_off;
+    for (int l = tid; l < nG; l += BK_T) {
+        double qv = 0.0;
+        for (int e = gxp[l]; e < gxp[l + 1]; ++e) {
+            const int cidx = a.gx_col[e];
+            if (cidx >= 0) {
+                if (mode == SCHUR_APPLY) qv += a.gx_val[e] * xl[cidx];
+            } else {
+                qv -= a.gx_val[e] * v[-cidx - 1];
+            }
+        }
+        a.qloc[d.goff + l] = qv;
+    }
+}
+
+// once per context, outside any graph capture
+void prepare_schur_blk(int ld, int band_w, int max_nI, int maxG) {
+    if ((band_w + 1 + 31) / 32 <= 4) return;
+    const size_t smem = 128 + sizeof(double) * (size_t(BK_S) * BK_P * ld + max_nI + maxG);
+    cudaFuncSetAttribute(k_schur_blk, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+}
+
 constexpr int COL_R = 8;
 
 template <int G, int NS>
@@ -597,6 +733,11 @@ static void launch_t(const SchurArgs& a, int nstage, size_t smem, cudaStream_t s
 
 int launch_schur_local(const SchurArgs& a, cudaStream_t st) {
     if (a.nsl == 0) return 0;
+    if (a.mode != SCHUR_COLUMNS && (a.band_w + 1 + 31) / 32 > 4 && !getenv("DE_SCHUR_WARP")) {   // wide bands
+        const size_t smem = 128 + sizeof(double) * (size_t(BK_S) * BK_P * a.ld + a.max_nI + a.maxG);
+        k_schur_blk<<<unsigned(a.nsl), BK_T, smem, st>>>(a);
+        return 1;
+    }
     if (a.mode == SCHUR_COLUMNS && a.band_w + 1 <= SF_W && a.ld % 2 == 0 && !getenv("DE_FORM_WARP") &&
         size_t(2) * SF_CB * a.ld * 8 + size_t(a.max_ig) * 12 + size_t(a.max_nI + 1) * 4 <= 200 * 1024) {
         const size_t smem = size_t(2) * SF_CB * a.ld * sizeof(double) + size_t(a.max_ig) * 12 + size_t(a.max_nI + 1) * 4;
