@@ -305,8 +305,8 @@ def main():
     schur_kernel = "k_schur_explicit" if st.schur_explicit else "k_schur_local"
     schur_bytes = st.bytes_schur_explicit if st.schur_explicit else st.bytes_schur
     roof_s = roofline(schur_kernel, "C2 Schur apply", schur_bytes, k_ms, k_n)
-    roof_p = roofline("k_prec_coop", "C5 inverse-Lanczos preconditioner, one cooperative launch", st.bytes_prec,
-                      p_ms, p_n) if p_n else None
+    roof_p = roofline("k_prec_coop", "C5 preconditioner application: k_prec_coop + k_prec_ritz + k_prec_combine, "
+                      "event-timed as one", st.bytes_prec, p_ms, p_n) if p_n else None
     if roof_p and (roof_p["share_of_step"] or 0) > (roof_s["share_of_step"] or 0):
         roof, roof2 = roof_p, roof_s
     else:
