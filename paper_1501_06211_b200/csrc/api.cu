@@ -877,7 +877,7 @@ de_status_t setup_impl(const de_mesh_t* mesh, const double* density, double E0, 
     TRY(dalloc(c, &c->d_state, 1));
     TRY(dalloc(c, &c->d_scal, 8));
     TRY(dalloc(c, &c->d_fail, 1));
-    c->rb.nblk = 148 * 2;
+    c->rb.nblk = 148 * 8;   // enough blocks for one interface dof per thread in k_gather_pq
     TRY(dalloc(c, &c->rb.part, size_t(c->rb.nblk) * 4));
     TRY(dalloc(c, &c->rb.counter, 1));
     DE_CUDA(cudaMemsetAsync(c->rb.counter, 0, sizeof(unsigned int), c->st));
