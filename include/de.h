@@ -99,6 +99,11 @@ typedef struct {
                                 facet element of M and L is scaled by the mean SIMP modulus of its two adjacent
                                 elements; the preconditioner is rebuilt by de_factor after each density update.
                                 0 (default): the unweighted norm of PAPER.md:172 (R6) */
+    int32_t outer;           /* outer Krylov method of de_solve: 0 (default) = interface PCG on S u_Gamma = g (BASELINE
+                                metric); 1 = right-preconditioned flexible GMRES on the full system
+                                K u = f with P~ = [[K_II, K_IGamma], [0, S~]],
+                                single rank; `iterations` then counts FGMRES iterations */
+    int32_t restart;         /* FGMRES restart length m, 1 <= m <= 31 (default 30) */
 } de_options_t;
 
 typedef struct {

@@ -16,9 +16,10 @@ from dataclasses import replace
 
 from .fem import free_system, true_relres, apply_K
 from .topology import build_topology
-from .dd import subdomain_blocks, factor_subdomains, schur_apply, condensed_rhs, back_substitute
+from .dd import (subdomain_blocks, factor_subdomains, schur_apply, condensed_rhs, back_substitute, solve_II,
+                 dense_schur)
 from .precond import build_components, apply_precond
-from .krylov import pcg
+from .krylov import pcg, fgmres
 
 
 def monolithic_solve(prob):
@@ -71,6 +72,42 @@ class DDOracle:
         g = condensed_rhs(prob, self.topo, self.blocks)
         uG, its, conv, hist = pcg(self.S, g, self.P, tol_abs, maxit, x0=x0, beta=self.beta)
         return back_substitute(prob, self.topo, self.blocks, uG), its, conv, hist
+
+    def P_full(self, v, exact_S=None):
+        """P~^-1 v on a full dof vector: z_Gamma = S~^-1 v_Gamma, then
+        z_I = K_II^-1 (v_I - K_IGamma z_Gamma) per subdomain; Dirichlet entries 0."""
+        topo = self.topo
+        vG = v[topo.gamma_dofs]
+        zG = np.linalg.solve(exact_S, vG) if exact_S is not None else self.P(vG)
+        z = np.zeros_like(v)
+        z[topo.gamma_dofs] = zG
+        for b in self.blocks:
+            if len(b.I):
+                z[b.I] = solve_II(b, v[b.I] - b.AIG @ zG[b.R])
+        return z
+
+    def solve_fgmres(self, rtol=None, maxit=2000, restart=30, exact_S=False):
+        """The paper's formulation (NEXT(4)): right-preconditioned flexible GMRES on the
+        full system K u = f over the free dofs with P~ = [[K_II, K_IGamma], [0, S~]], S~ = H_theta (or the exact
+        Schur complement when exact_S). Stop: ||f - K u|| <= rtol ||f_free|| (the estimate, then the true
+        residual at each restart). Returns DDResult."""
+        prob = self.prob
+        rtol = prob.rtol if rtol is None else rtol
+        if self.blocks is None:
+            self.factor()
+        free = prob.fixed == 0
+        Sd = dense_schur(self.blocks, self.topo.n_G) if exact_S else None
+
+        def A(u):
+            out = apply_K(prob, u)
+            out[~free] = 0.0
+            return out
+
+        b = np.where(free, prob.rhs, 0.0)
+        nf = np.linalg.norm(b)
+        u, its, conv, hist = fgmres(A, b, lambda v: self.P_full(v, Sd), rtol * nf, maxit, restart)
+        return DDResult(u=u, iterations=its, converged=conv, relres=true_relres(prob, u),
+                        uG=u[self.topo.gamma_dofs], history=hist, its_pass1=its)
 
     def solve(self, rtol=None, maxit=20000, warm=False, max_refine=3):
         """Interface PCG to ||r_Gamma|| <= rtol ||f_free|| (recursive residual), then iterative

@@ -39,7 +39,8 @@ class de_options_t(C.Structure):
                 ("nranks", C.c_int32), ("device", C.c_int32), ("nccl_id", C.c_void_p),
                 ("stream", C.c_void_p), ("check_every", C.c_int32), ("use_graph", C.c_int32),
                 ("host_only", C.c_int32), ("prec_kernels", C.c_int32), ("schur_mode", C.c_int32),
-                ("weighted_trace", C.c_int32)]
+                ("weighted_trace", C.c_int32),
+                ("outer", C.c_int32), ("restart", C.c_int32)]
 
 
 class de_stats_t(C.Structure):

@@ -124,6 +124,11 @@ struct de_ctx {
     int col_batch = 0;
     int max_ig = 0;
     int64_t n_sexp = 0;
+    // full-system FGMRES (outer = 1) work space, allocated on first use
+    double *fg_V = nullptr, *fg_Z = nullptr, *fg_w = nullptr, *fg_r = nullptr, *fg_zero = nullptr, *fg_vG = nullptr,
+           *fg_zG = nullptr, *fg_h = nullptr;
+    RedBuf fg_rb{};
+    int fg_m = 0;
     // nccl
     void* comm = nullptr;
     de_stats_t stats{};
@@ -1031,6 +1036,121 @@ de_status_t true_residual(de_ctx* c, const double* d_f, const double* d_u, doubl
     return DE_OK;
 }
 
+// z = P~^-1 v on full dof vectors: z_Gamma = S~^-1 v_Gamma (the interface preconditioner),
+// z_I = K_II^-1 (v_I - K_IGamma z_Gamma) (the back-substitution of the Schur kernels), Dirichlet entries 0
+de_status_t prec_full(de_ctx* c, const double* v, double* z) {
+    HostSetup& hs = c->hs;
+    launch_gather_gamma(c->d_gamma_dofs, v, c->fg_vG, hs.n_G, c->st);
+    TRY(precond(c, c->fg_vG, c->fg_zG, nullptr, nullptr));
+    DE_CUDA(cudaMemsetAsync(z, 0, sizeof(double) * hs.ndof, c->st));
+    launch_scatter_gamma(c->d_gamma_dofs, c->fg_zG, z, hs.n_G, c->st);
+    launch_schur_local(schur_args(c, SCHUR_BACKSUB, c->fg_zG, v, z, nullptr), c->st);
+    c->launches += 3;
+    return check_launch();
+}
+
+// Right-preconditioned flexible GMRES(m) on K u = f over the free dofs (NEXT(4)); Arnoldi by
+// classical Gram-Schmidt applied twice (two batched fixed-order dot products per step), Givens rotations on the
+// host; stop when the estimate reaches rtol ||f|| (the true residual is recomputed at every restart).
+de_status_t fgmres_impl(de_ctx* c, const double* d_f, double rtol, double fnorm, double* d_u, int32_t* iters,
+                        double* relres) {
+    HostSetup& hs = c->hs;
+    if (c->nranks > 1) {
+        set_error("outer = 1 (full-system FGMRES) is single-rank in this version");
+        return DE_EINVAL;
+    }
+    const int m = std::min(std::max(1, c->opt.restart), FG_ND - 1);
+    const size_t nd = size_t(hs.ndof);
+    if (c->fg_m != m) {
+        TRY(dalloc(c, &c->fg_V, (m + 1) * nd));
+        TRY(dalloc(c, &c->fg_Z, m * nd));
+        TRY(dalloc(c, &c->fg_w, nd));
+        TRY(dalloc(c, &c->fg_r, nd));
+        TRY(dalloc(c, &c->fg_zero, nd));
+        TRY(dalloc(c, &c->fg_vG, size_t(hs.n_G)));
+        TRY(dalloc(c, &c->fg_zG, size_t(hs.n_G)));
+        TRY(dalloc(c, &c->fg_h, size_t(2 * FG_ND + 8)));
+        c->fg_rb.nblk = c->rb.nblk;
+        TRY(dalloc(c, &c->fg_rb.part, size_t(c->fg_rb.nblk) * FG_ND));
+        TRY(dalloc(c, &c->fg_rb.counter, 1));
+        DE_CUDA(cudaMemsetAsync(c->fg_rb.counter, 0, sizeof(unsigned int), c->st));
+        DE_CUDA(cudaMemsetAsync(c->fg_zero, 0, sizeof(double) * nd, c->st));
+        c->fg_m = m;
+    }
+    const int maxit = c->opt.max_iter > 0 ? c->opt.max_iter : 20000;
+    const double tol = rtol * fnorm;
+    DE_CUDA(cudaMemsetAsync(d_u, 0, sizeof(double) * nd, c->st));
+    std::vector<double> H(size_t(m + 1) * m), cs(m), sn(m), g(m + 1), hb(2 * FG_ND + 2);
+    int its = 0, cycles = 0;
+    double r2 = 0.0;
+    double* hd = c->fg_h;   // [0, FG_ND): first pass, [FG_ND, 2 FG_ND): second pass, [2 FG_ND]: ||w||^2
+    while (true) {
+        TRY(true_residual(c, d_f, d_u, &r2));   // d_res = K u - f (Dirichlet 0)
+        if (std::sqrt(r2) <= tol || its >= maxit) break;
+        DE_CUDA(cudaMemsetAsync(c->fg_r, 0, sizeof(double) * nd, c->st));
+        launch_axpy(c->fg_r, c->d_res, -1.0, hs.ndof, c->st);
+        DE_CUDA(cudaMemcpyAsync(c->d_scal, &r2, sizeof(double), cudaMemcpyHostToDevice, c->st));
+        launch_scale_invnorm(c->fg_V, c->fg_r, c->d_scal, hs.ndof, c->st);
+        std::fill(g.begin(), g.end(), 0.0);
+        g[0] = std::sqrt(r2);
+        int k = 0;
+        for (int j = 0; j < m; ++j) {
+            double* Vj = c->fg_V + j * nd;
+            double* Zj = c->fg_Z + j * nd;
+            TRY(prec_full(c, Vj, Zj));
+            launch_apply_K(c->md, c->d_Ee, Zj, c->fg_zero, c->d_cls, c->fg_w, hs.ndof, c->st);
+            launch_multidot(c->fg_V, nd, j + 1, c->fg_w, hs.ndof, c->fg_rb, hd, c->st);
+            launch_multi_axpy(c->fg_w, c->fg_V, nd, j + 1, hd, -1.0, hs.ndof, c->st);
+            launch_multidot(c->fg_V, nd, j + 1, c->fg_w, hs.ndof, c->fg_rb, hd + FG_ND, c->st);
+            launch_multi_axpy(c->fg_w, c->fg_V, nd, j + 1, hd + FG_ND, -1.0, hs.ndof, c->st);
+            launch_norm2(c->fg_w, hs.ndof, c->rb, hd + 2 * FG_ND, c->st);
+            launch_scale_invnorm(c->fg_V + (j + 1) * nd, c->fg_w, hd + 2 * FG_ND, hs.ndof, c->st);
+            c->launches += 8;
+            TRY(check_launch());
+            DE_CUDA(cudaMemcpyAsync(hb.data(), hd, sizeof(double) * (2 * FG_ND + 1), cudaMemcpyDeviceToHost, c->st));
+            DE_CUDA(cudaStreamSynchronize(c->st));
+            for (int i = 0; i <= j; ++i) H[size_t(i) * m + j] = hb[i] + hb[FG_ND + i];
+            H[size_t(j + 1) * m + j] = std::sqrt(std::max(hb[2 * FG_ND], 0.0));
+            for (int i = 0; i < j; ++i) {   // previous rotations
+                const double a = H[size_t(i) * m + j], b = H[size_t(i + 1) * m + j];
+                H[size_t(i) * m + j] = cs[i] * a + sn[i] * b;
+                H[size_t(i + 1) * m + j] = -sn[i] * a + cs[i] * b;
+            }
+            const double a = H[size_t(j) * m + j], b = H[size_t(j + 1) * m + j], rho = std::hypot(a, b);
+            cs[j] = rho > 0.0 ? a / rho : 1.0;
+            sn[j] = rho > 0.0 ? b / rho : 0.0;
+            H[size_t(j) * m + j] = rho;
+            H[size_t(j + 1) * m + j] = 0.0;
+            g[j + 1] = -sn[j] * g[j];
+            g[j] = cs[j] * g[j];
+            ++its;
+            k = j + 1;
+            if (std::fabs(g[j + 1]) <= tol || its >= maxit) break;
+        }
+        std::vector<double> y(k);
+        for (int i = k - 1; i >= 0; --i) {   // H y = g (upper triangular)
+            double t = g[i];
+            for (int jj = i + 1; jj < k; ++jj) t -= H[size_t(i) * m + jj] * y[jj];
+            y[i] = t / H[size_t(i) * m + i];
+        }
+        DE_CUDA(cudaMemcpyAsync(hd, y.data(), sizeof(double) * k, cudaMemcpyHostToDevice, c->st));
+        launch_multi_axpy(d_u, c->fg_Z, nd, k, hd, 1.0, hs.ndof, c->st);
+        c->launches += 1;
+        ++cycles;
+    }
+    c->stats.iterations = c->stats.iterations_pass1 = its;
+    c->stats.restarts = cycles;
+    c->stats.relres_true = c->stats.relres_recursive = std::sqrt(r2) / fnorm;
+    c->stats.kernels_launched = c->launches;
+    if (iters) *iters = its;
+    if (relres) *relres = c->stats.relres_true;
+    if (std::sqrt(r2) > tol) {
+        set_error("FGMRES did not reach rtol in %d iterations (true relres %.3e)", its, c->stats.relres_true);
+        return DE_ENOCONV;
+    }
+    return DE_OK;
+}
+
 de_status_t solve_impl(de_ctx* c, const double* d_f, double rtol, double* d_u, int32_t* iters, double* relres) {
     if (!c->factored) {
         set_error("de_solve called before a successful de_factor");
@@ -1056,6 +1176,12 @@ de_status_t solve_impl(de_ctx* c, const double* d_f, double rtol, double* d_u, i
         if (relres) *relres = 0.0;
         c->stats.relres_true = c->stats.relres_recursive = 0.0;
         return DE_OK;
+    }
+    if (c->opt.outer == 1) {
+        auto ta = std::chrono::steady_clock::now();
+        const de_status_t st = fgmres_impl(c, d_f, rtol, fnorm, d_u, iters, relres);
+        c->stats.ms_solve = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - ta).count();
+        return st;
     }
     const int maxit = c->opt.max_iter > 0 ? c->opt.max_iter : 20000;
     cudaEvent_t l0, l1;
@@ -1150,6 +1276,8 @@ void de_default_options(de_options_t* o) {
     o->stream = nullptr;
     o->check_every = 8;
     o->use_graph = 1;
+    o->outer = 0;
+    o->restart = 30;
 }
 
 const char* de_last_error(void) { return g_err; }

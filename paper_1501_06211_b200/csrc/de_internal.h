@@ -290,6 +290,12 @@ void launch_pcg_update_p(double* p, const double* z, int64_t n, PcgState* s, cud
 void launch_pcg_init(double* r, double* p, const double* z, const double* g, const double* Sx,
                      int64_t n, int mode, RedBuf rb, PcgState* s, cudaStream_t st);
 void launch_norm2(const double* v, int64_t n, RedBuf rb, double* out, cudaStream_t st);
+constexpr int FG_ND = 32;   // max FGMRES restart length + 1 (batched dot products)
+void launch_multidot(const double* V, int64_t ld, int nv, const double* w, int64_t n, RedBuf rb, double* out,
+                     cudaStream_t st);
+void launch_multi_axpy(double* w, const double* V, int64_t ld, int nv, const double* coef, double sign, int64_t n,
+                       cudaStream_t st);
+void launch_scale_invnorm(double* dst, const double* src, const double* sq, int64_t n, cudaStream_t st);
 void launch_copy(double* dst, const double* src, int64_t n, const PcgState* s, cudaStream_t st);
 void launch_axpy(double* y, const double* x, double a, int64_t n, cudaStream_t st);
 void launch_scatter_gamma(const int32_t* gamma_dofs, const double* uG, double* u, int64_t nG,

@@ -238,6 +238,52 @@ void launch_norm2(const double* v, int64_t n, RedBuf rb, double* out, cudaStream
     k_norm2<<<red_blocks(n, rb), RB, 0, st>>>(v, n, rb, out);
 }
 
+// ---------------------------------------------------------------- full-system FGMRES (NEXT(4)) helpers
+// out[i] = V_i . w for i < nv (nv <= FG_ND), V_i = V + i * ld; one fixed-order reduction (rb.part >= nblk*FG_ND)
+__global__ void k_multidot(const double* __restrict__ V, int64_t ld, int nv, const double* __restrict__ w, int64_t n,
+                           RedBuf rb, double* __restrict__ out) {
+    double v[FG_ND], tot[FG_ND];
+#pragma unroll
+    for (int i = 0; i < FG_ND; ++i) v[i] = 0.0;
+    for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < n; k += int64_t(gridDim.x) * blockDim.x) {
+        const double wk = w[k];
+#pragma unroll
+        for (int i = 0; i < FG_ND; ++i)
+            if (i < nv) v[i] = fma(V[i * ld + k], wk, v[i]);
+    }
+    if (grid_reduce<FG_ND>(v, tot, rb))
+        for (int i = 0; i < nv; ++i) out[i] = tot[i];
+}
+
+// w += sign * sum_{i < nv} coef[i] V_i (coef on the device)
+__global__ void k_multi_axpy(double* __restrict__ w, const double* __restrict__ V, int64_t ld, int nv,
+                             const double* __restrict__ coef, double sign, int64_t n) {
+    for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < n; k += int64_t(gridDim.x) * blockDim.x) {
+        double acc = 0.0;
+        for (int i = 0; i < nv; ++i) acc = fma(coef[i], V[i * ld + k], acc);
+        w[k] = fma(sign, acc, w[k]);
+    }
+}
+
+// dst = src / sqrt(*sq) (sq = squared norm on the device; dst = 0 when it is 0)
+__global__ void k_scale_invnorm(double* __restrict__ dst, const double* __restrict__ src, const double* sq, int64_t n) {
+    const double s = *sq > 0.0 ? 1.0 / sqrt(*sq) : 0.0;
+    for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < n; k += int64_t(gridDim.x) * blockDim.x)
+        dst[k] = src[k] * s;
+}
+
+void launch_multidot(const double* V, int64_t ld, int nv, const double* w, int64_t n, RedBuf rb, double* out,
+                     cudaStream_t st) {
+    k_multidot<<<red_blocks(n, rb), RB, 0, st>>>(V, ld, nv, w, n, rb, out);
+}
+void launch_multi_axpy(double* w, const double* V, int64_t ld, int nv, const double* coef, double sign, int64_t n,
+                       cudaStream_t st) {
+    k_multi_axpy<<<int(std::min<int64_t>((n + 255) / 256, 148 * 8)), 256, 0, st>>>(w, V, ld, nv, coef, sign, n);
+}
+void launch_scale_invnorm(double* dst, const double* src, const double* sq, int64_t n, cudaStream_t st) {
+    k_scale_invnorm<<<int(std::min<int64_t>((n + 255) / 256, 148 * 8)), 256, 0, st>>>(dst, src, sq, n);
+}
+
 __global__ void k_copy(double* __restrict__ dst, const double* __restrict__ src, int64_t n, const PcgState* s) {
     if (s != nullptr && s->done) return;
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)

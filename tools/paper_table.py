@@ -30,19 +30,8 @@ def its(p, **kw):
         S.close()
 
 
-def main():
-    t0 = time.time()
-    res = {}
-    for n in NS:
-        for ih in HS:
-            p = paper_problem(ih, n)
-            res[("I", n, ih)] = its(p, inner_mode=3)
-            res[("H", n, ih)] = its(p, theta=0.5)
-            res[("OPT", n, ih)] = its(p, theta=THETA_OPT[n])
-    out = ["# Table 1 re-run (PAPER.md:201-232) on the B200 path", "",
-           "Interface PCG to rtol 1e-6 on the paper's test problem (`synthetic.paper_problem`), k = 10, exact inner",
-           "solves; cell = ours / paper (paper: full-system GMRES, tolerance 1e-6). Compare trends, not values",
-           "(DESIGN.md R18).", "",
+def table(title, note, res):
+    out = [f"## {title}", "", note, "",
            "| 1/h | I: N=4 | 16 | 64 | H_0.5: N=4 | 16 | 64 | H_OPT (0.5/0.6/0.7): N=4 | 16 | 64 |",
            "|---|---|---|---|---|---|---|---|---|---|"]
     for k, ih in enumerate(HS):
@@ -51,7 +40,28 @@ def main():
             for n in NS:
                 cells.append(f"{res[(col, n, ih)]} / {PAPER[col][n][k]}")
         out.append(f"| {ih} | " + " | ".join(cells) + " |")
-    out += ["", f"wall time {time.time() - t0:.1f} s"]
+    return out
+
+
+def main():
+    t0 = time.time()
+    out = ["# Table 1 re-run (PAPER.md:201-232) on the B200 path", "",
+           "The paper's test problem (`synthetic.paper_problem`, DESIGN.md R18), k = 10 Lanczos vectors, exact inner",
+           "solves, tolerance 1e-6; cell = ours / paper (paper: GMRES on the full system).", ""]
+    for outer, title, note in (
+            (1, "Full-system FGMRES with P~ = [[K_II, K_IG], [0, S~]] (the paper's solver, NEXT(4))",
+             "Right-preconditioned flexible GMRES(31) on K u = f (PAPER.md:153-181)."),
+            (0, "Interface PCG (the BASELINE method)", "PCG on S u_Gamma = g, rtol 1e-6 on ||f||.")):
+        res = {}
+        kw0 = dict(outer=1, restart=31) if outer else {}
+        for n in NS:
+            for ih in HS:
+                p = paper_problem(ih, n)
+                res[("I", n, ih)] = its(p, inner_mode=3, **kw0)
+                res[("H", n, ih)] = its(p, theta=0.5, **kw0)
+                res[("OPT", n, ih)] = its(p, theta=THETA_OPT[n], **kw0)
+        out += table(title, note, res) + [""]
+    out += [f"wall time {time.time() - t0:.1f} s"]
     print("\n".join(out))
 
 
