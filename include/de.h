@@ -204,6 +204,42 @@ de_status_t de_get_kernel_time(const de_ctx_t* ctx, double* ms_schur_per_launch,
 de_status_t de_get_prec_time(const de_ctx_t* ctx, double* ms_prec_per_launch, int64_t* launches);
 
 void de_destroy(de_ctx_t* ctx);
+/* ---- Topology-optimisation design update (R20) ----
+ * The loop the solver serves: solve K(rho) u = f, then one optimality-criteria (OC) step, then de_factor.
+ * The paper states no OC constants; R20 fixes the standard minimum-compliance OC update:
+ *   dc_e   = -p rho_e^(p-1) (E0 - Emin) u_e^T KE0 u_e          compliance c = sum_e E_e u_e^T KE0 u_e
+ *   rho_e' = clip(rho_e (max(-dc_e,0)/lambda)^eta, max(rho_min, rho_e - move), min(1, rho_e + move))
+ *   lambda by bisection on [0, 1e9 max(-dc)] until l2 - l1 <= tol (l1 + l2) or maxit halvings, so that
+ *   sum_e rho_e' = volfrac * n_elem (unit element volumes). VTS is p = 1, Emin = 0. */
+typedef struct {
+    double volfrac;   /* target mean density V, in (0, 1] */
+    double move;      /* move limit per step, > 0 */
+    double rho_min;   /* lower density bound, in (0, 1); the upper bound is 1 */
+    double eta;       /* damping exponent, > 0 (0.5 standard) */
+    double tol;       /* relative bisection tolerance on lambda, > 0 */
+    int32_t maxit;    /* bisection steps, in [1, 10000] (each is two launches; converged steps are no-ops) */
+} de_oc_params_t;
+
+/* volfrac 0.5, move 0.2, rho_min 1e-3, eta 0.5, tol 1e-12, maxit 200. */
+void de_default_oc_params(de_oc_params_t* prm);
+
+/* Element sensitivities of the compliance at the context's current densities for the displacement d_u
+ * (device, float64, ndof — e.g. de_solve_device's output). d_dc: device, float64, prod(nel) out, or NULL
+ * (kept inside the context for de_oc_update_device). compliance: host scalar out, or NULL (no sync). */
+de_status_t de_sensitivities_device(de_ctx_t* ctx, const double* d_u, double* d_dc, double* compliance);
+
+/* One OC step from the sensitivities d_dc (device, prod(nel); NULL = those of the last
+ * de_sensitivities_device call): the new densities replace the context's (de_factor must be called next)
+ * and are copied to d_rho_new (device, prod(nel)) if non-NULL. lambda: host scalar out, or NULL.
+ * DE_EINVAL on parameters out of range or when d_dc is NULL and no sensitivities exist. */
+de_status_t de_oc_update_device(de_ctx_t* ctx, const double* d_dc, const de_oc_params_t* prm,
+                                double* d_rho_new, double* lambda);
+
+/* Host-buffer form of both calls: u host (ndof) in, rho_new host (prod(nel)) out (may be NULL);
+ * compliance/lambda host scalars (may be NULL). */
+de_status_t de_oc_step(de_ctx_t* ctx, const double* u, const de_oc_params_t* prm, double* rho_new,
+                       double* compliance, double* lambda);
+
 const char* de_last_error(void);
 
 #ifdef __cplusplus

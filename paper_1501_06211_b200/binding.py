@@ -58,6 +58,11 @@ class de_stats_t(C.Structure):
                 ("bytes_prec", C.c_double)]
 
 
+class de_oc_params_t(C.Structure):
+    _fields_ = [("volfrac", C.c_double), ("move", C.c_double), ("rho_min", C.c_double), ("eta", C.c_double),
+                ("tol", C.c_double), ("maxit", C.c_int32)]
+
+
 _lib = None
 
 
@@ -92,6 +97,10 @@ def lib():
         "de_set_profiling": (I32, [P, I32]),
         "de_get_kernel_time": (I32, [P, C.POINTER(D), C.POINTER(I64)]),
         "de_get_prec_time": (I32, [P, C.POINTER(D), C.POINTER(I64)]),
+        "de_default_oc_params": (None, [C.POINTER(de_oc_params_t)]),
+        "de_sensitivities_device": (I32, [P, P, P, C.POINTER(D)]),
+        "de_oc_update_device": (I32, [P, P, C.POINTER(de_oc_params_t), P, C.POINTER(D)]),
+        "de_oc_step": (I32, [P, P, C.POINTER(de_oc_params_t), P, C.POINTER(D), C.POINTER(D)]),
         "de_destroy": (None, [P]),
         "de_last_error": (C.c_char_p, []),
     }
@@ -253,6 +262,36 @@ def de_get_prec_time(ctx):
     return ms.value, n.value
 
 
+def de_default_oc_params(**kw) -> de_oc_params_t:
+    o = de_oc_params_t()
+    lib().de_default_oc_params(C.byref(o))
+    for k, v in kw.items():
+        setattr(o, k, v)
+    return o
+
+
+def de_sensitivities_device(ctx, d_u_ptr: int, d_dc_ptr: int | None = None, want_compliance=True):
+    c = C.c_double()
+    _check(lib().de_sensitivities_device(ctx, C.c_void_p(d_u_ptr), C.c_void_p(d_dc_ptr) if d_dc_ptr else None,
+                                         C.byref(c) if want_compliance else None))
+    return c.value if want_compliance else None
+
+
+def de_oc_update_device(ctx, d_dc_ptr: int | None, params: de_oc_params_t, d_rho_new_ptr: int | None = None):
+    lam = C.c_double()
+    _check(lib().de_oc_update_device(ctx, C.c_void_p(d_dc_ptr) if d_dc_ptr else None, C.byref(params),
+                                     C.c_void_p(d_rho_new_ptr) if d_rho_new_ptr else None, C.byref(lam)))
+    return lam.value
+
+
+def de_oc_step(ctx, u, params: de_oc_params_t, nelem: int):
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    rho = np.empty(nelem, np.float64)
+    c, lam = C.c_double(), C.c_double()
+    _check(lib().de_oc_step(ctx, _ptr(u), C.byref(params), _ptr(rho), C.byref(c), C.byref(lam)))
+    return rho, c.value, lam.value
+
+
 def de_destroy(ctx):
     if ctx:
         lib().de_destroy(ctx)
@@ -285,6 +324,11 @@ class Solver:
 
     def solve(self, rhs, rtol=1e-10, allow_noconv=False):
         return de_solve(self.ctx, rhs, rtol, allow_noconv=allow_noconv)
+
+    def oc_step(self, u, nelem, **params):
+        """One optimality-criteria design update from the displacement u (R20); the new densities
+        replace the context's, so factor() must be called before the next solve."""
+        return de_oc_step(self.ctx, u, de_default_oc_params(**params), nelem)
 
     def stats(self):
         return de_get_stats(self.ctx)

@@ -11,7 +11,7 @@ CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libde.so")
 SOURCES = ["host_setup.cpp", "kernels_fem.cu", "kernels_schur.cu", "kernels_krylov.cu",
-           "kernels_precond.cu", "kernels_prec_coop.cu", "api.cu"]
+           "kernels_precond.cu", "kernels_prec_coop.cu", "kernels_topopt.cu", "api.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",

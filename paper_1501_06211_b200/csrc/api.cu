@@ -128,6 +128,10 @@ struct de_ctx {
     double *fg_V = nullptr, *fg_Z = nullptr, *fg_w = nullptr, *fg_r = nullptr, *fg_zero = nullptr, *fg_vG = nullptr,
            *fg_zG = nullptr, *fg_h = nullptr;
     RedBuf fg_rb{};
+    // topology-optimisation design update (allocated on first use)
+    double *oc_dc = nullptr, *oc_part = nullptr, *oc_rho = nullptr;
+    OcState* oc_st = nullptr;
+    bool oc_have_dc = false;
     int fg_m = 0;
     // nccl
     void* comm = nullptr;
@@ -819,6 +823,7 @@ de_status_t setup_impl(const de_mesh_t* mesh, const double* density, double E0, 
     }
     c->md.nke = hs.nke;
     upload_KE0(hs.KE0, hs.nke, c->st);
+    upload_KE0_oc(hs.KE0, hs.nke, c->st);
     TRY(dupload(c, &c->d_sd, c->hsd));
     TRY(dalloc(c, &c->d_rho, hs.nelem));
     DE_CUDA(cudaMemcpyAsync(c->d_rho, density, sizeof(double) * hs.nelem, cudaMemcpyHostToDevice, c->st));
@@ -1557,6 +1562,122 @@ de_status_t de_get_prec_time(const de_ctx_t* c, double* ms, int64_t* launches) {
     }
     if (ms) *ms = c->prof_n_prec ? c->prof_ms_prec / double(c->prof_n_prec) : 0.0;
     if (launches) *launches = c->prof_n_prec;
+    return DE_OK;
+}
+
+void de_default_oc_params(de_oc_params_t* p) {
+    if (!p) return;
+    p->volfrac = 0.5;
+    p->move = 0.2;
+    p->rho_min = 1e-3;
+    p->eta = 0.5;
+    p->tol = 1e-12;
+    p->maxit = 200;
+}
+
+namespace {
+de_status_t oc_alloc(de_ctx* c) {
+    if (c->oc_dc) return DE_OK;
+    const int64_t n = c->hs.nelem;
+    TRY(dalloc(c, &c->oc_dc, size_t(n)));
+    TRY(dalloc(c, &c->oc_rho, size_t(n)));
+    TRY(dalloc(c, &c->oc_part, size_t(2 * oc_blocks(n))));
+    TRY(dalloc(c, &c->oc_st, 1));
+    return DE_OK;
+}
+
+de_status_t oc_check(const de_oc_params_t* p) {
+    if (!p) {
+        set_error("null OC parameters");
+        return DE_EINVAL;
+    }
+    if (!(p->volfrac > 0.0 && p->volfrac <= 1.0) || !(p->move > 0.0) || !(p->rho_min > 0.0 && p->rho_min < 1.0) ||
+        !(p->eta > 0.0) || !(p->tol > 0.0) || p->maxit < 1 || p->maxit > 10000) {
+        set_error("OC parameters out of range (volfrac in (0,1], move > 0, rho_min in (0,1), eta > 0, tol > 0, "
+                  "maxit in [1, 10000])");
+        return DE_EINVAL;
+    }
+    return DE_OK;
+}
+
+OcParams oc_params(const de_oc_params_t* p) {
+    return OcParams{p->volfrac, p->move, p->rho_min, p->eta, p->tol, p->maxit};
+}
+}  // namespace
+
+de_status_t de_sensitivities_device(de_ctx_t* c, const double* d_u, double* d_dc, double* compliance) {
+    if (!c || !d_u) {
+        set_error("null argument");
+        return DE_EINVAL;
+    }
+    TRY(need_device(c));
+    DE_CUDA(cudaSetDevice(c->opt.device));
+    TRY(oc_alloc(c));
+    const int64_t n = c->hs.nelem;
+    launch_simp(c->d_rho, c->d_Ee, n, c->E0, c->Emin, c->p, c->st);
+    c->launches += 1 + launch_sensitivities(c->md, d_u, c->d_rho, c->d_Ee, c->E0, c->Emin, c->p, n, c->oc_dc,
+                                            c->oc_part, c->oc_st, c->st);
+    c->oc_have_dc = true;
+    if (d_dc && d_dc != c->oc_dc)
+        DE_CUDA(cudaMemcpyAsync(d_dc, c->oc_dc, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->st));
+    if (compliance) {
+        OcState h{};
+        DE_CUDA(cudaMemcpyAsync(&h, c->oc_st, sizeof(OcState), cudaMemcpyDeviceToHost, c->st));
+        DE_CUDA(cudaStreamSynchronize(c->st));
+        *compliance = h.compliance;
+    }
+    return DE_OK;
+}
+
+de_status_t de_oc_update_device(de_ctx_t* c, const double* d_dc, const de_oc_params_t* prm, double* d_rho_new,
+                                double* lambda) {
+    if (!c) {
+        set_error("null context");
+        return DE_EINVAL;
+    }
+    TRY(oc_check(prm));
+    TRY(need_device(c));
+    DE_CUDA(cudaSetDevice(c->opt.device));
+    TRY(oc_alloc(c));
+    const int64_t n = c->hs.nelem;
+    if (!d_dc && !c->oc_have_dc) {
+        set_error("de_oc_update_device: d_dc is NULL and no de_sensitivities_device call preceded it");
+        return DE_EINVAL;
+    }
+    if (d_dc && d_dc != c->oc_dc)
+        DE_CUDA(cudaMemcpyAsync(c->oc_dc, d_dc, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->st));
+    c->launches += launch_oc_update(c->d_rho, c->oc_dc, n, oc_params(prm), c->oc_part, c->oc_st, c->oc_rho, c->st);
+    DE_CUDA(cudaMemcpyAsync(c->d_rho, c->oc_rho, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->st));
+    if (d_rho_new)
+        DE_CUDA(cudaMemcpyAsync(d_rho_new, c->oc_rho, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->st));
+    c->factored = false;
+    c->dens_dirty = true;
+    if (lambda) {
+        OcState h{};
+        DE_CUDA(cudaMemcpyAsync(&h, c->oc_st, sizeof(OcState), cudaMemcpyDeviceToHost, c->st));
+        DE_CUDA(cudaStreamSynchronize(c->st));
+        *lambda = h.lambda;
+    }
+    return DE_OK;
+}
+
+de_status_t de_oc_step(de_ctx_t* c, const double* u, const de_oc_params_t* prm, double* rho_new,
+                       double* compliance, double* lambda) {
+    if (!c || !u) {
+        set_error("null argument");
+        return DE_EINVAL;
+    }
+    TRY(oc_check(prm));
+    TRY(need_device(c));
+    DE_CUDA(cudaSetDevice(c->opt.device));
+    const int64_t nd = c->hs.ndof, n = c->hs.nelem;
+    DE_CUDA(cudaMemcpyAsync(c->d_ubuf, u, sizeof(double) * nd, cudaMemcpyHostToDevice, c->st));
+    TRY(de_sensitivities_device(c, c->d_ubuf, nullptr, compliance));
+    TRY(de_oc_update_device(c, nullptr, prm, nullptr, lambda));
+    if (rho_new) {
+        DE_CUDA(cudaMemcpyAsync(rho_new, c->oc_rho, sizeof(double) * n, cudaMemcpyDeviceToHost, c->st));
+        DE_CUDA(cudaStreamSynchronize(c->st));
+    }
     return DE_OK;
 }
 

@@ -144,6 +144,16 @@ struct PcgState {
     int32_t it, done, status, maxit;
 };
 
+// optimality-criteria design update (kernels_topopt.cu, R20)
+struct OcParams {
+    double volfrac, move, rho_min, eta, tol;
+    int32_t maxit;
+};
+struct OcState {
+    double compliance, l1, l2, lambda;
+    int32_t it, done;
+};
+
 struct ElimDev {
     int32_t nfaces, ncross, ncomp, maxface;
     int32_t *face_off, *face_nodes, *face_band;
@@ -223,6 +233,13 @@ struct LzState {                    // per component inverse-Lanczos bookkeeping
 void launch_simp(const double* rho, double* Ee, int64_t nelem, double E0, double Emin, double p,
                  cudaStream_t st);
 void upload_KE0(const double* ke, int nke, cudaStream_t st);
+void upload_KE0_oc(const double* ke, int nke, cudaStream_t st);
+int oc_blocks(int64_t n);
+int launch_sensitivities(const MeshDev& m, const double* u, const double* rho, const double* Ee, double E0,
+                         double Emin, double p, int64_t nelem, double* dc, double* part, OcState* st,
+                         cudaStream_t s);
+int launch_oc_update(const double* rho, const double* dc, int64_t n, const OcParams& prm, double* part,
+                     OcState* st, double* rho_new, cudaStream_t s);
 void launch_assemble_band(const MeshDev& m, const SubDesc* sd, int nsl, const int32_t* idofs,
                           const double* Ee, double* band, int ld, int band_w, int max_nI,
                           cudaStream_t st);

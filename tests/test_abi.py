@@ -49,14 +49,14 @@ def test_default_options_and_struct_sizes(lib):
     import subprocess, tempfile
     src = ('#include "de.h"\n#include <stdio.h>\n#include <stddef.h>\nint main(){printf("%zu %zu %zu %zu %zu",'
            'sizeof(de_options_t), sizeof(de_mesh_t), sizeof(de_stats_t), offsetof(de_options_t, nccl_id),'
-           'offsetof(de_stats_t, n_cross));return 0;}')
+           'offsetof(de_stats_t, n_cross));printf(" %zu", sizeof(de_oc_params_t));return 0;}')
     with tempfile.TemporaryDirectory() as d:
         open(os.path.join(d, "t.c"), "w").write(src)
         subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), os.path.join(d, "t.c"), "-o",
                                os.path.join(d, "t")])
         got = list(map(int, subprocess.check_output([os.path.join(d, "t")]).split()))
     assert got == [ctypes.sizeof(B.de_options_t), ctypes.sizeof(B.de_mesh_t), ctypes.sizeof(B.de_stats_t),
-                   B.de_options_t.nccl_id.offset, B.de_stats_t.n_cross.offset]
+                   B.de_options_t.nccl_id.offset, B.de_stats_t.n_cross.offset, ctypes.sizeof(B.de_oc_params_t)]
 
 
 def test_no_cpu_fallback_without_device(lib):
