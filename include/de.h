@@ -73,10 +73,11 @@ typedef struct {
     double theta;            /* fractional index theta of H~_theta; default 0.5 */
     int32_t lanczos_k;       /* inverse-Lanczos basis size k; default 10 */
     int32_t inner_mode;      /* preconditioner: 1 = inverse Lanczos with exact inner solves (mode X,
-                                DESIGN.md R10); 3 = identity S~ = I. (0 = SPEC face-PCG inner: not
-                                on the GPU path yet -> DE_EINVAL) */
-    double inner_tol;        /* reserved for inner_mode 0 */
-    int32_t inner_max_iter;  /* reserved for inner_mode 0 */
+                                DESIGN.md R10); 0 = inverse Lanczos with SPEC's face-preconditioned PCG
+                                inner solves of K (mode F: tol inner_tol, x0 = 0, cap inner_max_iter;
+                                PAPER.md:235-237,273); 3 = identity S~ = I */
+    double inner_tol;        /* inner_mode 0: relative 2-norm tolerance of the inner PCG; default 1e-3 */
+    int32_t inner_max_iter;  /* inner_mode 0: inner PCG iteration cap; default 1000 */
     int32_t max_iter;        /* outer PCG iteration cap; default 20000 */
     int32_t beta_variant;    /* 0 = Fletcher-Reeves (default), 1 = Polak-Ribiere (flexible) */
     int32_t warm_start;      /* 1: start PCG from the previous solve's u_Gamma (config-5 sequence) */
@@ -132,6 +133,8 @@ typedef struct {
     double bytes_schur_explicit; /* algorithmic bytes of one explicit S apply: sum_s n_Gamma,s^2 * 8 + vectors */
     double bytes_prec;       /* algorithmic bytes of one preconditioner application (k_prec_coop; per-phase
                                 streaming model of DESIGN.md "Kernels and their rooflines"), 0 if none */
+    int64_t inner_iterations; /* inner_mode 0: face-PCG iterations of all inner solves since de_setup
+                                 (summed over solves and components); 0 otherwise */
 } de_stats_t;
 
 /* Fill *opt with defaults (theta 0.5, k 10, inner_mode 1, max_iter 20000, FR, 1 rank). */

@@ -642,6 +642,23 @@ de_status_t upload_prec_impl(de_ctx* c) {
     DE_CUDA(cudaMemsetAsync(P.counter, 0, size_t(nslots) * sizeof(unsigned int), c->st));
     prec_prepare(P);
     c->have_prec = true;
+    if (c->opt.inner_mode == 0) {   // SPEC face-PCG inner solves (multi-kernel path + k_face_pcg)
+        if (fpcg_prepare(P, c->opt.device) <= 0) {
+            set_error("inner_mode 0 needs a cooperative launch of k_face_pcg (device or shared memory limit)");
+            return DE_ECUDA;
+        }
+        P.inner_f = 1;
+        P.fp_tol = c->opt.inner_tol;
+        P.fp_maxit = c->opt.inner_max_iter;
+        TRY(dalloc(c, &P.fr, nf));
+        TRY(dalloc(c, &P.fz, nf));
+        TRY(dalloc(c, &P.fp, nf));
+        TRY(dalloc(c, &P.fq, nf));
+        TRY(dalloc(c, &P.fpart, size_t(2) * MAXC * P.fp_nb));
+        TRY(dalloc(c, &P.fits, 1));
+        DE_CUDA(cudaMemsetAsync(P.fits, 0, sizeof(unsigned long long), c->st));
+        return DE_OK;
+    }
     if (c->opt.prec_kernels == 0 && prec_coop_prepare(P, c->opt.device, c->coop)) {
         TRY(dalloc(c, &c->coop.red, prec_coop_red_doubles(c->coop)));
         TRY(dalloc(c, &c->coop.gram, prec_coop_gram_doubles(c->coop)));
@@ -711,12 +728,16 @@ de_status_t setup_impl(const de_mesh_t* mesh, const double* density, double E0, 
         set_error("invalid material parameters (E0 > 0, Emin >= 0, p > 0, -1 < nu < 1/2, h > 0)");
         return DE_EINVAL;
     }
-    if (opt.inner_mode != 1 && opt.inner_mode != 3) {
-        set_error("inner_mode %d not supported on the GPU path (1 = exact-inner inverse Lanczos, 3 = identity)",
-                  opt.inner_mode);
+    if (opt.inner_mode != 0 && opt.inner_mode != 1 && opt.inner_mode != 3) {
+        set_error("inner_mode %d not supported on the GPU path (0 = face-PCG inner solves, 1 = exact-inner "
+                  "inverse Lanczos, 3 = identity)", opt.inner_mode);
         return DE_EINVAL;
     }
-    if (opt.inner_mode == 1 && (opt.lanczos_k < 1 || opt.lanczos_k > KMAX)) {
+    if (opt.inner_mode == 0 && (!(opt.inner_tol > 0.0) || opt.inner_max_iter < 1)) {
+        set_error("inner_mode 0 needs inner_tol > 0 and inner_max_iter >= 1");
+        return DE_EINVAL;
+    }
+    if ((opt.inner_mode == 0 || opt.inner_mode == 1) && (opt.lanczos_k < 1 || opt.lanczos_k > KMAX)) {
         set_error("lanczos_k must be in [1, %d]", KMAX);
         return DE_EINVAL;
     }
@@ -891,7 +912,7 @@ de_status_t setup_impl(const de_mesh_t* mesh, const double* density, double E0, 
     TRY(dalloc(c, &c->rb.part, size_t(c->rb.nblk) * 4));
     TRY(dalloc(c, &c->rb.counter, 1));
     DE_CUDA(cudaMemsetAsync(c->rb.counter, 0, sizeof(unsigned int), c->st));
-    if (opt.inner_mode == 1) TRY(upload_prec(c));
+    if (opt.inner_mode == 0 || opt.inner_mode == 1) TRY(upload_prec(c));
     DE_CUDA(cudaStreamSynchronize(c->st));
     TRY(check_launch());
     // ---- NCCL
@@ -1431,6 +1452,13 @@ de_status_t de_get_stats(const de_ctx_t* c, de_stats_t* s) {
         return DE_EINVAL;
     }
     *s = c->stats;
+    s->inner_iterations = 0;
+    if (c->have_prec && c->P.inner_f && c->P.fits) {
+        unsigned long long n = 0;
+        DE_CUDA(cudaMemcpyAsync(&n, c->P.fits, sizeof(n), cudaMemcpyDeviceToHost, c->st));
+        DE_CUDA(cudaStreamSynchronize(c->st));
+        s->inner_iterations = int64_t(n);
+    }
     return DE_OK;
 }
 

@@ -336,7 +336,14 @@ struct PrecDev {
     double* part;
     unsigned int* counter;
     int nblk;
+    // inner_mode 0 (SPEC face-PCG inner solves of K, R10): one cooperative kernel per solve
+    int32_t inner_f, fp_nb, fp_maxit;
+    size_t fp_smem;
+    double fp_tol;
+    double *fr, *fz, *fp, *fq, *fpart;
+    unsigned long long* fits;   // inner PCG iterations accumulated over all solves (de_stats)
 };
+int fpcg_prepare(PrecDev& P, int device);   // blocks / smem of k_face_pcg; 0 if no cooperative launch
 void prec_apply(const PrecDev& P, const double* r, double* z, const PcgState* s, cudaStream_t st,
                 int* nlaunch);
 void launch_gauss_jordan(double* A, double* Bbuf, int n, cudaStream_t st);

@@ -14,6 +14,9 @@
 // Reductions are fixed-shape (deterministic), segmented per component and per task.
 #include "de_internal.h"
 
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
+
 namespace de {
 
 constexpr int PB = 256;
@@ -176,6 +179,252 @@ __global__ void k_cross_solve(ElimDev E, const double* __restrict__ b, const dou
             x[E.cross_flat[base + rr]] = acc;
         }
     }
+}
+
+// ------------------------------------------------------------------ mode F: face-preconditioned inner PCG
+// SPEC's inner solve of K x = b (R10), every component at
+// once: textbook PCG from x0 = 0, preconditioner = K restricted to each face (cross points removed) solved
+// exactly with the face band factors + Jacobi (diag K) at the cross points, stop when ||r||_2 <= tol ||b||_2
+// (per component) or after maxit iterations. One cooperative kernel per solve, four grid barriers per
+// iteration (p update | q = K p, p.q | x, r update, r.r | z = P r, r.z); per-component scalars are fixed-order
+// sums of per-block partials that every block recomputes after the barrier (bitwise identical everywhere).
+constexpr int FP_T = 256;
+
+struct FpcgArgs {
+    PrecDev P;
+    const double* b;
+    double* x;
+    const PcgState* s;
+};
+
+// z_F = K_FF^-1 r_F for face F (warp; both band sweeps as in k_face_solve, factor read from global memory);
+// returns this lane's share of r_F . z_F
+__device__ double fp_face(const ElimDev& E, int F, const double* __restrict__ r, double* __restrict__ z,
+                          double* rb, double* ys, int* idx, int lane) {
+    const int o = E.face_off[F], n = E.face_off[F + 1] - o, bw = E.face_band[F], ld = bw + 1;
+    const double* Lf = E.face_fac + E.face_fac_off[F];
+    const double* Mf = Lf + size_t(n) * ld;
+    __syncwarp();
+    for (int i = lane; i < n; i += 32) {
+        const int node = E.face_nodes[o + i];
+        idx[i] = node;
+        rb[i] = r[node];
+    }
+    __syncwarp();
+#pragma unroll 1
+    for (int sw = 0; sw < 2; ++sw) {
+        const double* fac = sw == 0 ? Lf : Mf;
+        const double* src = sw == 0 ? rb : ys;   // the second sweep writes rb[n, 2n) (r_F stays for the dot)
+        double v = lane < n ? src[lane] : 0.0;
+        __syncwarp();
+        for (int j = 0; j < n; ++j) {
+            const double* col = fac + size_t(j) * ld;
+            const double cl = (lane >= 1 && lane <= bw) ? col[lane] : 0.0;
+            const double nxt = (j + 32 < n) ? src[j + 32] : 0.0;
+            const double yj = __shfl_sync(0xffffffffu, v, 0) * col[0];
+            v = fma(-cl, yj, v);
+            const double vs = __shfl_down_sync(0xffffffffu, v, 1);
+            v = (lane == 31) ? nxt : vs;
+            if (sw == 0) ys[n - 1 - j] = yj;
+            else if (lane == 0) rb[n + n - 1 - j] = yj;
+        }
+        __syncwarp();
+    }
+    double acc = 0.0;
+    for (int i = lane; i < n; i += 32) {
+        const double zi = rb[n + i];
+        z[idx[i]] = zi;
+        acc += rb[i] * zi;
+    }
+    return acc;
+}
+
+__device__ __forceinline__ double fp_diag(const CsrDev& K, int64_t i) {
+    for (int e = K.ptr[i]; e < K.ptr[i + 1]; ++e)
+        if (K.col[e] == i) return K.val[e];
+    return 1.0;
+}
+
+// block partial of acc[0..nc) into part[(slot*MAXC + c)*nb + block]; fixed-order totals into tot[c]
+__device__ void fp_reduce(const FpcgArgs& a, double (&acc)[MAXC], int slot, double* tot, double (*sred)[MAXC]) {
+    const int nc = a.P.ncomp, lane = threadIdx.x & 31, w = threadIdx.x >> 5, nb = gridDim.x;
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c) {
+        double t = acc[c];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        if (lane == 0) sred[w][c] = t;
+    }
+    __syncthreads();
+    if (threadIdx.x < nc) {
+        double t = 0.0;
+        for (int k = 0; k < FP_T / 32; ++k) t += sred[k][threadIdx.x];
+        a.P.fpart[(size_t(slot) * MAXC + threadIdx.x) * nb + blockIdx.x] = t;
+    }
+    __syncthreads();
+    cg::this_grid().sync();
+    if (w < nc) {
+        const double* pp = a.P.fpart + (size_t(slot) * MAXC + w) * nb;
+        double t = 0.0;
+        for (int k = lane; k < nb; k += 32) t += *((volatile const double*)(pp + k));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        if (lane == 0) tot[w] = t;
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(FP_T) k_face_pcg(FpcgArgs a) {
+    if (a.s && a.s->done) return;
+    const PrecDev& P = a.P;
+    const ElimDev& E = P.eK;
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ double fsm[];
+    __shared__ double sred[FP_T / 32][MAXC];
+    __shared__ double tot[MAXC], nb2[MAXC], rz[MAXC], al[MAXC], be[MAXC];
+    __shared__ int done[MAXC];
+    const int nc = P.ncomp, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t n = P.nflat, gt = blockIdx.x * int64_t(FP_T) + threadIdx.x, gs = int64_t(gridDim.x) * FP_T;
+    const int gw = blockIdx.x * (FP_T / 32) + w, nw = gridDim.x * (FP_T / 32);
+    const int mf = E.maxface & 0xffff;
+    double* rb = fsm + size_t(w) * (4 * mf);        // [0, n) r_F, [n, 2n) z_F
+    double* ys = rb + 2 * mf;
+    int* idx = reinterpret_cast<int*>(fsm + size_t(FP_T / 32) * 4 * mf) + w * mf;
+    double* x = a.x;
+    double *r = P.fr, *z = P.fz, *p = P.fp, *q = P.fq;
+    double acc[MAXC];
+    int slot = 0;
+    // x = 0, r = b, ||b||^2
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c) acc[c] = 0.0;
+    for (int64_t i = gt; i < n; i += gs) {
+        const double bi = a.b[i];
+        x[i] = 0.0;
+        r[i] = bi;
+        acc[comp_of(P.comp_off, nc, i)] += bi * bi;
+    }
+    fp_reduce(a, acc, slot, tot, sred);
+    slot ^= 1;
+    if (threadIdx.x < MAXC) {
+        nb2[threadIdx.x] = threadIdx.x < nc ? tot[threadIdx.x] : 0.0;
+        done[threadIdx.x] = threadIdx.x < nc ? (tot[threadIdx.x] == 0.0) : 1;
+    }
+    __syncthreads();
+    int it = 0;
+    for (;;) {
+        // z = P r (faces: warp each; cross points: Jacobi), r.z
+#pragma unroll
+        for (int c = 0; c < MAXC; ++c) acc[c] = 0.0;
+        for (int F = gw; F < E.nfaces; F += nw) {
+            const int c = comp_of(P.comp_off, nc, E.face_nodes[E.face_off[F]]);
+            if (done[c]) continue;
+            const double t = fp_face(E, F, r, z, rb, ys, idx, lane);
+#pragma unroll
+            for (int cc = 0; cc < MAXC; ++cc)
+                if (cc == c) acc[cc] += t;
+        }
+        for (int64_t k = gt; k < E.ncross; k += gs) {
+            const int64_t i = E.cross_flat[k];
+            const int c = comp_of(P.comp_off, nc, i);
+            if (done[c]) continue;
+            const double zi = r[i] / fp_diag(P.K, i);
+            z[i] = zi;
+#pragma unroll
+            for (int cc = 0; cc < MAXC; ++cc)
+                if (cc == c) acc[cc] += r[i] * zi;
+        }
+        fp_reduce(a, acc, slot, tot, sred);
+        slot ^= 1;
+        if (threadIdx.x < nc && !done[threadIdx.x]) {
+            be[threadIdx.x] = it == 0 ? 0.0 : tot[threadIdx.x] / rz[threadIdx.x];
+            rz[threadIdx.x] = tot[threadIdx.x];
+        }
+        __syncthreads();
+        ++it;
+        // p = z + beta p
+        for (int64_t i = gt; i < n; i += gs) {
+            const int c = comp_of(P.comp_off, nc, i);
+            if (!done[c]) p[i] = it == 1 ? z[i] : z[i] + be[c] * p[i];
+        }
+        grid.sync();
+        // q = K p, p.q
+#pragma unroll
+        for (int c = 0; c < MAXC; ++c) acc[c] = 0.0;
+        for (int64_t i = gt; i < n; i += gs) {
+            const int c = comp_of(P.comp_off, nc, i);
+            if (done[c]) continue;
+            double t = 0.0;
+            for (int e = P.K.ptr[i]; e < P.K.ptr[i + 1]; ++e) t += P.K.val[e] * p[P.K.col[e]];
+            q[i] = t;
+#pragma unroll
+            for (int cc = 0; cc < MAXC; ++cc)
+                if (cc == c) acc[cc] += p[i] * t;
+        }
+        fp_reduce(a, acc, slot, tot, sred);
+        slot ^= 1;
+        if (threadIdx.x < nc && !done[threadIdx.x]) al[threadIdx.x] = rz[threadIdx.x] / tot[threadIdx.x];
+        __syncthreads();
+        // x += alpha p, r -= alpha q, r.r
+#pragma unroll
+        for (int c = 0; c < MAXC; ++c) acc[c] = 0.0;
+        for (int64_t i = gt; i < n; i += gs) {
+            const int c = comp_of(P.comp_off, nc, i);
+            if (done[c]) continue;
+            x[i] += al[c] * p[i];
+            const double ri = r[i] - al[c] * q[i];
+            r[i] = ri;
+#pragma unroll
+            for (int cc = 0; cc < MAXC; ++cc)
+                if (cc == c) acc[cc] += ri * ri;
+        }
+        fp_reduce(a, acc, slot, tot, sred);
+        slot ^= 1;
+        if (threadIdx.x < nc && !done[threadIdx.x]) {
+            const double t = sqrt(tot[threadIdx.x]), bn = sqrt(nb2[threadIdx.x]);
+            if (t <= P.fp_tol * bn || it >= P.fp_maxit) {
+                done[threadIdx.x] = 1;
+                if (blockIdx.x == 0) atomicAdd(P.fits, (unsigned long long)it);
+            }
+        }
+        __syncthreads();
+        bool all = true;
+        for (int c = 0; c < nc; ++c) all = all && done[c];
+        if (all) break;
+    }
+}
+
+int fpcg_prepare(PrecDev& P, int device) {
+    int nsm = 0, coop = 0;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device);
+    if (!coop) return 0;
+    const int mf = std::max(1, P.eK.maxface & 0xffff);
+    const size_t smem = size_t(FP_T / 32) * (4 * mf * sizeof(double) + mf * sizeof(int));
+    if (smem > 200 * 1024) return 0;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k_face_pcg, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_face_pcg, FP_T, smem) != cudaSuccess || per_sm < 1)
+        return 0;
+    P.fp_nb = nsm * std::min(per_sm, 2);
+    P.fp_smem = smem;
+    return P.fp_nb;
+}
+
+static void face_pcg_solve(const PrecDev& P, const double* b, double* x, const PcgState* s, cudaStream_t st,
+                           int* nl) {
+    FpcgArgs a{P, b, x, s};
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(P.fp_nb);
+    cfg.blockDim = dim3(FP_T);
+    cfg.dynamicSmemBytes = P.fp_smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_face_pcg, a);
+    ++*nl;
 }
 
 static void elim_solve(const PrecDev& P, const ElimDev& E, const double* b, double* x, const PcgState* s,
@@ -570,7 +819,8 @@ void prec_apply(const PrecDev& P, const double* r, double* z, const PcgState* s,
     k_spmv_dot<<<gseg, PB, 0, st>>>(P, P.M, P.s, P.Mw, 0, 0, s); ++nl;            // ||s||_M
     k_lz_normalize<<<eb, 256, 0, st>>>(P, P.s, P.Mw, 0, s); ++nl;                  // q_1, v = M q_1
     for (int j = 1; j < P.kmax; ++j) {
-        elim_solve(P, P.eK, P.v, P.w, s, st, &nl);                                 // w = K^-1 M q_j
+        if (P.inner_f) face_pcg_solve(P, P.v, P.w, s, st, &nl);                   // w ~ K^-1 M q_j (mode F)
+        else elim_solve(P, P.eK, P.v, P.w, s, st, &nl);                            // w = K^-1 M q_j
         k_spmv_dot<<<gseg, PB, 0, st>>>(P, P.M, P.w, P.Mw, 1, j, s); ++nl;        // ||w||_M before
         for (int pass = 0; pass < 2; ++pass) {                                     // CGS2
             if (pass == 1) { k_spmv_dot<<<gseg, PB, 0, st>>>(P, P.M, P.w, P.Mw, -1, j, s); ++nl; }
