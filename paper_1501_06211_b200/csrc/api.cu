@@ -694,7 +694,7 @@ double elim_bytes_model(const HElim& E, bool tri) {
     return b;
 }
 
-double prec_bytes_model(const HostSetup& hs, int k) {
+double prec_bytes_model(const HostSetup& hs, int k, bool gram_cgs2) {
     const double n = double(hs.comp_off[hs.ncomp]), nnz = double(hs.M.val.size()), d = 8.0;
     bool tri = true;
     for (const HElim* E : {&hs.elimK, &hs.elimM})
@@ -708,7 +708,7 @@ double prec_bytes_model(const HostSetup& hs, int k) {
     b += spmv + n * d * 3;                                                  // seed: Ms, Ls, s.r
     for (int j = 1; j < k; ++j) {
         b += spmv + n * d * (j + 2);                                        // A: M w, L w, W^T M w
-        b += n * d * (3.0 * j + 3 + 3);                                     // B: w1, M w1, L w1
+        if (!gram_cgs2) b += n * d * (3.0 * j + 3 + 3);                     // B: w1, M w1, L w1 (two-pass)
         b += n * d * (3.0 * j + 4 + 3);                                     // C: w2, M w2, L w2, Gram row j
     }
     b += n * d * k + n * (4 + d);                                           // z = W coef, scatter
@@ -959,7 +959,7 @@ de_status_t setup_impl(const de_mesh_t* mesh, const double* density, double E0, 
                     double(c->n_local_I + c->nsl) * 4.0;
     S.bytes_iter = fb + double(c->n_ig + c->n_gx) * 12.0 + double(c->n_local_G) * 8.0 * 3.0 +
                    double(hs.n_G) * 8.0 * 11.0;
-    S.bytes_prec = c->have_prec ? prec_bytes_model(hs, c->P.kmax) : 0.0;
+    S.bytes_prec = c->have_prec ? prec_bytes_model(hs, c->P.kmax, c->use_coop && c->coop.gram_cgs2) : 0.0;
     return DE_OK;
 }
 

@@ -353,7 +353,7 @@ void prec_prepare(const PrecDev& P);   // one-time kernel attributes (outside gr
 struct CoopBuffers {
     int nb = 0, nsm = 148;
     size_t smem = 0;
-    int stage = 0, per_warp = 0, mf = 0, ncmax = 0, nbc_max = 0, tridiag = 0;
+    int stage = 0, per_warp = 0, mf = 0, ncmax = 0, nbc_max = 0, tridiag = 0, gram_cgs2 = 1;
     double *red = nullptr, *gram = nullptr, *gram_tot = nullptr, *w1 = nullptr, *mw1 = nullptr, *lw1 = nullptr;
     unsigned long long* timers = nullptr;   // phase stamps (diagnostics; env DE_PREC_TIMERS=1)
     const void* kfn = nullptr;              // k_prec_coop instantiation (basis bound, timers)

@@ -10,8 +10,10 @@
 // EVERY block recomputes after the barrier, so all blocks hold bitwise identical copies and no extra
 // barrier is needed to broadcast them.
 // Per Lanczos step (2D): exact K-solve (2 barriers: faces by parallel cyclic reduction + t_C; cross-point
-// GEMV; the face correction x_F = y_F - G x_C is folded into the next phase) + phase A (M w, L w, dots) +
-// phase B (CGS pass 1, images by linearity) + phase C (CGS pass 2, ||w||_M, Gram row) = 5 barriers.
+// GEMV; the face correction x_F = y_F - G x_C is folded into the next phase) + phase A (M w, L w, dots h) +
+// phase C (w - W (2h - G h) with the images by linearity, ||w||_M, Gram row) = 4 barriers: the second
+// Gram-Schmidt pass is formed from the Gram matrix G = W^T M W (R21); env DE_CGS2_TWO_PASS runs the
+// literal two-pass form (phase B = pass 1 over the rows, phase C = pass 2) for A/B runs and tests.
 #include "de_internal.h"
 
 #include <cooperative_groups.h>
@@ -46,6 +48,7 @@ struct CoopArgs {
     int mf;             // max face size
     int ncmax;          // max cross points per component
     int tridiag;        // 1: every face block is tridiagonal with <= TRI_MAX nodes (2D) -> thread per face
+    int gram_cgs2;      // 1: the second Gram-Schmidt pass is formed from the Gram matrix (one row pass fewer)
     unsigned long long* timers;   // optional phase timestamps (block 0), DE_PREC_TIMERS
 };
 
@@ -935,8 +938,29 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
         if (tid < nc) nb2v[tid] = tot[tid][0];
         if (tid < KMAX) hsm[c][tid] = tid < kc ? tot[c][1 + tid] * sclh[c][tid] * sclh[c][tid] : 0.0;
         __syncthreads();
+        if (a.gram_cgs2) {
+            // second Gram-Schmidt pass from the Gram matrix (R21): h' = W^T M (w - W h) = h - G h with
+            // G = W^T M W from the Gram rows 0..kc-1 (summed by now), so w2 = w - W (2h - G h) in one pass over the
+            // rows; per raw basis vector the coefficient is 2 hsm_t - sclh_t^2 sum_s Graw_M[t][s] hsm_s
+            double* gsm = dsm;   // [KMAX][KMAX] raw M-Gram of this component (dsm is free between phases)
+            for (int e = tid; e < kc * kc; e += CT) {
+                const int t = e / kc, u = e - t * kc, hi_ = t > u ? t : u, lo_ = t > u ? u : t;
+                gsm[t * KMAX + u] = *((volatile const double*)(a.gram_tot + (size_t(c) * KMAX + hi_) * GW + KMAX + lo_));
+            }
+            __syncthreads();
+            double hn = 0.0;
+            if (tid < kc) {
+                double g = 0.0;
+                for (int u = 0; u < kc; ++u) g += gsm[tid * KMAX + u] * hsm[c][u];
+                hn = 2.0 * hsm[c][tid] - sclh[c][tid] * sclh[c][tid] * g;
+            }
+            __syncthreads();
+            if (tid < kc) hsm[c][tid] = hn;
+            __syncthreads();
+        }
         // B: w1 = w - W h; M w1 = M w - (M W) h and L w1 = L w - (L W) h by linearity (own rows only);
         // dots h'_t = W_t . M w1
+        if (!a.gram_cgs2) {
         DBGT(130);
         ZERO_VALS();
         if (part)
@@ -974,6 +998,7 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
         pp ^= 1;
         if (tid < KMAX) hsm[c][tid] = tid < kc ? tot[c][tid] * sclh[c][tid] * sclh[c][tid] : 0.0;
         __syncthreads();
+        }   // !a.gram_cgs2
         // C: w2 = w1 - W h' with M w2, L w2 by linearity (M w2 is the next solve's rhs); ||w2||_M^2; row j of
         // the Rayleigh-Ritz Gram matrices before normalisation: w2.(L W_t), w2.(M W_t) (t < j), w2.L w2,
         // w2.M w2, w2.r
@@ -990,7 +1015,7 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
                     mt[t] = ok ? P.MW[size_t(t) * nf + i] : 0.0;
                     lt[t] = ok ? P.LW[size_t(t) * nf + i] : 0.0;
                 }
-                double x = a.w1[i], m = a.mw1[i], l = a.lw1[i];
+                double x = a.gram_cgs2 ? P.w[i] : a.w1[i], m = a.mw1[i], l = a.lw1[i];
                 const double rv = P.rf[i];
 #pragma unroll
                 for (int t = 0; t < KM; ++t) {
@@ -1189,6 +1214,7 @@ bool prec_coop_prepare(const PrecDev& P, int device, CoopBuffers& B) {
     B.ncmax = ncmax;
     B.tridiag = (P.eK.tri && P.eM.tri) ? 1 : 0;   // informational; each ElimDev carries its own flag
     B.nbc_max = (nb + P.ncomp - 1) / P.ncomp;
+    B.gram_cgs2 = getenv("DE_CGS2_TWO_PASS") ? 0 : 1;   // A/B switch: the literal two-pass CGS2
     return true;
 }
 
@@ -1214,6 +1240,7 @@ int prec_apply_coop(const PrecDev& P, const CoopBuffers& B, const double* r, dou
     a.mf = B.mf;
     a.ncmax = B.ncmax;
     a.tridiag = B.tridiag;
+    a.gram_cgs2 = B.gram_cgs2;
     a.timers = B.timers;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(B.nb);
