@@ -824,7 +824,10 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
     const int64_t lo = P.comp_off[c], hi = P.comp_off[c + 1];
     // row-parallel phases run on warps 1..CW-1 (RW rows per block chunk); warp 0 hosts the grid-barrier
     // thread and only joins the block reductions
-    const int64_t r0 = tid >= 32 ? lo + int64_t(lb) * RW + (tid - 32) : hi, rs = int64_t(nbc) * RW;
+    // 32-row warp chunks dealt warp-major over the component's blocks (chunk q = k*(CW-1)*nbc + (w-1)*nbc + lb),
+    // so expensive row ranges (the cross points at the end of each component, rows with more couplings) spread
+    // over many blocks instead of a few (measured: the block-contiguous layout left some blocks 1.4x the median)
+    const int64_t r0 = tid >= 32 ? lo + (int64_t(tid / 32 - 1) * nbc + lb) * 32 + (tid & 31) : hi, rs = int64_t(nbc) * RW;
     const int64_t nf = P.nflat;
     int pp = 0;
     double vals[KM + 2];
@@ -903,6 +906,7 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
         const bool dbg = TIM && a.timers && blockIdx.x == 0 && tid == 32 && j == 5;
 #define DBGT(k) do { if (dbg) a.timers[k] = gtimer(); } while (0)
         DBGT(120);
+        if (TIM && a.timers && j == 5 && tid == 32) a.timers[200 + 4096 + 1024 + blockIdx.x] = gtimer();   // A start
         const long long tA0 = clock64();
         ZERO_VALS();
         if (part)
@@ -928,6 +932,12 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
         if (TIM && a.timers && j == 5 && blockIdx.x < 4 && (tid & 31) == 0) a.timers[140 + blockIdx.x * CW + (tid >> 5)] = clock64() - tA0;
         block_partials(a, vals, 1 + KM, pp, c, lb, sred);
         DBGT(122);
+        if (TIM && a.timers && j == 5 && tid == 32) {
+            a.timers[200 + 4096 + 1536 + blockIdx.x] = gtimer();   // A arrival
+            unsigned sm;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+            a.timers[200 + 4096 + 2048 + blockIdx.x] = sm;
+        }
         grid.sync();
     __syncwarp();   // lane 0 spun in the barrier: reconverge before warp-synchronous code
     STAMP(stamp++);

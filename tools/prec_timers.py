@@ -41,3 +41,29 @@ slow = np.argsort(-f1all)[:12]
 print("slowest mode1 warps (gw, cycles, block, warp):", [(int(g), int(f1all[g]), int(g) // 8, int(g) % 8) for g in slow])
 f0all = np.array(list(t)[200:200 + 2368], dtype=np.float64)
 print("their mode0 cycles:", [int(f0all[g]) for g in slow])
+# phase A (Lanczos step 5) per block: start (after the E2 barrier) and arrival at the A barrier (globaltimer ns)
+st = np.array(list(t)[200 + 4096 + 1024:200 + 4096 + 1024 + 512], dtype=np.float64)
+ar = np.array(list(t)[200 + 4096 + 1536:200 + 4096 + 1536 + 512], dtype=np.float64)
+nbk = int((st > 0).sum())
+if nbk:
+    st, ar = st[:nbk], ar[:nbk]
+    t0 = st.min()
+    print("phaseA blocks", nbk, "start spread us", (st.max() - t0) / 1e3, "arrival min/p50/max us", (ar.min() - t0) / 1e3,
+          (np.median(ar) - t0) / 1e3, (ar.max() - t0) / 1e3)
+    late = np.argsort(-(ar - t0))[:12]
+    print("latest arrivals (block, start us, arrive us):", [(int(b), round((st[b] - t0) / 1e3, 2), round((ar[b] - t0) / 1e3, 2)) for b in late])
+    dur = (ar - st) / 1e3
+    print("A duration by component (even/odd blocks): mean", dur[0::2].mean(), dur[1::2].mean(), "max", dur[0::2].max(), dur[1::2].max())
+    early = np.argsort(st - t0)[-8:]
+    print("latest starts:", [(int(b), round((st[b] - t0) / 1e3, 2)) for b in early])
+sm = np.array(list(t)[200 + 4096 + 2048:200 + 4096 + 2048 + 512], dtype=np.int64)[:nbk]
+if nbk:
+    d = (ar - t0) / 1e3
+    bysm = {}
+    for b in range(nbk):
+        bysm.setdefault(int(sm[b]), []).append(d[b])
+    slow = sorted(bysm.items(), key=lambda kv: -max(kv[1]))[:10]
+    print("slowest SMs (smid: arrivals us):", [(k, [round(x, 1) for x in v]) for k, v in slow])
+    print("latest blocks' SMs:", [(int(b), int(sm[b])) for b in late])
+    s_ids = np.array(sorted(bysm)); mx = np.array([max(bysm[k]) for k in s_ids])
+    print("mean arrival by SM range 0-73 / 74-147:", mx[s_ids < 74].mean(), mx[s_ids >= 74].mean())
