@@ -635,7 +635,9 @@ __device__ int jacobi_reg(double* C, double* V, int n) {
         }
         off = warp_sum(off);
         dia = warp_sum(dia);
-        if (off <= 1e-30 * dia) break;
+        // converged when ||offdiag||_F <= 1e-12 ||diag||_F: eigenvector errors ~1e-12 relative, far inside the
+        // preconditioner's 1e-9 parity tolerance (one sweep fewer than 1e-15 on c5: 0.6469 -> 0.6428 ms)
+        if (off <= 1e-24 * dia) break;
         ++nsw;
         const double thr = 1e-15 * sqrt(dia);
         int rotated = 0;
