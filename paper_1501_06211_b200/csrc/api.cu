@@ -228,9 +228,9 @@ de_status_t schur_apply(de_ctx* c, const double* x, double* q) {
     return allreduce(c, q, size_t(c->hs.n_G));
 }
 
-de_status_t precond(de_ctx* c, const double* r, double* z, const PcgState* s, int* nl) {
+de_status_t precond(de_ctx* c, const double* r, double* z, const PcgState* s, int* nl, bool literal = false) {
     if (c->have_prec && c->use_coop) {
-        if (prec_apply_coop(c->P, c->coop, r, z, s, c->st) < 0) {
+        if (prec_apply_coop(c->P, c->coop, r, z, s, c->st, literal) < 0) {
             set_error("cooperative preconditioner launch failed: %s", cudaGetErrorString(cudaGetLastError()));
             return DE_ECUDA;
         }
@@ -666,6 +666,7 @@ de_status_t upload_prec_impl(de_ctx* c) {
         TRY(dalloc(c, &c->coop.w1, nf));
         TRY(dalloc(c, &c->coop.mw1, nf));
         TRY(dalloc(c, &c->coop.lw1, nf));
+        if (c->coop.fold) TRY(dalloc(c, &c->coop.ucross, size_t(KMAX) * std::max(1, P.eK.ncross)));
         if (getenv("DE_PREC_TIMERS")) {
             TRY(dalloc(c, &c->coop.timers, 200 + 8192));
             DE_CUDA(cudaMemsetAsync(c->coop.timers, 0, (200 + 8192) * sizeof(unsigned long long), c->st));
@@ -694,7 +695,7 @@ double elim_bytes_model(const HElim& E, bool tri) {
     return b;
 }
 
-double prec_bytes_model(const HostSetup& hs, int k, bool gram_cgs2) {
+double prec_bytes_model(const HostSetup& hs, int k, bool gram_cgs2, bool fold) {
     const double n = double(hs.comp_off[hs.ncomp]), nnz = double(hs.M.val.size()), d = 8.0;
     bool tri = true;
     for (const HElim* E : {&hs.elimK, &hs.elimM})
@@ -707,7 +708,7 @@ double prec_bytes_model(const HostSetup& hs, int k, bool gram_cgs2) {
     b += elim_bytes_model(hs.elimM, tri) + double(k - 1) * elim_bytes_model(hs.elimK, tri);
     b += spmv + n * d * 3;                                                  // seed: Ms, Ls, s.r
     for (int j = 1; j < k; ++j) {
-        b += spmv + n * d * (j + 2);                                        // A: M w, L w, W^T M w
+        b += spmv + n * d * (fold ? j + 1 : j + 2);   // A: M w, L w, h (fold: (M W)^T y in the elimination, R22)
         if (!gram_cgs2) b += n * d * (3.0 * j + 3 + 3);                     // B: w1, M w1, L w1 (two-pass)
         b += n * d * (3.0 * j + 4 + 3);                                     // C: w2, M w2, L w2, Gram row j
     }
@@ -959,7 +960,8 @@ de_status_t setup_impl(const de_mesh_t* mesh, const double* density, double E0, 
                     double(c->n_local_I + c->nsl) * 4.0;
     S.bytes_iter = fb + double(c->n_ig + c->n_gx) * 12.0 + double(c->n_local_G) * 8.0 * 3.0 +
                    double(hs.n_G) * 8.0 * 11.0;
-    S.bytes_prec = c->have_prec ? prec_bytes_model(hs, c->P.kmax, c->use_coop && c->coop.gram_cgs2) : 0.0;
+    S.bytes_prec = c->have_prec ? prec_bytes_model(hs, c->P.kmax, c->use_coop && c->coop.gram_cgs2,
+                                                   c->use_coop && c->coop.fold) : 0.0;
     return DE_OK;
 }
 
@@ -1067,7 +1069,9 @@ de_status_t true_residual(de_ctx* c, const double* d_f, const double* d_u, doubl
 de_status_t prec_full(de_ctx* c, const double* v, double* z) {
     HostSetup& hs = c->hs;
     launch_gather_gamma(c->d_gamma_dofs, v, c->fg_vG, hs.n_G, c->st);
-    TRY(precond(c, c->fg_vG, c->fg_zG, nullptr, nullptr));
+    // the literal two-pass CGS2 inside the preconditioner under FGMRES: measured, the one-pass form (R21) lets
+    // FGMRES on the paper problem (h = 1/32, N = 16) stall at 1.06e-8 (tests/test_fgmres_gpu.py)
+    TRY(precond(c, c->fg_vG, c->fg_zG, nullptr, nullptr, true));
     DE_CUDA(cudaMemsetAsync(z, 0, sizeof(double) * hs.ndof, c->st));
     launch_scatter_gamma(c->d_gamma_dofs, c->fg_zG, z, hs.n_G, c->st);
     launch_schur_local(schur_args(c, SCHUR_BACKSUB, c->fg_zG, v, z, nullptr), c->st);

@@ -353,7 +353,8 @@ void prec_prepare(const PrecDev& P);   // one-time kernel attributes (outside gr
 struct CoopBuffers {
     int nb = 0, nsm = 148;
     size_t smem = 0;
-    int stage = 0, per_warp = 0, mf = 0, ncmax = 0, nbc_max = 0, tridiag = 0, gram_cgs2 = 1;
+    int stage = 0, per_warp = 0, mf = 0, ncmax = 0, nbc_max = 0, tridiag = 0, gram_cgs2 = 1, fold = 0;
+    double* ucross = nullptr;   // fold: [KMAX][ncross of eK]
     double *red = nullptr, *gram = nullptr, *gram_tot = nullptr, *w1 = nullptr, *mw1 = nullptr, *lw1 = nullptr;
     unsigned long long* timers = nullptr;   // phase stamps (diagnostics; env DE_PREC_TIMERS=1)
     const void* kfn = nullptr;              // k_prec_coop instantiation (basis bound, timers)
@@ -362,6 +363,6 @@ bool prec_coop_prepare(const PrecDev& P, int device, CoopBuffers& B);
 size_t prec_coop_red_doubles(const CoopBuffers& B);
 size_t prec_coop_gram_doubles(const CoopBuffers& B);
 int prec_apply_coop(const PrecDev& P, const CoopBuffers& B, const double* r, double* z, const PcgState* s,
-                    cudaStream_t st);
+                    cudaStream_t st, bool literal = false);
 
 }  // namespace de

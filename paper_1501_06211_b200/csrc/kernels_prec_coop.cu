@@ -13,7 +13,8 @@
 // GEMV; the face correction x_F = y_F - G x_C is folded into the next phase) + phase A (M w, L w, dots h) +
 // phase C (w - W (2h - G h) with the images by linearity, ||w||_M, Gram row) = 4 barriers: the second
 // Gram-Schmidt pass is formed from the Gram matrix G = W^T M W (R21); env DE_CGS2_TWO_PASS runs the
-// literal two-pass form (phase B = pass 1 over the rows, phase C = pass 2) for A/B runs and tests.
+// literal two-pass form (phase B = pass 1 over the rows, phase C = pass 2) for A/B runs and tests. With the fold
+// (R22, 2D default) h is summed inside the elimination and phase A merges into C: 3 barriers per step.
 #include "de_internal.h"
 
 #include <cooperative_groups.h>
@@ -30,6 +31,7 @@ constexpr int NRED = KMAX + 2;
 constexpr int RW = CT - 32;                   // rows per block chunk in row-parallel phases
 constexpr int GW = 2 * KMAX + 1;              // Gram row j: G_L[j][t] (t<=j), G_M[j][t] (KMAX+t), (W^T r)[j] (2 KMAX)
 constexpr int GRAM_TASKS = KMAX * GW;
+constexpr int FOLD_OFF = 4096;                // dsm offset (doubles) of the fold's per-thread h accumulators
 
 struct CoopArgs {
     PrecDev P;
@@ -49,6 +51,8 @@ struct CoopArgs {
     int ncmax;          // max cross points per component
     int tridiag;        // 1: every face block is tridiagonal with <= TRI_MAX nodes (2D) -> thread per face
     int gram_cgs2;      // 1: the second Gram-Schmidt pass is formed from the Gram matrix (one row pass fewer)
+    int fold;           // 1 (with gram_cgs2, 2D fused eliminations): h = W^T M w is summed inside the elimination
+    double* ucross;     // [KMAX][ncross of eK]: u_t = G^T (M W_t)_F, the face part of M W_t folded onto cross points
     unsigned long long* timers;   // optional phase timestamps (block 0), DE_PREC_TIMERS
 };
 
@@ -403,9 +407,14 @@ __device__ __forceinline__ void face_warp_pcr(const PrecDev& P, const ElimDev& E
 }
 
 // x = X^-1 (scl * b) by exact elimination (faces -> cross points -> faces); 3 grid barriers.
+// fold_j > 0 (K-solve of Lanczos step fold_j, fused 2D path): the first phase also stores u_{j-1} = G^T b_F
+// (b = M W_{j-1} raw), and the second phase accumulates the block partials of h_t = (M W_t) . x for t < kc,
+// x = X^-1 (scl b) = y - G x_C (R22): h_t = sum_i MW_t[i] y_i + sum_k (MW_t[cf_k] - u_t[k]) x_C[k],
+// written to the reduction slots (pp, c, 1 + t) like block_partials.
 template <bool TIM>
 __device__ void elim_coop(cg::grid_group& grid, const CoopArgs& a, const ElimDev& E, const double* b,
-                          const double* scl, double* out, double* dsm, int c, int lb, int nbc, int& stamp) {
+                          const double* scl, double* out, double* dsm, int c, int lb, int nbc, int& stamp,
+                          int fold_j = 0, int kc = 0, int pp = 0, int64_t r0 = 0, int64_t rs = 1) {
     const PrecDev& P = a.P;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     // warp 0 hosts the grid-barrier thread; it comes out of every barrier late, so face solves run
@@ -456,6 +465,7 @@ __device__ void elim_coop(cg::grid_group& grid, const CoopArgs& a, const ElimDev
                     const double sgt = warp_sum(acc[u]);
                     if (lane == 0 && ci < E.ncross)
                         tCg[ci] = scl[ccomp(P.comp_off, P.ncomp, cf[u])] * (b[cf[u]] - sgt);
+                        if (fold_j > 0) a.ucross[size_t(fold_j - 1) * E.ncross + ci] = sgt;
                 }
             }
         }
@@ -565,11 +575,39 @@ __device__ void elim_coop(cg::grid_group& grid, const CoopArgs& a, const ElimDev
             if (dbg2) a.timers[182] = gtimer();
             __syncthreads();
             if (dbg2) a.timers[183] = gtimer();
+            double* hacc = dsm + FOLD_OFF;   // [KMAX][CT] per-thread h accumulators (fold)
+            if (fold_j > 0)
+                for (int t = 0; t < KMAX; ++t) hacc[t * CT + threadIdx.x] = 0.0;
             for (int r = rlo + threadIdx.x; r < rhi; r += CT) {
                 double acc = 0.0;
                 for (int q = 0; q < CW; ++q) acc += part[q * nr + (r - rlo)];
                 xC[base + r] = acc;
-                out[E.cross_flat[base + r]] = acc;
+                const int cf = E.cross_flat[base + r];
+                out[cf] = acc;
+                if (fold_j > 0)
+                    for (int t = 0; t < kc; ++t)
+                        hacc[t * CT + threadIdx.x] +=
+                            (P.MW[size_t(t) * P.nflat + cf] - a.ucross[size_t(t) * E.ncross + base + r]) * acc;
+            }
+            __syncthreads();
+        }
+        if (fold_j > 0) {
+            double* hacc = dsm + FOLD_OFF;
+            if (ncc <= 0)
+                for (int t = 0; t < KMAX; ++t) hacc[t * CT + threadIdx.x] = 0.0;
+            // face part: sum_i MW_t[i] y_i over this block's rows (y = 0 on cross rows)
+            for (int64_t i = r0; i < P.comp_off[c + 1]; i += rs) {
+                const double yi = y[i];
+                for (int t = 0; t < kc; ++t) hacc[t * CT + threadIdx.x] += P.MW[size_t(t) * P.nflat + i] * yi;
+            }
+            __syncthreads();
+            // block sums (fixed order) into the reduction slots (pp, c, 1 + t); slot 0 (unused) = 0
+            for (int v = w; v <= kc; v += CW) {
+                double t_ = 0.0;
+                if (v > 0)
+                    for (int q = 0; q < CW; ++q) t_ += hacc[(v - 1) * CT + q * 32 + lane];
+                t_ = warp_sum(t_);
+                if (lane == 0) a.red[((size_t(pp) * MAXC + c) * NRED + v) * a.nbc_max + lb] = t_;
             }
             __syncthreads();
         }
@@ -901,11 +939,19 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
     // ---- inverse Lanczos steps
     const bool fuseK = P.eK.tri && P.eK.fuse;
     for (int j = 1; j < P.kmax; ++j) {
-        elim_coop<TIM>(grid, a, P.eK, j == 1 ? P.MW : P.Mw, scl, P.w, dsm, c, lb, nbc, stamp);   // w = K^-1 M q_j
+        const bool fold = a.fold && fuseK;   // h summed inside the elimination (R22): no phase A, no barrier
+        elim_coop<TIM>(grid, a, P.eK, j == 1 ? P.MW : P.Mw, scl, P.w, dsm, c, lb, nbc, stamp,
+                       fold ? j : 0, kcs[c], pp, r0, rs);   // w = K^-1 M q_j
         const bool part = act[c] && !brk[c];
         const int kc = kcs[c];
-        // A: (M w, L w) by one SpMV over the shared pattern; ||w||_M^2 and h_t = W_t . M w
         const bool dbg = TIM && a.timers && blockIdx.x == 0 && tid == 32 && j == 5;
+        if (fold) {
+            read_totals(a, pp, 1 + kc, nb, tot);
+            pp ^= 1;
+            if (tid < KMAX) hsm[c][tid] = tid < kc ? tot[c][1 + tid] * sclh[c][tid] * sclh[c][tid] : 0.0;
+            __syncthreads();
+        } else {
+        // A: (M w, L w) by one SpMV over the shared pattern; ||w||_M^2 and h_t = W_t . M w
 #define DBGT(k) do { if (dbg) a.timers[k] = gtimer(); } while (0)
         DBGT(120);
         if (TIM && a.timers && j == 5 && tid == 32) a.timers[200 + 4096 + 1024 + blockIdx.x] = gtimer();   // A start
@@ -950,6 +996,7 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
         if (tid < nc) nb2v[tid] = tot[tid][0];
         if (tid < KMAX) hsm[c][tid] = tid < kc ? tot[c][1 + tid] * sclh[c][tid] * sclh[c][tid] : 0.0;
         __syncthreads();
+        }   // !fold
         if (a.gram_cgs2) {
             // second Gram-Schmidt pass from the Gram matrix (R21): h' = W^T M (w - W h) = h - G h with
             // G = W^T M W from the Gram rows 0..kc-1 (summed by now), so w2 = w - W (2h - G h) in one pass over the
@@ -1027,7 +1074,15 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
                     mt[t] = ok ? P.MW[size_t(t) * nf + i] : 0.0;
                     lt[t] = ok ? P.LW[size_t(t) * nf + i] : 0.0;
                 }
-                double x = a.gram_cgs2 ? P.w[i] : a.w1[i], m = a.mw1[i], l = a.lw1[i];
+                double x, m, l;
+                if (fold) {   // the former phase A on the same row: w_i and (M w)_i, (L w)_i by the fused SpMV
+                    x = spmv_elim(P.M, P.L, i, P.eK, P.y, P.y + nf, m, l);
+                    vals[1] += x * m;   // ||w||_M^2 before the orthogonalisation (breakdown test)
+                } else {
+                    x = a.gram_cgs2 ? P.w[i] : a.w1[i];
+                    m = a.mw1[i];
+                    l = a.lw1[i];
+                }
                 const double rv = P.rf[i];
 #pragma unroll
                 for (int t = 0; t < KM; ++t) {
@@ -1052,15 +1107,17 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
             }
         if (dbg) a.timers[111] = gtimer();
         if (part) gram_partials(a, gacc, c, lb, j);
-        block_partials(a, vals, 1, pp, c, lb, sred);
+        block_partials(a, vals, fold ? 2 : 1, pp, c, lb, sred);
         if (dbg) a.timers[112] = gtimer();
         grid.sync();
     __syncwarp();   // lane 0 spun in the barrier: reconverge before warp-synchronous code
     STAMP(stamp++);
         if (dbg) a.timers[113] = gtimer();
-        read_totals(a, pp, 1, nb, tot);
+        read_totals(a, pp, fold ? 2 : 1, nb, tot);
         if (dbg) a.timers[114] = gtimer();
         pp ^= 1;
+        if (fold && tid < nc) nb2v[tid] = tot[tid][1];
+        __syncthreads();
         if (tid < nc) {
             const bool pt = act[tid] && !brk[tid];
             const double na = sqrt(fmax(tot[tid][0], 0.0)), nbn = sqrt(fmax(nb2v[tid], 0.0));
@@ -1227,6 +1284,11 @@ bool prec_coop_prepare(const PrecDev& P, int device, CoopBuffers& B) {
     B.tridiag = (P.eK.tri && P.eM.tri) ? 1 : 0;   // informational; each ElimDev carries its own flag
     B.nbc_max = (nb + P.ncomp - 1) / P.ncomp;
     B.gram_cgs2 = getenv("DE_CGS2_TWO_PASS") ? 0 : 1;   // A/B switch: the literal two-pass CGS2
+    // fold h into the elimination (R22): 2D fused eliminations, one-pass Gram-Schmidt, room for the accumulators
+    B.fold = (B.gram_cgs2 && P.eK.tri && P.eK.fuse && !getenv("DE_NO_FOLD") &&
+              size_t(ncmax) + size_t(CW) * B.nbc_max + 2 <= size_t(FOLD_OFF) &&
+              (size_t(FOLD_OFF) + size_t(KMAX) * CT) * 8 <= B.smem) ? 1 : 0;
+    if (getenv("DE_VERBOSE")) fprintf(stderr, "[de] k_prec_coop: fold %d (R22)\n", B.fold);
     return true;
 }
 
@@ -1234,7 +1296,7 @@ size_t prec_coop_red_doubles(const CoopBuffers& B) { return size_t(2) * MAXC * N
 size_t prec_coop_gram_doubles(const CoopBuffers& B) { return size_t(MAXC) * GRAM_TASKS * B.nbc_max; }
 
 int prec_apply_coop(const PrecDev& P, const CoopBuffers& B, const double* r, double* z, const PcgState* s,
-                    cudaStream_t st) {
+                    cudaStream_t st, bool literal) {
     CoopArgs a{};
     a.P = P;
     a.r = r;
@@ -1252,7 +1314,9 @@ int prec_apply_coop(const PrecDev& P, const CoopBuffers& B, const double* r, dou
     a.mf = B.mf;
     a.ncmax = B.ncmax;
     a.tridiag = B.tridiag;
-    a.gram_cgs2 = B.gram_cgs2;
+    a.gram_cgs2 = literal ? 0 : B.gram_cgs2;   // literal: SPEC's two-pass CGS2 (used under FGMRES)
+    a.fold = literal ? 0 : B.fold;
+    a.ucross = B.ucross;
     a.timers = B.timers;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(B.nb);
