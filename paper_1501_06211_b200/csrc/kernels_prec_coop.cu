@@ -760,13 +760,18 @@ __device__ bool ritz_warp(const double* Ain, const double* Bin, const double* wr
         V[i * LDK + j] = (i == j) ? 1.0 : 0.0;
     }
     __syncwarp();
+    // rinv (the unused rot scratch) keeps 1/L_jj: the three triangular solves multiply instead of divide
+    double* rinv = rot;
     for (int j = 0; j < n; ++j) {
         const double d = R[j * LDK + j];
         if (!(d > 0.0)) return false;
-        const double l = sqrt(d);
+        const double il = rsqrt(d), l = d * il;
         __syncwarp();
-        if (lane == 0) R[j * LDK + j] = l;
-        if (lane > j && lane < n) R[lane * LDK + j] /= l;
+        if (lane == 0) {
+            R[j * LDK + j] = l;
+            rinv[j] = il;
+        }
+        if (lane > j && lane < n) R[lane * LDK + j] *= il;
         __syncwarp();
         for (int idx = lane; idx < (n - j - 1) * (n - j - 1); idx += 32) {
             const int i = j + 1 + idx / (n - j - 1), kk = j + 1 + idx % (n - j - 1);
@@ -778,14 +783,14 @@ __device__ bool ritz_warp(const double* Ain, const double* Bin, const double* wr
         for (int i = 0; i < n; ++i) {
             double t = C[i * LDK + lane];
             for (int kk = 0; kk < i; ++kk) t -= R[i * LDK + kk] * X[kk * LDK + lane];
-            X[i * LDK + lane] = t / R[i * LDK + i];
+            X[i * LDK + lane] = t * rinv[i];
         }
     __syncwarp();
     if (lane < n)
         for (int i = 0; i < n; ++i) {
             double t = X[lane * LDK + i];
             for (int kk = 0; kk < i; ++kk) t -= C[lane * LDK + kk] * R[i * LDK + kk];
-            C[lane * LDK + i] = t / R[i * LDK + i];
+            C[lane * LDK + i] = t * rinv[i];
         }
     __syncwarp();
     for (int idx = lane; idx < n * n; idx += 32) {
@@ -820,11 +825,13 @@ __device__ bool ritz_warp(const double* Ain, const double* Bin, const double* wr
     if (lane < n) {
         const double th = C[lane * LDK + lane];
         if (!sing && !(th > 0.0)) bad = 1;
-        const double f = sing ? 1.0 / (1.0 + pow(fmax(th, 0.0), 1.0 - theta)) : pow(th, theta - 1.0);
+        // theta = 1/2 (the paper's H_0.5): sqrt/rsqrt instead of the much longer pow sequence
+        const double f = theta == 0.5 ? (sing ? 1.0 / (1.0 + sqrt(fmax(th, 0.0))) : rsqrt(th))
+                                      : (sing ? 1.0 / (1.0 + pow(fmax(th, 0.0), 1.0 - theta)) : pow(th, theta - 1.0));
         for (int i = n - 1; i >= 0; --i) {
             double t = V[i * LDK + lane];
             for (int kk = i + 1; kk < n; ++kk) t -= R[kk * LDK + i] * X[kk * LDK + lane];
-            X[i * LDK + lane] = t / R[i * LDK + i];
+            X[i * LDK + lane] = t * rinv[i];
         }
         double t = 0.0;
         for (int i = 0; i < n; ++i) t += X[i * LDK + lane] * wr[i];
