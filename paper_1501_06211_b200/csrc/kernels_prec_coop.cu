@@ -689,12 +689,15 @@ __device__ int jacobi_reg(double* C, double* V, int n) {
             const double dq = __shfl_xor_sync(FULL, diag, 1);
             double cs = 1.0, sn = 0.0;
             if (even && lane < M && fabs(offp) > thr && fabs(offp) > 1e-300) {
-                // rotation zeroing C[p][q] (p = lane, q = lane + 1): t = tan of the angle, |t| <= 1
+                // rotation zeroing C[p][q] (p = lane, q = lane + 1), the small angle (|tan| <= 1):
+                // cos^2 = (1 + |d|/rt)/2, sin cos = sgn(d) apq/rt with rt = sqrt(d^2 + 4 apq^2) -- the same
+                // rotation as t = 2 apq/(d + sgn(d) rt), cs = 1/sqrt(1+t^2), in two rsqrt and no sqrt/divide
                 const double d = dq - diag, apq = offp;
-                const double rt = sqrt(d * d + 4.0 * apq * apq);
-                const double t = 2.0 * apq / (d >= 0.0 ? d + rt : d - rt);
-                cs = rsqrt(1.0 + t * t);
-                sn = t * cs;
+                const double ir = rsqrt(fma(d, d, 4.0 * apq * apq));
+                const double h = 0.5 * fma(fabs(d), ir, 1.0);
+                const double ih = rsqrt(h);
+                cs = h * ih;
+                sn = (d >= 0.0 ? apq : -apq) * ir * ih;
                 rotated = 1;
             }
             cs = __shfl_sync(FULL, cs, lane & ~1);
