@@ -463,9 +463,10 @@ __device__ void elim_coop(cg::grid_group& grid, const CoopArgs& a, const ElimDev
                 for (int u = 0; u < 2; ++u) {
                     const int ci = ci0 + u * nwarps;
                     const double sgt = warp_sum(acc[u]);
-                    if (lane == 0 && ci < E.ncross)
+                    if (lane == 0 && ci < E.ncross) {
                         tCg[ci] = scl[ccomp(P.comp_off, P.ncomp, cf[u])] * (b[cf[u]] - sgt);
                         if (fold_j > 0) a.ucross[size_t(fold_j - 1) * E.ncross + ci] = sgt;
+                    }
                 }
             }
         }
