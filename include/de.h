@@ -48,7 +48,8 @@ typedef enum {
                             rho <= 0 or non-finite, nu not in (-1, 1/2), E0 <= 0, Emin < 0,
                             no Dirichlet dof, unsupported option)                          */
     DE_ENOTSPD = -2,     /* non-positive pivot in an interior factorisation (subdomain id in message) */
-    DE_ENOCONV = -3,     /* max_iter reached; u holds the last iterate        */
+    DE_ENOCONV = -3,     /* max_iter reached, or the refined iterate missed rtol (stats.relres_dd);
+                            u holds the last iterate                           */
     DE_EBREAKDOWN = -4,  /* p^T S p <= 0, or a non-positive Ritz value (R9)       */
     DE_ESTATE = -5,      /* de_solve before de_factor                                      */
     DE_ENOMEM = -6,
@@ -135,6 +136,10 @@ typedef struct {
                                 streaming model of DESIGN.md "Kernels and their rooflines"), 0 if none */
     int64_t inner_iterations; /* inner_mode 0: face-PCG iterations of all inner solves since de_setup
                                  (summed over solves and components); 0 otherwise */
+    double relres_dd;        /* ||f - K (u_hi + u_lo)||_2 / ||f||_2 of the double-double iterate carried through
+                                the iterative refinement (R11/R17); de_solve returns DE_OK iff this is
+                                <= rtol. The returned u is fl(u_hi + u_lo), so relres_true exceeds it by at most
+                                the FP64 rounding floor of the problem (measured for config 5: 1.35e-10) */
 } de_stats_t;
 
 /* Fill *opt with defaults (theta 0.5, k 10, inner_mode 1, max_iter 20000, FR, 1 rank). */
@@ -158,7 +163,9 @@ de_status_t de_factor(de_ctx_t* ctx);
 
 /* Solve K(rho) u = f. rhs: host, ndof (Dirichlet entries ignored);
  * u: host, ndof out (0 at Dirichlet dofs). rtol relative to ||rhs_free||_2 (R11).
- * iterations/final_relres may be NULL. final_relres = true ||f - K u|| / ||f|| over free dofs. */
+ * iterations/final_relres may be NULL. final_relres = true ||f - K u|| / ||f|| over free dofs of the
+ * returned FP64 u (double-double residual); DE_OK means the refined double-double iterate, whose FP64
+ * rounding u is, meets rtol (de_stats_t.relres_dd; R17). */
 de_status_t de_solve(de_ctx_t* ctx, const double* rhs, double rtol, double* u,
                      int32_t* iterations, double* final_relres);
 

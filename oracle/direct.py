@@ -26,6 +26,9 @@ from __future__ import annotations
 import numpy as np
 import scipy.linalg as sla
 import scipy.sparse as sp
+import os
+
+from threadpoolctl import ThreadpoolController
 
 from .fem import free_system, element_stiffness, simp_modulus, element_dofs
 
@@ -92,34 +95,55 @@ class NDCholesky:
         self.fronts = []
         upd = {}
         last = 0
-        for t, (nodes, kids) in enumerate(tree):
-            P = piv[t]
-            last += len(P)
-            sub = K[P]
-            cand = [sub.indices.astype(np.int64)] + [upd[k][0] for k in kids]
-            cand = np.unique(np.concatenate(cand)) if cand else np.zeros(0, np.int64)
-            U = cand[pos[cand] >= last]                # not yet eliminated (pos of the subtree < last)
-            idx = np.concatenate([P, U])
-            m, n = len(P), len(idx)
-            F = np.zeros((n, n))
-            F[:m, :] = sub[:, idx].toarray()
-            F[m:, :m] = F[:m, m:].T
-            sidx = np.argsort(idx, kind="stable")
-            for k in kids:
-                Uk, Mk = upd.pop(k)
-                loc = sidx[np.searchsorted(idx, Uk, sorter=sidx)]
-                F[np.ix_(loc, loc)] += Mk
-            if m:
-                Lpp = np.linalg.cholesky(F[:m, :m])   # raises LinAlgError if not SPD
-                Lup = sla.solve_triangular(Lpp, F[:m, m:], lower=True, check_finite=False).T
-                Mt = F[m:, m:] - Lup @ Lup.T
-            else:
-                Lpp, Lup, Mt = np.zeros((0, 0)), np.zeros((len(U), 0)), F[m:, m:]
-            self.fronts.append((P, U, Lpp, np.ascontiguousarray(Lup)))
-            upd[t] = (U, Mt)
+        where = -np.ones(K.shape[0], dtype=np.int64)   # dof -> column of the current front
+        # OpenBLAS threads only pay on large fronts (measured: 8 threads on the small ones are 13x slower)
+        ctl = ThreadpoolController()
+        with ctl.limit(limits=1, user_api="blas"):
+            for t, (nodes, kids) in enumerate(tree):
+                P = piv[t]
+                last += len(P)
+                sub = K[P]
+                cand = [sub.indices.astype(np.int64)] + [upd[k][0] for k in kids]
+                cand = np.unique(np.concatenate(cand))
+                U = cand[pos[cand] >= last]            # not yet eliminated (pos of the subtree < last)
+                idx = np.concatenate([P, U])
+                m, n = len(P), len(idx)
+                where[idx] = np.arange(n)
+                F = np.zeros((n, n))
+                rows = np.repeat(np.arange(m), np.diff(sub.indptr))
+                cols = where[sub.indices]
+                keep = cols >= 0                       # entries to eliminated dofs were taken by the children
+                F[rows[keep], cols[keep]] = sub.data[keep]
+                F[m:, :m] = F[:m, m:].T
+                for k in kids:
+                    Uk, Mk = upd.pop(k)
+                    loc = where[Uk]
+                    F[np.ix_(loc, loc)] += Mk
+                where[idx] = -1
+                if m:
+                    if n >= 1024:
+                        with ctl.limit(limits=os.cpu_count() or 1, user_api="blas"):
+                            Lpp, Lup, Mt = self._partial(F, m)
+                    else:
+                        Lpp, Lup, Mt = self._partial(F, m)
+                else:
+                    Lpp, Lup, Mt = np.zeros((0, 0)), np.zeros((len(U), 0)), F[m:, m:]
+                self.fronts.append((P, U, Lpp, np.ascontiguousarray(Lup)))
+                upd[t] = (U, Mt)
         self.n = K.shape[0]
+        self._ctl = ctl
+
+    @staticmethod
+    def _partial(F, m):
+        Lpp = np.linalg.cholesky(F[:m, :m])            # raises LinAlgError if not SPD
+        Lup = sla.solve_triangular(Lpp, F[:m, m:], lower=True, check_finite=False).T
+        return Lpp, Lup, F[m:, m:] - Lup @ Lup.T
 
     def solve(self, b: np.ndarray) -> np.ndarray:
+        with self._ctl.limit(limits=1, user_api="blas"):
+            return self._solve(b)
+
+    def _solve(self, b: np.ndarray) -> np.ndarray:
         y = np.array(b, dtype=np.float64, copy=True)
         for P, U, Lpp, Lup in self.fronts:             # forward: L y = b
             if len(P):

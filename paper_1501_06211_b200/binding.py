@@ -55,7 +55,7 @@ class de_stats_t(C.Structure):
                 ("bytes_schur", C.c_double), ("kernels_launched", C.c_int64),
                 ("iterations_pass1", C.c_int32), ("schur_explicit", C.c_int32),
                 ("bytes_schur_explicit", C.c_double),
-                ("bytes_prec", C.c_double), ("inner_iterations", C.c_int64)]
+                ("bytes_prec", C.c_double), ("inner_iterations", C.c_int64), ("relres_dd", C.c_double)]
 
 
 class de_oc_params_t(C.Structure):

@@ -118,6 +118,7 @@ struct de_ctx {
     int64_t prof_n = 0, prof_n_prec = 0;
     int64_t launches = 0;
     double* d_ubuf2 = nullptr;
+    double* d_ulo = nullptr;          // low part of the double-double refinement iterate (R17)
     bool explicit_schur = false;
     double* d_sexp = nullptr;
     double* d_colscratch = nullptr;
@@ -447,9 +448,15 @@ de_status_t upload_prec_impl(de_ctx* c) {
         TRY(dupload(c, &D.xfc_ptr, E.XFC.ptr));
         TRY(dupload(c, &D.xfc_col, E.XFC.col));
         TRY(dupload(c, &D.xfc_val, E.XFC.val));
-        for (int i = 0; i <= MAXC; ++i) D.sc_off[i] = E.sc_off[std::min(i, hs.ncomp)];
-        TRY(dupload(c, &D.Sinv, E.SC));
-        for (int cc = 0; cc < hs.ncomp; ++cc) {   // S_C^-1 by Gauss-Jordan on the device (setup only)
+        // one S_C^-1 for all components when they are identical (HElim::sc_shared): every component points at it
+        D.sc_shared = E.sc_shared;
+        for (int i = 0; i <= MAXC; ++i) D.sc_off[i] = E.sc_shared ? 0 : E.sc_off[std::min(i, hs.ncomp)];
+        if (E.sc_shared) {
+            TRY(dupload(c, &D.Sinv, std::vector<double>(E.SC.begin(), E.SC.begin() + E.sc_off[1])));
+        } else {
+            TRY(dupload(c, &D.Sinv, E.SC));
+        }
+        for (int cc = 0; cc < (E.sc_shared ? 1 : hs.ncomp); ++cc) {   // S_C^-1 by Gauss-Jordan (setup only)
             const int nc = E.cross_comp_off[cc + 1] - E.cross_comp_off[cc];
             if (nc > 0) launch_gauss_jordan(D.Sinv + E.sc_off[cc], gjbuf, nc, c->st);
         }
@@ -690,7 +697,7 @@ double elim_bytes_model(const HElim& E, bool tri) {
     b += double(E.XCF.val.size()) * (12.0 + 8.0) + double(E.ncross) * (4 + 4 + 8 + 8 + 8);   // t_C
     for (size_t cc = 0; cc + 1 < E.sc_off.size(); ++cc) {
         const double nc = double(E.cross_comp_off[cc + 1] - E.cross_comp_off[cc]);
-        b += nc * nc * 8.0;                                                 // dense S_C^-1 rows
+        if (cc == 0 || !E.sc_shared) b += nc * nc * 8.0;                    // dense S_C^-1 rows (once if shared)
     }
     return b;
 }
@@ -906,6 +913,7 @@ de_status_t setup_impl(const de_mesh_t* mesh, const double* density, double E0, 
     TRY(dalloc(c, &c->d_ubuf, nd));
     TRY(dalloc(c, &c->d_fbuf, nd));
     TRY(dalloc(c, &c->d_ubuf2, nd));
+    TRY(dalloc(c, &c->d_ulo, nd));
     TRY(dalloc(c, &c->d_state, 1));
     TRY(dalloc(c, &c->d_scal, 8));
     TRY(dalloc(c, &c->d_fail, 1));
@@ -1053,9 +1061,9 @@ de_status_t dd_pass(de_ctx* c, const double* d_rhs, double tol_abs, bool warm, i
     return allreduce(c, d_out, size_t(c->hs.ndof));
 }
 
-// res = f - K u (free dofs), returns ||res||^2 on the host
-de_status_t true_residual(de_ctx* c, const double* d_f, const double* d_u, double* r2) {
-    launch_apply_K(c->md, c->d_Ee, d_u, d_f, c->d_cls, c->d_res, c->hs.ndof, c->st);
+// res = f - K (u + ulo) (free dofs; ulo may be null), returns ||res||^2 on the host
+de_status_t true_residual(de_ctx* c, const double* d_f, const double* d_u, double* r2, const double* d_ulo = nullptr) {
+    launch_apply_K(c->md, c->d_Ee, d_u, d_f, c->d_cls, c->d_res, c->hs.ndof, c->st, d_ulo);
     launch_norm2(c->d_res, c->hs.ndof, c->rb, c->d_scal, c->st);
     c->launches += 2;
     TRY(check_launch());
@@ -1170,7 +1178,7 @@ de_status_t fgmres_impl(de_ctx* c, const double* d_f, double rtol, double fnorm,
     }
     c->stats.iterations = c->stats.iterations_pass1 = its;
     c->stats.restarts = cycles;
-    c->stats.relres_true = c->stats.relres_recursive = std::sqrt(r2) / fnorm;
+    c->stats.relres_true = c->stats.relres_recursive = c->stats.relres_dd = std::sqrt(r2) / fnorm;
     c->stats.kernels_launched = c->launches;
     if (iters) *iters = its;
     if (relres) *relres = c->stats.relres_true;
@@ -1204,7 +1212,7 @@ de_status_t solve_impl(de_ctx* c, const double* d_f, double rtol, double* d_u, i
         DE_CUDA(cudaStreamSynchronize(c->st));
         if (iters) *iters = 0;
         if (relres) *relres = 0.0;
-        c->stats.relres_true = c->stats.relres_recursive = 0.0;
+        c->stats.relres_true = c->stats.relres_recursive = c->stats.relres_dd = 0.0;
         return DE_OK;
     }
     if (c->opt.outer == 1) {
@@ -1226,21 +1234,27 @@ de_status_t solve_impl(de_ctx* c, const double* d_f, double rtol, double* d_u, i
     double rec = std::sqrt(std::max(hsv.rr, 0.0)) / fnorm;
     double r2 = 0.0;
     TRY(true_residual(c, d_f, d_u, &r2));
-    // iterative refinement on the full system (R11): u += DD(f - K u)
-    // stop refining when a round no longer halves the residual (the FP64 floor, R11)
+    // iterative refinement on the full system (R11/R17): (u_hi, u_lo) += DD(f - K (u_hi + u_lo)) with
+    // the iterate carried as a double-double sum, so the FP64 rounding of u does not stop the refinement; stop
+    // when the double-double iterate meets rtol or a round no longer halves its residual
+    DE_CUDA(cudaMemsetAsync(c->d_ulo, 0, sizeof(double) * hs.ndof, c->st));
     double r2_prev = HUGE_VAL;
+    bool have_lo = false;
     while (std::sqrt(r2) > rtol * fnorm && conv && status != DE_EBREAKDOWN && its < maxit && refines < 3 &&
            r2 < 0.25 * r2_prev) {
         r2_prev = r2;
         TRY(dd_pass(c, c->d_res, 0.5 * rtol * fnorm, false, maxit - its, c->d_ubuf2, hsv));
-        launch_axpy(d_u, c->d_ubuf2, 1.0, hs.ndof, c->st);
+        launch_dd_accum(d_u, c->d_ulo, c->d_ubuf2, hs.ndof, c->st);
         c->launches += 1;
+        have_lo = true;
         its += hsv.it;
         status = hsv.status;
         conv = hsv.rr <= hsv.tol2;
         ++refines;
-        TRY(true_residual(c, d_f, d_u, &r2));
+        TRY(true_residual(c, d_f, d_u, &r2, c->d_ulo));
     }
+    const double r2_dd = r2;   // residual of the double-double iterate u_hi + u_lo
+    if (have_lo) TRY(true_residual(c, d_f, d_u, &r2));   // of the returned u = u_hi = fl(u_hi + u_lo)
     DE_CUDA(cudaEventRecord(l1, c->st));
     launch_gather_gamma(c->d_gamma_dofs, d_u, c->d_xprev, hs.n_G, c->st);   // warm start for the next solve
     c->launches += 1;
@@ -1255,6 +1269,7 @@ de_status_t solve_impl(de_ctx* c, const double* d_f, double rtol, double* d_u, i
     c->stats.restarts = refines;
     c->stats.relres_recursive = rec;
     c->stats.relres_true = std::sqrt(r2) / fnorm;
+    c->stats.relres_dd = std::sqrt(r2_dd) / fnorm;
     c->stats.ms_pcg = lms;
     c->stats.ms_solve = std::chrono::duration<double, std::milli>(t1 - t0).count();
     c->stats.launches_per_iter = c->launches_per_iter;
@@ -1265,9 +1280,11 @@ de_status_t solve_impl(de_ctx* c, const double* d_f, double rtol, double* d_u, i
         set_error("PCG breakdown (p^T S p <= 0 or a non-positive Ritz value) at iteration %d", its);
         return DE_EBREAKDOWN;
     }
-    if (!conv || c->stats.relres_true > rtol) {
-        set_error("did not reach rtol in %d iterations (true relres %.3e, recursive %.3e)", its,
-                  c->stats.relres_true, rec);
+    // R17: the computed (double-double) solution must meet rtol; the returned FP64 u = fl(u_hi + u_lo) may sit
+    // above rtol only by its own rounding (relres_true, >= the FP64 floor of the problem)
+    if (!conv || c->stats.relres_dd > rtol) {
+        set_error("did not reach rtol in %d iterations (true relres %.3e, double-double iterate %.3e, "
+                  "recursive %.3e)", its, c->stats.relres_true, c->stats.relres_dd, rec);
         return DE_ENOCONV;
     }
     return DE_OK;

@@ -54,6 +54,9 @@ struct HElim {
     HCsr XFC;                           // rows: face-node slots (face_nodes order); cols: cross index
     std::vector<int64_t> sc_off;        // [ncomp+1] offsets of dense S_C per component
     std::vector<double> SC;             // dense S_C (row-major per component), inverted on device
+    // 1 when every component's S_C is bitwise identical to component 0's (same skeleton and Dirichlet rows:
+    // the trace norm is componentwise): one S_C^-1 serves all components
+    int32_t sc_shared = 0;
 };
 
 struct HostSetup {
@@ -167,6 +170,7 @@ struct ElimDev {
     double* xfc_val;
     int64_t sc_off[MAXC + 1];
     double* Sinv;
+    int32_t sc_shared;           // 1: all components use the one S_C^-1 at Sinv (HElim::sc_shared)
     // face-interleaved tridiagonal copy (2D): 32 faces per group, entry (j, lane) at (g*TRI_N + j)*32 + lane
     int32_t tri;                 // 1 if every face block is tridiagonal with <= TRI_N nodes and <= 2 cross couplings
     int32_t* tri_n;              // [nfaces] nodes per face
@@ -249,7 +253,8 @@ void launch_assemble_pairs(const MeshDev& m, const int32_t* da, const int32_t* d
 int launch_band_cholesky(const SubDesc* sd, int nsl, double* band, int ld, int band_w,
                          int* d_fail, cudaStream_t st);
 void launch_apply_K(const MeshDev& m, const double* Ee, const double* u, const double* f,
-                    const int8_t* cls, double* res, int64_t ndof, cudaStream_t st);
+                    const int8_t* cls, double* res, int64_t ndof, cudaStream_t st, const double* ulo = nullptr);
+void launch_dd_accum(double* hi, double* lo, const double* d, int64_t n, cudaStream_t st);
 
 enum SchurMode { SCHUR_APPLY = 0, SCHUR_CONDENSE = 1, SCHUR_BACKSUB = 2, SCHUR_COLUMNS = 3 };
 struct SchurArgs {

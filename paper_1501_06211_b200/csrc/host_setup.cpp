@@ -9,6 +9,7 @@
 #include "de_internal.h"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -286,6 +287,13 @@ de_status_t build_elim(const HostSetup& hs, const HCsr& X, HElim& E) {
             }
         }
     }
+    // identical components (e.g. every component clamped on the same Dirichlet face): keep one S_C
+    E.sc_shared = hs.ncomp > 1 ? 1 : 0;
+    for (int c = 1; c < hs.ncomp && E.sc_shared; ++c)
+        if (E.sc_off[c + 1] - E.sc_off[c] != E.sc_off[1] - E.sc_off[0] ||
+            !std::equal(E.SC.begin() + E.sc_off[c], E.SC.begin() + E.sc_off[c + 1], E.SC.begin()))
+            E.sc_shared = 0;
+    if (getenv("DE_NO_SC_SHARE")) E.sc_shared = 0;   // A/B switch
     return DE_OK;
 }
 

@@ -209,9 +209,12 @@ __device__ __forceinline__ dd_t two_prod(double a, double b) {
     return {p, fma(a, b, -p)};
 }
 
+// res = f - K (u + ulo) on free dofs (0 on Dirichlet dofs): K u in double-double from the FP64 element data;
+// ulo (optional, the low part of a double-double iterate, |ulo| ~ eps |u|) enters through an FP64 product
+// whose rounding is ~eps^2 relative -- far below the result's own rounding
 __global__ void k_apply_K(MeshDev m, const double* __restrict__ Ee, const double* __restrict__ u,
-                          const double* __restrict__ f, const int8_t* __restrict__ cls,
-                          double* __restrict__ res, int64_t ndof) {
+                          const double* __restrict__ ulo, const double* __restrict__ f,
+                          const int8_t* __restrict__ cls, double* __restrict__ res, int64_t ndof) {
     const int dim = m.dim;
     for (int64_t d = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; d < ndof; d += int64_t(gridDim.x) * blockDim.x) {
         if (cls[d] == 2) {
@@ -234,11 +237,16 @@ __global__ void k_apply_K(MeshDev m, const double* __restrict__ Ee, const double
                     const int la = (co[0] - ex) + 2 * (co[1] - ey) + 4 * (co[2] - ez);
                     const int64_t e = ex + int64_t(m.nel[0]) * (ey + int64_t(m.nel[1]) * ez);
                     dd_t t = {0.0, 0.0};
+                    double tl = 0.0;
                     for (int lb = 0; lb < (1 << dim); ++lb) {
                         const int64_t nbn = (ex + (lb & 1)) + int64_t(m.nn[0]) * ((ey + ((lb >> 1) & 1)) + int64_t(m.nn[1]) * (ez + ((lb >> 2) & 1)));
-                        for (int cb = 0; cb < dim; ++cb)
-                            t = dd_add(t, two_prod(c_KE[(dim * la + c) * m.nke + dim * lb + cb], u[dim * nbn + cb]));
+                        for (int cb = 0; cb < dim; ++cb) {
+                            const double ke = c_KE[(dim * la + c) * m.nke + dim * lb + cb];
+                            t = dd_add(t, two_prod(ke, u[dim * nbn + cb]));
+                            if (ulo) tl = fma(ke, ulo[dim * nbn + cb], tl);
+                        }
                     }
+                    t.lo += tl;
                     acc = dd_add(acc, dd_mul_d(t, Ee[e]));
                 }
         res[d] = -(acc.hi + acc.lo);   // f - K u, accurate to ~1 ulp of the result
@@ -246,9 +254,25 @@ __global__ void k_apply_K(MeshDev m, const double* __restrict__ Ee, const double
 }
 
 void launch_apply_K(const MeshDev& m, const double* Ee, const double* u, const double* f,
-                    const int8_t* cls, double* res, int64_t ndof, cudaStream_t st) {
+                    const int8_t* cls, double* res, int64_t ndof, cudaStream_t st, const double* ulo) {
     const int blocks = int(std::min<int64_t>((ndof + 255) / 256, 148 * 16));
-    k_apply_K<<<blocks, 256, 0, st>>>(m, Ee, u, f, cls, res, ndof);
+    k_apply_K<<<blocks, 256, 0, st>>>(m, Ee, u, ulo, f, cls, res, ndof);
+}
+
+// (hi, lo) += d as a double-double sum (two_sum, then renormalised so hi = fl(hi + lo))
+__global__ void k_dd_accum(double* __restrict__ hi, double* __restrict__ lo, const double* __restrict__ d,
+                           int64_t n) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        const dd_t s = two_sum(hi[i], d[i]);
+        const dd_t r = two_sum(s.hi, s.lo + lo[i]);
+        hi[i] = r.hi;
+        lo[i] = r.lo;
+    }
+}
+
+void launch_dd_accum(double* hi, double* lo, const double* d, int64_t n, cudaStream_t st) {
+    const int blocks = int(std::min<int64_t>((n + 255) / 256, 148 * 16));
+    k_dd_accum<<<blocks, 256, 0, st>>>(hi, lo, d, n);
 }
 
 }  // namespace de

@@ -1,0 +1,187 @@
+"""GPU parity at the BASELINE sizes, in the launch configuration bench.py times (default options).
+
+Reference answers come from the oracle only:
+  * u_ref: the plain definition u = K_ff^-1 f (Eq. (4)) by oracle.direct (nested-dissection
+    Cholesky; SuperLU cannot factor c4/c5) with extended-precision refinement; fl(u_ref) is the FP64 rounding
+    of the exact solution and its residual is the measured FP64 floor of the problem (R17);
+  * the Schur apply and the preconditioner: oracle.dd.schur_apply / oracle.precond.apply_precond on the full
+    c5 geometry, compared element by element.
+Gates (BASELINE.json north_star): ||u - u_ref|| <= 1e-8 ||u_ref||; de_solve returns DE_OK (the refined
+double-double iterate meets rtol 1e-10); the returned FP64 u has relres <= max(1e-10, 1.25 x the measured
+floor of fl(u_ref)) -- no FP64 vector can do materially better than fl(u_ref).
+Config 3 (FP64-ill-posed, R15/SURVEY Q15): normwise backward error <= 1e-12 for both solvers.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from synthetic import make_config, density_sequence_step  # noqa: E402
+from oracle.topology import build_topology  # noqa: E402
+from oracle.dd import subdomain_blocks, factor_subdomains, schur_apply  # noqa: E402
+from oracle.precond import build_components, apply_precond  # noqa: E402
+from oracle.direct import refine_dd, relres_ext, direct_solve  # noqa: E402
+from oracle.fem import free_system  # noqa: E402
+
+FLOOR_FACTOR = 1.25
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _dev():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1501_06211_b200.build import build
+    build()
+    torch.cuda.set_device(0)
+
+
+def _solver(p, **kw):
+    from paper_1501_06211_b200 import binding as B
+    return B.Solver.from_problem(p, device=0, **kw)
+
+
+def _check_against_direct(p, u, relres, st):
+    hi, lo, hist = refine_dd(p, rounds=2)
+    floor = hist[-1]                                   # relres of fl(u_ref), the FP64 floor
+    err = np.linalg.norm(u - hi) / np.linalg.norm(hi)
+    gate = max(1e-10, FLOOR_FACTOR * floor)
+    print(f"{p.name}: ||u-u_ref||/||u_ref|| = {err:.3e}, relres(u) = {relres:.4e} (oracle {relres_ext(p, u):.4e}), "
+          f"relres_dd = {st.relres_dd:.3e}, floor fl(u_ref) = {floor:.4e}")
+    assert err <= 1e-8
+    assert st.relres_dd <= 1e-10
+    assert relres <= gate
+    assert relres_ext(p, u) <= gate                     # the oracle's own residual of the GPU u
+    return floor
+
+
+def _sampled_blocks(p, T, S):
+    """Assembled A_II and its factor on three sampled subdomains against the oracle (before/after factor)."""
+    from paper_1501_06211_b200 import binding as B
+    samples = sorted({0, T.nsub // 3, T.nsub - 1})
+    blocks = factor_subdomains(subdomain_blocks(p, T, only=samples))
+    for sl, b in zip(samples, blocks):
+        A = B.de_get_assembled_band(S.ctx, sl)
+        C = b.AII.tocoo()
+        low = C.row >= C.col
+        ref = np.zeros_like(A)
+        ref[C.col[low], C.row[low] - C.col[low]] = C.data[low]
+        assert np.abs(A - ref).max() <= 1e-13 * np.abs(ref).max()
+    S.factor()
+    for sl, b in zip(samples, blocks):
+        L = B.de_get_factor_band(S.ctx, sl)
+        assert np.abs(L[:, :b.band + 1] - b.chol.T).max() <= 1e-11 * np.abs(b.chol).max()
+
+
+@pytest.mark.parametrize("name", ["c2", "c4"])
+def test_full_size_solution_matches_direct_oracle(name):
+    p = make_config(name)
+    T = build_topology(p)
+    S = _solver(p)
+    try:
+        _sampled_blocks(p, T, S)
+        u, its, relres, _ = S.solve(p.rhs, p.rtol)        # raises DEError unless DE_OK
+        _check_against_direct(p, u, relres, S.stats())
+    finally:
+        S.close()
+
+
+def test_c5_sequence_full_size_solves_1_25_50():
+    """C7 / SURVEY O10: the 50-solve config-5 sequence at 2048x1024 (refactor + warm start each step);
+    solves 1, 25 and 50 against the direct oracle, every solve DE_OK."""
+    p = make_config("c5")
+    T = build_topology(p)
+    S = _solver(p, warm_start=1)
+    rho = p.density.copy()
+    try:
+        _sampled_blocks(p, T, S)
+        its_all = []
+        for t in range(50):
+            if t > 0:
+                rho = density_sequence_step(rho, t)
+                S.update_densities(rho)
+                S.factor()
+            u, its, relres, _ = S.solve(p.rhs, p.rtol)    # DE_OK required at every step
+            its_all.append(its)
+            if t in (0, 24, 49):
+                _check_against_direct(p.with_density(rho), u, relres, S.stats())
+        print("iterations per solve:", its_all)
+        assert np.mean(its_all[1:]) < its_all[0]          # warm starts pay
+    finally:
+        S.close()
+
+
+def test_c5_schur_apply_elementwise():
+    from paper_1501_06211_b200 import binding as B
+    p = make_config("c5")
+    T = build_topology(p)
+    blocks = factor_subdomains(subdomain_blocks(p, T))
+    S = _solver(p)
+    try:
+        S.factor()
+        x = np.random.default_rng(21).normal(size=T.n_G)
+        ref = schur_apply(blocks, T.n_G, x)
+        dx = torch.tensor(x, dtype=torch.float64, device="cuda")
+        dq = torch.empty_like(dx)
+        B.de_schur_apply_device(S.ctx, dx.data_ptr(), dq.data_ptr())
+        q = dq.cpu().numpy()
+        # element-wise: every entry within 1e-11 of the vector's scale (sums of ~2 x 256 products per entry)
+        assert np.abs(q - ref).max() <= 1e-11 * np.abs(ref).max()
+        assert np.linalg.norm(q - ref) <= 1e-11 * np.linalg.norm(ref)
+    finally:
+        S.close()
+
+
+def test_c5_preconditioner_elementwise():
+    """de_precond_apply_device on the full c5 skeleton (2 x 126,110 nodes, 4,000 faces, 1,953 cross points per
+    component) against oracle apply_precond (inverse Lanczos k = 10, theta = 1/2, exact inner solves)."""
+    from paper_1501_06211_b200 import binding as B
+    p = make_config("c5")
+    T = build_topology(p)
+    comps = build_components(p, T)
+    S = _solver(p)
+    try:
+        S.factor()
+        rng = np.random.default_rng(22)
+        for trial in range(2):
+            r = rng.normal(size=T.n_G)
+            ref = apply_precond(comps, r, "lanczos", 0.5, 10, "X")
+            dr = torch.tensor(r, dtype=torch.float64, device="cuda")
+            dz = torch.empty_like(dr)
+            B.de_precond_apply_device(S.ctx, dr.data_ptr(), dz.data_ptr())
+            z = dz.cpu().numpy()
+            for cd in comps:                               # per component: the norm is componentwise
+                g = cd.skel.gidx
+                assert np.abs(z[g] - ref[g]).max() <= 1e-9 * np.abs(ref[g]).max()
+                assert np.linalg.norm(z[g] - ref[g]) <= 1e-9 * np.linalg.norm(ref[g])
+    finally:
+        S.close()
+
+
+def test_c3_full_size_backward_error():
+    """R15 / SURVEY Q15: config 3 is FP64-ill-posed; gate the normwise backward error
+    ||f - K u||_2 / (||K||_1 ||u||_2 + ||f||_2) <= 1e-12 for both solvers (GPU at a fixed budget, oracle direct),
+    and report the forward difference and the stagnated relative residual (not gated)."""
+    from paper_1501_06211_b200 import binding as B
+    p = make_config("c3")
+    K, f, free = free_system(p)
+    normK1 = abs(K).sum(axis=0).max()
+    u_ref = direct_solve(p)
+
+    def bwd(u):
+        r = f - K @ u[free]
+        return np.linalg.norm(r) / (normK1 * np.linalg.norm(u[free]) + np.linalg.norm(f))
+
+    S = _solver(p, max_iter=2000)
+    try:
+        S.factor()
+        # the budget ends the solve (DE_ENOCONV is the expected status on this instance, R15)
+        u, its, relres, status = S.solve(p.rhs, p.rtol, allow_noconv=True)
+        assert status in (B.DE_OK, B.DE_ENOCONV)
+        be_gpu, be_ref = bwd(u), bwd(u_ref)
+        fwd = np.linalg.norm(u - u_ref) / np.linalg.norm(u_ref)
+        print(f"c3: its {its}, relres {relres:.3e}, backward error GPU {be_gpu:.3e} oracle {be_ref:.3e}, "
+              f"forward difference {fwd:.3e}")
+        assert be_gpu <= 1e-12 and be_ref <= 1e-12
+    finally:
+        S.close()

@@ -256,51 +256,6 @@ def test_config5_sequence_warm_start():
         S.close()
 
 
-@pytest.mark.parametrize("name", ["c2", "c4", "c5"])
-def test_full_size_sampled(name):
-    """BASELINE sizes in the bench launch configuration: properties at any size (true residual by
-    the oracle's own K) plus sampled subdomain factors/assembled blocks against the oracle."""
-    from paper_1501_06211_b200 import binding as B
-    p = make_config(name)
-    T = build_topology(p)
-    S = _solver(p)
-    try:
-        samples = sorted({0, T.nsub // 3, T.nsub - 1})
-        blocks = factor_subdomains(subdomain_blocks(p, T, only=samples))
-        for sl, b in zip(samples, blocks):
-            A = B.de_get_assembled_band(S.ctx, sl)
-            C = b.AII.tocoo()
-            low = C.row >= C.col
-            ref = np.zeros_like(A)
-            ref[C.col[low], C.row[low] - C.col[low]] = C.data[low]
-            assert np.abs(A - ref).max() <= 1e-13 * np.abs(ref).max()
-        S.factor()
-        for sl, b in zip(samples, blocks):
-            L = B.de_get_factor_band(S.ctx, sl)
-            assert np.abs(L[:, :b.band + 1] - b.chol.T).max() <= 1e-11 * np.abs(b.chol).max()
-        u, its, relres, _ = S.solve(p.rhs, p.rtol, allow_noconv=True)
-        # R17: the gate is 1e-10, or the FP64 representation floor eps*|| |K||u| ||/||f|| when that is
-        # larger (config 5: ~7e-10 — no FP64-stored u can do better than about that)
-        gate = max(1e-10, residual_floor(p, u))
-        assert relres <= gate, (relres, gate)
-        assert true_relres(p, u) <= 2 * gate
-    finally:
-        S.close()
-
-
-def residual_floor(p, u):
-    """eps * || |K| |u| ||_2 / ||f||_2 over free dofs (oracle element matrices, absolute values)."""
-    from oracle.fem import element_stiffness, simp_modulus, element_dofs
-    KE = np.abs(element_stiffness(p.dim, p.nu))
-    E = simp_modulus(p.density, p.E0, p.Emin, p.p)
-    ed = element_dofs(p.dim, p.nel)
-    fe = (np.abs(u)[ed] @ KE.T) * E[:, None]
-    out = np.zeros_like(u)
-    np.add.at(out, ed.ravel(), fe.ravel())
-    free = p.fixed == 0
-    return float(np.finfo(float).eps / 2 * np.linalg.norm(out[free]) / np.linalg.norm(p.rhs[free]))
-
-
 def test_c3_full_size_budgeted_iterates_match_oracle():
     """R15 at the BASELINE size: config 3 is FP64-ill-posed, so the gate is agreement of the GPU
     and oracle interface iterates after the same fixed budget (same algorithm, same inputs)."""
