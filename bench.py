@@ -100,71 +100,91 @@ def density_schedule(prob, n):
 
 # --------------------------------------------------------------------------- oracle (CPU) leg
 
-def cpu_baseline(prob, gpu_iters, budget_s=20.0):
-    """The oracle as it stands, on a bounded sample of the same workload: per-iteration cost
-    (Schur apply over a subset of subdomains, scaled to all; one full preconditioner
-    application; PCG vector work) and per-step factorisation cost (same subset, scaled)."""
-    from oracle.topology import build_topology
-    from oracle.dd import subdomain_blocks, factor_subdomains, local_schur_apply
-    from oracle.precond import build_components, apply_precond
-    topo = build_topology(prob)
-    ns = min(topo.nsub, 64)
-    sample = list(np.linspace(0, topo.nsub - 1, ns).astype(int))
-    t0 = time.perf_counter()
-    blocks = factor_subdomains(subdomain_blocks(prob, topo, only=sample))
-    t_fac = (time.perf_counter() - t0) * topo.nsub / ns
-    rng = np.random.default_rng(0)
-    x = rng.normal(size=topo.n_G)
-    reps, t_s = 0, 0.0
-    while t_s < budget_s * 0.3 or reps < 1:
-        t0 = time.perf_counter()
-        for b in blocks:
-            local_schur_apply(b, x[b.R])
-        t_s += time.perf_counter() - t0
-        reps += 1
-    t_schur = t_s / reps * topo.nsub / ns
-    comps = build_components(prob, topo)
-    apply_precond(comps, x, "lanczos", 0.5, 10, "X")       # factorises the skeleton operators once
-    reps, t_p = 0, 0.0
-    while t_p < budget_s * 0.2 or reps < 1:
-        t0 = time.perf_counter()
-        apply_precond(comps, x, "lanczos", 0.5, 10, "X")
-        t_p += time.perf_counter() - t0
-        reps += 1
-    t_prec = t_p / reps
-    t_iter = t_schur + t_prec
-    iters = max(1, gpu_iters)
-    step = t_fac + iters * t_iter
-    value = prob.ndof and (topo.n_I + topo.n_G) * iters / step / 1e6
-    return {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"{ns}/{topo.nsub} subdomains (Schur apply + banded factorisation, scaled x{topo.nsub / ns:.0f}) "
-                      f"+ full preconditioner application; step = factor + {iters} iterations (GPU count); "
-                      f"t_iter={t_iter:.3f}s t_factor={t_fac:.2f}s; numpy/scipy single thread, host cpus={os.cpu_count()}",
-            "s_per_iter": t_iter, "s_factor": t_fac}
+WORKLOADS = {
+    "c5": "c5: BASELINE config 5 step (2048x1024 Q1 plane stress, 64x32 subdomains of 32x32, SIMP p=3, "
+          "density update -> refactor -> warm PCG rtol 1e-10)",
+    "c4": "c4: BASELINE config 4 (3D Q1 hex 96x48x48, 8x4x4 subdomains of 12^3, SIMP p=3) as a sequence step "
+          "(density update -> refactor -> warm PCG rtol 1e-10)",
+}
+L2_NOTE = {"c5": "inputs larger than L2 (factor bands 2.15 GB, explicit S_s 0.56 GB per step vs 126 MB L2)",
+           "c4": "inputs larger than L2 (factor bands 1.92 GB vs 126 MB L2)"}
+
+
+def workload_config(name, n_free, n_gamma, nsub, gpus):
+    """The `config` object of both arms (identical keys and values for the same workload)."""
+    return {"workload": WORKLOADS.get(name, name), "n_free": int(n_free), "n_gamma": int(n_gamma),
+            "subdomains": int(nsub), "preconditioner": "inverse Lanczos k=10, theta=0.5, exact inner solves (R10)",
+            "l2": L2_NOTE.get(name, "see DESIGN.md"), "parallelism": f"subdomain slabs x{gpus}"}
+
+
+def gpu_iterations_per_step(name):
+    """The GPU's iterations per step of this workload, from the committed bench line (profiles/), so the oracle
+    arm extrapolates to the same step; 600 when none is recorded."""
+    for f in ("round2_bench_%s.json" % name, "round1_bench_%s.json" % name):
+        try:
+            return int(round(json.load(open(os.path.join(ROOT, "profiles", f)))["iterations_per_step"]))
+        except Exception:
+            pass
+    return 600
+
+
+def cpu_baseline(prob, gpu_iters):
+    """The oracle as it stands on all host cores (bench_oracle.py): median of 3 measured samples of
+    (factorisation of all subdomains, full PCG iterations), step extrapolated to the GPU's iteration count."""
+    import bench_oracle as BO
+    m = BO.measure(prob, gpu_iters)
+    return {"value": m["value"], "unit": UNIT, "cores": m["workers"], "kind": "oracle", "sample": m["sample"]}
 
 
 def run_reference(args):
+    """--impl reference: the oracle (oracle/) on the host cores, on the native arm's workload, metric and unit.
+    Each step is one measured bounded sample (factorisation of all subdomains + 3 full PCG iterations on all
+    cores); value is the step of the workload (factor + the GPU's iteration count) extrapolated from the median
+    sample parts. Under torchrun only rank 0 runs."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
+    import bench_oracle as BO
     from synthetic import make_config
     prob = make_config(args.config)
-    n_free = int(np.sum(prob.fixed == 0))
-    gpu_iters = 900 if args.config == "c5" else 200
-    cb = cpu_baseline(prob, gpu_iters, budget_s=8.0)
-    steps = []
-    for _ in range(args.warmup + args.steps):
-        steps.append(cb["s_factor"] + gpu_iters * cb["s_per_iter"])
-    ms = 1e3 * float(np.mean(steps[args.warmup:]))
-    line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{args.config} (BASELINE config 5: 2048x1024 Q1, 64x32 subdomains, "
-                                   "density-sequence step)"},
-            "cpu_baseline": cb, "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
-                                        "d2h_bytes_per_step": 0},
-            "note": "oracle (oracle/) on host cores; bounded sample per step, scaled as stated in cpu_baseline.sample"}
-    print(json.dumps(line))
+    gpu_iters = gpu_iterations_per_step(args.config)
+    pool = BO.OraclePool(prob)
+    try:
+        pool.factor()
+        pool.pcg_iterations(1)
+        tf, ti, samples = [], [], []
+        for t in range(args.warmup + args.steps):
+            ta = time.perf_counter()
+            f = pool.factor()
+            i = pool.pcg_iterations(3, seed=t)
+            if t >= args.warmup:
+                tf.append(f)
+                ti.append(i)
+                samples.append(time.perf_counter() - ta)
+        topo = pool.topo
+        t_factor, t_iter = statistics.median(tf), statistics.median(ti)
+        n_free = int(np.sum(prob.fixed == 0))
+        step_s = t_factor + gpu_iters * t_iter
+        value = n_free * gpu_iters / step_s / 1e6
+        cores = pool.nw
+        sample = (f"each step = one measured sample on {pool.nw} worker processes (+{len(pool.comps)} preconditioner "
+                  f"workers; 1 BLAS thread each; os.cpu_count()={os.cpu_count()}): factorisation of all {topo.nsub} "
+                  f"subdomains (median {t_factor:.3f}s) + 3 full PCG iterations (median {t_iter:.4f}s/iteration); "
+                  f"value = the workload step (factor + {gpu_iters} iterations, the GPU's count) EXTRAPOLATED from "
+                  f"those medians = {step_s:.1f}s")
+        line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(samples)),
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic",
+                "config": workload_config(args.config, n_free, topo.n_G, topo.nsub, args.gpus),
+                "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+                "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+                "extrapolated_ms_per_workload_step": 1e3 * step_s, "gpu_iterations_per_step": gpu_iters,
+                "note": "oracle (oracle/) on host cores; ms_per_step is the measured sample, value the extrapolated "
+                        "workload step (cpu_baseline.sample)"}
+        print(json.dumps(line))
+    finally:
+        pool.close()
     return 0
 
 
@@ -226,21 +246,21 @@ def main():
     for t in range(args.warmup):                    # untimed warm-up (graph build, caches)
         step(t)
     torch.cuda.synchronize()
-    B.de_set_profiling(ctx, True)
     clocks = ClockSampler(local)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     clocks.start()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    its_tot, rel_max, reldd_max, launches = 0, 0.0, 0.0, 0
-    e0.record(stream)
+    its_tot, rel_max, reldd_max, launches, ms_pcg = 0, 0.0, 0.0, 0, 0.0
+    e0.record(stream)                               # timed region: profiling (event nodes) off
     for t in range(args.warmup, nsteps):
         its, rel = step(t)
         its_tot += its
         rel_max = max(rel_max, rel)
         st_ = solver.stats()
         reldd_max = max(reldd_max, st_.relres_dd)
+        ms_pcg += st_.ms_pcg
         launches += st_.kernels_launched + 5        # + factor kernels
     e1.record(stream)
     torch.cuda.synchronize()
@@ -252,12 +272,20 @@ def main():
         tt = torch.tensor([ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
-    k_ms, k_n = B.de_get_kernel_time(ctx)
-    p_ms, p_n = B.de_get_prec_time(ctx)
-    B.de_set_profiling(ctx, False)
     st = solver.stats()
     value = n_free * its_tot / (ms / 1e3) / 1e6
     ms_step = ms / args.steps
+    # per-kernel launch times for the roofline: separate, untimed steps with event-record nodes captured around
+    # each Schur apply and preconditioner application inside the PCG graph (on the library's stream)
+    nprof = min(2, args.steps)
+    B.de_set_profiling(ctx, True)
+    its_prof = 0
+    for t in range(nprof):
+        its_prof += step(args.warmup + t)[0]
+    torch.cuda.synchronize()
+    k_ms, k_n = B.de_get_kernel_time(ctx)
+    p_ms, p_n = B.de_get_prec_time(ctx)
+    B.de_set_profiling(ctx, False)
 
     # ------------------------------------------------ e2e: host buffers through the C-ABI
     e2e = None
@@ -298,51 +326,71 @@ def main():
         return 0
 
     pk = peaks()
-    traffic = {}
+    traffic, traffic_src = {}, None
     try:
         prof = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
         if prof.get("config") == args.config and prof.get("n_gpus", 1) == world:
             traffic = prof.get("dram_bytes_per_launch", {})
+            traffic_src = prof.get("source")
     except Exception:
         pass
     peak_src = "MEASURED_PEAKS.json hbm_gbs" if not pk.get("_fallback") else "fallback 6650 GB/s"
+    hbm = pk["hbm_gbs"]
 
-    def roofline(kernel, what, algo_bytes, launch_ms, launches):
+    def roofline(kernel, what, algo_bytes, bytes_how, launch_ms, launches, model_bytes=None):
         achieved = algo_bytes / (launch_ms / 1e3) / 1e9 if launch_ms > 0 else None
-        return {"bound": "hbm", "kernel": f"{kernel} ({what})", "achieved": achieved, "peak": pk["hbm_gbs"],
-                "unit": "GB/s", "frac": (achieved / pk["hbm_gbs"]) if achieved else None,
-                "traffic": traffic.get(kernel), "algorithmic_bytes_per_launch": algo_bytes,
-                "launch_ms": launch_ms, "launches_timed": launches,
-                "share_of_step": (launch_ms * launches / ms) if launches else None, "peak_source": peak_src}
+        tr = traffic.get(kernel)
+        per_step = launches / max(1, nprof)
+        out = {"bound": "hbm", "kernel": f"{kernel} ({what})", "achieved": achieved, "peak": hbm,
+               "unit": "GB/s", "frac": (achieved / hbm) if achieved else None, "traffic": tr,
+               "algorithmic_bytes_per_launch": algo_bytes, "algorithmic_bytes_how": bytes_how,
+               "launch_ms": launch_ms, "launches_profiled": launches,
+               "share_of_step": (launch_ms * per_step / ms_step) if launches else None, "peak_source": peak_src}
+        if tr:
+            out["frac_measured_dram"] = tr / (launch_ms / 1e3) / 1e9 / hbm
+            out["traffic_source"] = traffic_src
+        if model_bytes:
+            out["streaming_model_bytes_per_launch"] = model_bytes
+        return out
 
     schur_kernel = "k_schur_explicit" if st.schur_explicit else "k_schur_local"
     schur_bytes = st.bytes_schur_explicit if st.schur_explicit else st.bytes_schur
-    roof_s = roofline(schur_kernel, "C2 Schur apply", schur_bytes, k_ms, k_n)
+    roof_s = roofline(schur_kernel, "C2 Schur apply", schur_bytes,
+                      "one pass over the packed local Schur complements S_s (lower 16x16 tiles) + local interface "
+                      "vectors" if st.schur_explicit else
+                      "one pass over the factor band + ring blocks + local interface vectors", k_ms, k_n)
     roof_p = roofline("k_prec_coop", "C5 preconditioner application: k_prec_coop + k_prec_ritz + k_prec_combine, "
-                      "event-timed as one", st.bytes_prec, p_ms, p_n) if p_n else None
+                      "event-timed as one", st.bytes_prec_min,
+                      "minimum bytes: every distinct byte one application touches counted once (skeleton operators "
+                      "M, L; per elimination the face data, couplings and S_C^-1, once when shared by the "
+                      "components; r, z; the k basis vectors W, MW, LW written once) -- de_stats.bytes_prec_min",
+                      p_ms, p_n, st.bytes_prec) if p_n else None
     if roof_p and (roof_p["share_of_step"] or 0) > (roof_s["share_of_step"] or 0):
         roof, roof2 = roof_p, roof_s
     else:
         roof, roof2 = roof_s, roof_p
+    # HBM fraction of the PCG iteration = B_alg/iter x iterations / t_iterloop / peak, with
+    # B_alg/iter = one pass over the interior factors + interface vectors (de_stats.bytes_iter), and the same with
+    # the bytes of the representation the loop actually streams (explicit S_s on c5)
+    bytes_rep = (st.bytes_schur_explicit if st.schur_explicit else st.bytes_schur) + st.n_Gamma * 8.0 * 11.0
+    iter_frac = {"b_alg_per_iter": st.bytes_iter, "t_pcg_ms_total": ms_pcg, "iterations": its_tot,
+                 "frac_b_alg": st.bytes_iter * its_tot / (ms_pcg / 1e3) / 1e9 / hbm if ms_pcg > 0 else None,
+                 "bytes_per_iter_as_streamed": bytes_rep,
+                 "frac_as_streamed": bytes_rep * its_tot / (ms_pcg / 1e3) / 1e9 / hbm if ms_pcg > 0 else None,
+                 "how": "SURVEY.md 8(d): bytes/iter x iterations / PCG-loop time (de_stats.ms_pcg: condense, PCG, "
+                        "refinement, back-substitution) / measured HBM peak"}
     cb = None
     if not args.no_cpu_baseline and world == 1:
-        cb = cpu_baseline(prob, its_tot // max(1, args.steps))
-        cb = {k: v for k, v in cb.items() if k not in ("s_per_iter", "s_factor")}
+        cb = cpu_baseline(prob, int(round(its_tot / max(1, args.steps))))
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{args.config}: BASELINE config 5 step (2048x1024 Q1 plane stress, 64x32 "
-                                   "subdomains of 32x32, SIMP p=3, density update -> refactor -> warm PCG rtol 1e-10)"
-                       if args.config == "c5" else args.config,
-                       "n_free": int(n_free), "n_gamma": int(st.n_Gamma), "subdomains": int(st.n_sub),
-                       "preconditioner": "inverse Lanczos k=10, theta=0.5, exact inner solves (R10)",
-                       "l2": "inputs larger than L2 (factor bands %.2f GB/rank)" % (st.bytes_factor / 1e9),
-                       "parallelism": f"subdomain slabs x{world}"},
+            "config": workload_config(args.config, n_free, st.n_Gamma, st.n_sub, args.gpus),
             "iterations_per_step": its_tot / args.steps, "true_relres_max": rel_max,
             "relres_dd_max": reldd_max, "solve_status_failures": status_fail,
             "solves_per_sec": 1e3 / ms_step, "factor_ms": st.ms_factor,
             "gpu_launches": int(launches), "clocks": clk, "roofline": roof, "roofline_secondary": roof2,
-            "e2e": e2e, "cpu_baseline": cb}
+            "iteration_hbm_fraction": iter_frac, "e2e": e2e, "cpu_baseline": cb}
     print(json.dumps(line))
     solver.close()
     if world > 1:

@@ -106,7 +106,19 @@ typedef struct {
                                 K u = f with P~ = [[K_II, K_IGamma], [0, S~]],
                                 single rank; `iterations` then counts FGMRES iterations */
     int32_t restart;         /* FGMRES restart length m, 1 <= m <= 31 (default 30) */
+    void* loopback;          /* nranks > 1 without NCCL: a de_loopback_t* shared by the nranks contexts of one process
+                                (see de_loopback_create); NULL (default) = NCCL with nccl_id */
 } de_options_t;
+
+/* Single-process loopback group: nranks contexts on one device, each driven by its own host thread, exercise the
+ * multi-rank path (owned subdomain slabs, partial interface sums, the cross-rank exchanges) without NCCL. Every
+ * all-reduce becomes: copy to this rank's device slot, host barrier, fixed-order sum of slots 0..nranks-1 on this
+ * rank's stream, host barrier -- host-synchronised, so no kernel ever waits on another rank's kernel and the PCG
+ * loop runs uncaptured (use_graph is ignored). Results are bitwise identical on every rank. Test/verification
+ * path of DESIGN.md §8; the owner destroys the group after every context using it. */
+typedef struct de_loopback de_loopback_t;
+de_status_t de_loopback_create(int32_t nranks, de_loopback_t** out);
+void de_loopback_destroy(de_loopback_t* g);
 
 typedef struct {
     int64_t ndof, n_free, n_I, n_Gamma, n_sub, n_sub_local;
@@ -140,6 +152,8 @@ typedef struct {
                                 the iterative refinement (R11/R17); de_solve returns DE_OK iff this is
                                 <= rtol. The returned u is fl(u_hi + u_lo), so relres_true exceeds it by at most
                                 the FP64 rounding floor of the problem (measured for config 5: 1.35e-10) */
+    double bytes_prec_min;   /* distinct bytes one preconditioner application touches, each counted once (operators,
+                                r, z, basis written once): the minimum-bytes figure of its roofline */
 } de_stats_t;
 
 /* Fill *opt with defaults (theta 0.5, k 10, inner_mode 1, max_iter 20000, FR, 1 rank). */

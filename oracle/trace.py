@@ -17,7 +17,9 @@ component whose skeleton has a connected piece without Dirichlet contact is
 Pins (tests/test_oracle_trace_precond.py): SPEC.md:179 worked example (single face,
 one interior node, h=1/2 -> M=[1/3], L=[4]); L row sums vanish away from
 Dirichlet; the 1D pencil eigenvalues (6/h^2)(1-cos phi_j)/(2+cos phi_j);
-M sums to the total facet measure (1^T M 1 = |Gamma_c| incl. eliminated part).
+M sums to the total facet measure (1^T M 1 = |Gamma_c| incl. eliminated part); the 3D
+facet matrices by the tensor-product pencil of one square interface with a Dirichlet rim
+(eigenvalues alpha_i + alpha_j of the 1D pencil, mass eigenvalues mu_i mu_j).
 """
 from __future__ import annotations
 

@@ -40,7 +40,7 @@ class de_options_t(C.Structure):
                 ("stream", C.c_void_p), ("check_every", C.c_int32), ("use_graph", C.c_int32),
                 ("host_only", C.c_int32), ("prec_kernels", C.c_int32), ("schur_mode", C.c_int32),
                 ("weighted_trace", C.c_int32),
-                ("outer", C.c_int32), ("restart", C.c_int32)]
+                ("outer", C.c_int32), ("restart", C.c_int32), ("loopback", C.c_void_p)]
 
 
 class de_stats_t(C.Structure):
@@ -55,7 +55,8 @@ class de_stats_t(C.Structure):
                 ("bytes_schur", C.c_double), ("kernels_launched", C.c_int64),
                 ("iterations_pass1", C.c_int32), ("schur_explicit", C.c_int32),
                 ("bytes_schur_explicit", C.c_double),
-                ("bytes_prec", C.c_double), ("inner_iterations", C.c_int64), ("relres_dd", C.c_double)]
+                ("bytes_prec", C.c_double), ("inner_iterations", C.c_int64), ("relres_dd", C.c_double),
+                ("bytes_prec_min", C.c_double)]
 
 
 class de_oc_params_t(C.Structure):
@@ -103,6 +104,8 @@ def lib():
         "de_oc_step": (I32, [P, P, C.POINTER(de_oc_params_t), P, C.POINTER(D), C.POINTER(D)]),
         "de_destroy": (None, [P]),
         "de_last_error": (C.c_char_p, []),
+        "de_loopback_create": (I32, [I32, C.POINTER(P)]),
+        "de_loopback_destroy": (None, [P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -290,6 +293,17 @@ def de_oc_step(ctx, u, params: de_oc_params_t, nelem: int):
     c, lam = C.c_double(), C.c_double()
     _check(lib().de_oc_step(ctx, _ptr(u), C.byref(params), _ptr(rho), C.byref(c), C.byref(lam)))
     return rho, c.value, lam.value
+
+
+def de_loopback_create(nranks: int):
+    g = C.c_void_p()
+    _check(lib().de_loopback_create(int(nranks), C.byref(g)))
+    return g
+
+
+def de_loopback_destroy(g):
+    if g:
+        lib().de_loopback_destroy(g)
 
 
 def de_destroy(ctx):

@@ -10,6 +10,8 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <condition_variable>
+#include <mutex>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -67,6 +69,29 @@ static NcclApi& nccl() {
 }  // namespace de
 
 using namespace de;
+
+// Loopback group (include/de.h de_loopback_create): host barrier + device slots [n][cap]
+struct de_loopback {
+    int n = 1;
+    std::mutex m;
+    std::condition_variable cv;
+    int count = 0;
+    long gen = 0;
+    double* slots = nullptr;
+    size_t cap = 0;
+    int device = 0;
+    void barrier() {
+        std::unique_lock<std::mutex> lk(m);
+        const long g = gen;
+        if (++count == n) {
+            count = 0;
+            ++gen;
+            cv.notify_all();
+        } else {
+            cv.wait(lk, [&] { return gen != g; });
+        }
+    }
+};
 
 struct de_ctx {
     HostSetup hs;
@@ -136,6 +161,7 @@ struct de_ctx {
     int fg_m = 0;
     // nccl
     void* comm = nullptr;
+    de_loopback* lb = nullptr;        // loopback group instead of NCCL (tests of the multi-rank path)
     de_stats_t stats{};
 };
 
@@ -179,6 +205,21 @@ de_status_t check_launch() {
 
 de_status_t allreduce(de_ctx* c, double* buf, size_t n) {
     if (c->nranks <= 1) return DE_OK;
+    if (c->lb) {   // loopback: host-synchronised, fixed-order sum of the ranks' slots (bitwise equal on every rank)
+        de_loopback* g = c->lb;
+        if (n > g->cap) {
+            set_error("loopback all-reduce of %zu doubles exceeds the group's capacity %zu", n, g->cap);
+            return DE_EINVAL;
+        }
+        DE_CUDA(cudaMemcpyAsync(g->slots + size_t(c->rank) * g->cap, buf, n * sizeof(double),
+                                cudaMemcpyDeviceToDevice, c->st));
+        DE_CUDA(cudaStreamSynchronize(c->st));
+        g->barrier();
+        launch_sum_slots(buf, g->slots, g->n, g->cap, int64_t(n), c->st);
+        DE_CUDA(cudaStreamSynchronize(c->st));
+        g->barrier();
+        return check_launch();
+    }
     int r = nccl().allreduce(buf, buf, n, 8 /*ncclFloat64*/, 0 /*ncclSum*/, c->comm, c->st);
     if (r != 0) {
         set_error("ncclAllReduce failed: %s", nccl().errstr ? nccl().errstr(r) : "?");
@@ -313,7 +354,7 @@ de_status_t read_state(de_ctx* c, PcgState* h) {
 }
 
 de_status_t run_loop(de_ctx* c, PcgState& hsv) {
-    const bool use_graph = c->opt.use_graph != 0;
+    const bool use_graph = c->opt.use_graph != 0 && !c->lb;   // loopback exchanges are host-synchronised
     if (use_graph && (!c->gexec || c->graph_prof != c->profiling)) TRY(build_graph(c));
     while (true) {
         const int it_before = hsv.it;
@@ -723,6 +764,29 @@ double prec_bytes_model(const HostSetup& hs, int k, bool gram_cgs2, bool fold) {
     return b;
 }
 
+// Distinct bytes one preconditioner application touches, each counted once: a lower bound on its HBM traffic
+// (perfect on-chip reuse inside the application; DESIGN.md §6 "minimum bytes"). r in, z out, the skeleton
+// operators M and L (shared CSR pattern), per elimination operator (K and M) the face data, the face/cross
+// couplings and S_C^-1 (once when the components share it), and the k basis vectors W, M W, L W written once.
+double prec_min_bytes(const HostSetup& hs, int k) {
+    const double n = double(hs.comp_off[hs.ncomp]), nnz = double(hs.M.val.size());
+    bool tri = true;
+    for (const HElim* E : {&hs.elimK, &hs.elimM})
+        for (int F = 0; F < E->nfaces && tri; ++F)
+            if (E->face_band[F] > 1 || E->face_off[F + 1] - E->face_off[F] > TRI_N) tri = false;
+    double b = n * (4 + 8 + 8) + (n + 1) * 4 + nnz * (4 + 8 + 8);
+    for (const HElim* E : {&hs.elimK, &hs.elimM}) {
+        const double nfn = double(E->face_nodes.size()), ncr = double(E->ncross);
+        if (tri)   // PCR coefficients + node ids per face, per-node couplings g (2 per node), G^T rows, cross ids
+            b += double(E->nfaces) * (PCR_Q * 32 * 8 + 32 * 4) + n * 2 * (4 + 8) + 2 * nfn * 12 + ncr * 12;
+        else       // band factors [L | M], node ids, X_FC and X_CF
+            b += double(E->face_fac.size()) * 8 + nfn * 4 + double(E->XFC.val.size() + E->XCF.val.size()) * 12 + ncr * 4;
+        for (int cc = 0; cc < hs.ncomp; ++cc)
+            if (cc == 0 || !E->sc_shared) b += double(E->sc_off[cc + 1] - E->sc_off[cc]) * 8;
+    }
+    return b + 3.0 * k * n * 8;
+}
+
 de_status_t setup_impl(const de_mesh_t* mesh, const double* density, double E0, double Emin, double p,
                        double nu, const de_partition_t* part, const de_options_t* opt_in, de_ctx* c) {
     de_options_t opt;
@@ -924,8 +988,26 @@ de_status_t setup_impl(const de_mesh_t* mesh, const double* density, double E0, 
     if (opt.inner_mode == 0 || opt.inner_mode == 1) TRY(upload_prec(c));
     DE_CUDA(cudaStreamSynchronize(c->st));
     TRY(check_launch());
-    // ---- NCCL
-    if (c->nranks > 1) {
+    // ---- NCCL (or the loopback group)
+    if (c->nranks > 1 && opt.loopback) {
+        de_loopback* g = static_cast<de_loopback*>(opt.loopback);
+        if (g->n != c->nranks) {
+            set_error("loopback group has %d ranks, options.nranks = %d", g->n, c->nranks);
+            return DE_EINVAL;
+        }
+        {   // capacity: the largest all-reduce is the full displacement vector (dd_pass)
+            std::lock_guard<std::mutex> lk(g->m);
+            if (g->cap < size_t(hs.ndof)) {
+                if (g->slots) cudaFree(g->slots);
+                g->slots = nullptr;
+                g->cap = 0;
+                DE_CUDA(cudaMalloc(&g->slots, size_t(g->n) * hs.ndof * sizeof(double)));
+                g->cap = size_t(hs.ndof);
+            }
+        }
+        c->lb = g;
+        g->barrier();   // every rank's setup (and the slot allocation) is done before any exchange
+    } else if (c->nranks > 1) {
         if (!nccl().ok) {
             set_error("nranks > 1 but libnccl.so.2 could not be loaded");
             return DE_ENCCL;
@@ -970,6 +1052,7 @@ de_status_t setup_impl(const de_mesh_t* mesh, const double* density, double E0, 
                    double(hs.n_G) * 8.0 * 11.0;
     S.bytes_prec = c->have_prec ? prec_bytes_model(hs, c->P.kmax, c->use_coop && c->coop.gram_cgs2,
                                                    c->use_coop && c->coop.fold) : 0.0;
+    S.bytes_prec_min = c->have_prec ? prec_min_bytes(hs, c->P.kmax) : 0.0;
     return DE_OK;
 }
 
@@ -1011,9 +1094,19 @@ de_status_t factor_impl(de_ctx* c) {
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     c->stats.ms_factor = ms;
-    if (fail) {
+    double any_fail = fail ? 1.0 : 0.0;
+    if (c->nranks > 1) {   // every rank must agree, or the healthy ranks would block in the next exchange
+        DE_CUDA(cudaMemcpyAsync(c->d_scal, &any_fail, sizeof(double), cudaMemcpyHostToDevice, c->st));
+        TRY(allreduce(c, c->d_scal, 1));
+        DE_CUDA(cudaMemcpyAsync(&any_fail, c->d_scal, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+        DE_CUDA(cudaStreamSynchronize(c->st));
+    }
+    if (fail || any_fail > 0.0) {
         c->factored = false;
-        set_error("non-positive pivot in the interior factorisation of subdomain %d", fail - 1);
+        if (fail)
+            set_error("non-positive pivot in the interior factorisation of subdomain %d", fail - 1);
+        else
+            set_error("non-positive pivot in the interior factorisation on another rank");
         return DE_ENOTSPD;
     }
     c->factored = true;
@@ -1205,6 +1298,10 @@ de_status_t solve_impl(de_ctx* c, const double* d_f, double rtol, double* d_u, i
     TRY(masked_norm2(c, d_f, &f2));
     c->launches += 3;
     const double fnorm = std::sqrt(f2);
+    if (!std::isfinite(fnorm)) {
+        set_error("rhs has non-finite entries on free dofs");
+        return DE_EINVAL;
+    }
     c->stats.iterations = 0;
     c->stats.restarts = 0;
     if (fnorm == 0.0) {
@@ -1728,6 +1825,23 @@ de_status_t de_oc_step(de_ctx_t* c, const double* u, const de_oc_params_t* prm, 
         DE_CUDA(cudaStreamSynchronize(c->st));
     }
     return DE_OK;
+}
+
+de_status_t de_loopback_create(int32_t nranks, de_loopback_t** out) {
+    if (!out || nranks < 1) {
+        set_error("de_loopback_create: nranks >= 1 and a non-null out pointer required");
+        return DE_EINVAL;
+    }
+    de_loopback_t* g = new de_loopback_t();
+    g->n = nranks;
+    *out = g;
+    return DE_OK;
+}
+
+void de_loopback_destroy(de_loopback_t* g) {
+    if (!g) return;
+    if (g->slots) cudaFree(g->slots);
+    delete g;
 }
 
 void de_destroy(de_ctx_t* c) {

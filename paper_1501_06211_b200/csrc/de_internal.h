@@ -319,6 +319,7 @@ void launch_multi_axpy(double* w, const double* V, int64_t ld, int nv, const dou
                        cudaStream_t st);
 void launch_scale_invnorm(double* dst, const double* src, const double* sq, int64_t n, cudaStream_t st);
 void launch_copy(double* dst, const double* src, int64_t n, const PcgState* s, cudaStream_t st);
+void launch_sum_slots(double* buf, const double* slots, int n, size_t cap, int64_t len, cudaStream_t st);
 void launch_axpy(double* y, const double* x, double a, int64_t n, cudaStream_t st);
 void launch_scatter_gamma(const int32_t* gamma_dofs, const double* uG, double* u, int64_t nG,
                           cudaStream_t st);

@@ -295,6 +295,21 @@ void launch_copy(double* dst, const double* src, int64_t n, const PcgState* s, c
     k_copy<<<blocks, 256, 0, st>>>(dst, src, n, s);
 }
 
+// buf = sum_{r < n} slots[r] in rank order (the loopback all-reduce: the same fixed order on every rank)
+__global__ void k_sum_slots(double* __restrict__ buf, const double* __restrict__ slots, int n, size_t cap,
+                            int64_t len) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < len; i += int64_t(gridDim.x) * blockDim.x) {
+        double s = 0.0;
+        for (int r = 0; r < n; ++r) s += slots[size_t(r) * cap + i];
+        buf[i] = s;
+    }
+}
+
+void launch_sum_slots(double* buf, const double* slots, int n, size_t cap, int64_t len, cudaStream_t st) {
+    const int blocks = int(std::max<int64_t>(1, std::min<int64_t>((len + 255) / 256, 148 * 8)));
+    k_sum_slots<<<blocks, 256, 0, st>>>(buf, slots, n, cap, len);
+}
+
 __global__ void k_axpy(double* __restrict__ y, const double* __restrict__ x, double a, int64_t n) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
         y[i] += a * x[i];

@@ -538,7 +538,7 @@ __device__ void elim_coop(cg::grid_group& grid, const CoopArgs& a, const ElimDev
             __syncthreads();
             if (dbg2) a.timers[181] = gtimer();
             const double* S = E.Sinv + E.sc_off[c];
-            const bool shared = E.sc_shared != 0;
+
             // block lb owns the contiguous rows [rlo, rhi); warp w takes one column slice of all of them (two
             // rows at a time, NA loads per row per lane in flight); warp partials are summed in fixed order
             const int rlo = int(int64_t(lb) * ncc / nbc), rhi = int(int64_t(lb + 1) * ncc / nbc), nr = rhi - rlo;
@@ -557,10 +557,11 @@ __device__ void elim_coop(cg::grid_group& grid, const CoopArgs& a, const ElimDev
                     for (int q = 0; q < NA; ++q) {
                         const int jj = j + 32 * q;
                         const bool ok = jj < c1;
-                        // streamed once per step (evict-first); a shared S_C^-1 is read by the blocks of every
-                        // component at the same time, so it stays cacheable for the partner's hit in L2
-                        v0[q] = ok ? (shared ? __ldcg(row0 + jj) : __ldcs(row0 + jj)) : 0.0;
-                        v1[q] = (ok && two) ? (shared ? __ldcg(row1 + jj) : __ldcs(row1 + jj)) : 0.0;
+                        // streamed once per step (evict-first); a shared S_C^-1 (HElim::sc_shared) is read by the
+                        // blocks of every component at about the same time, and evict-first lines still serve the
+                        // partner (measured: L2-cached loads evict the basis and are slower)
+                        v0[q] = ok ? __ldcs(row0 + jj) : 0.0;
+                        v1[q] = (ok && two) ? __ldcs(row1 + jj) : 0.0;
                         t[q] = ok ? tC[jj] : 0.0;
                     }
 #pragma unroll

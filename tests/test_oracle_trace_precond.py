@@ -49,6 +49,44 @@ def test_pencil_closed_form():
                                pin["values"], rtol=1e-12)
 
 
+def _single_plane(N, h):
+    """3D mesh 2 x N x N elements split into 2 x 1 x 1 subdomains: one interface plane x = h with (N+1)^2
+    nodes; its rim (y or z at the boundary) is Dirichlet in every component."""
+    nel, sub = (2, N, N), (1, N, N)
+    nx, ny, nz = 3, N + 1, N + 1
+    fixed = np.zeros(3 * nx * ny * nz, dtype=np.uint8)
+    for k in range(nz):
+        for j in range(ny):
+            if j in (0, N) or k in (0, N):
+                for i in range(nx):
+                    node = i + nx * (j + ny * k)
+                    fixed[3 * node:3 * node + 3] = 1
+    return Problem("plane", 3, nel, sub, fixed, np.ones(2 * N * N), np.zeros(3 * nx * ny * nz), h=h)
+
+
+@pytest.mark.parametrize("N,h", [(5, 0.25), (7, 1.0)])
+def test_3d_facet_trace_tensor_pencil(N, h):
+    """3D trace elements (bilinear quads, R6) pinned by the tensor-product closed form: on one square interface
+    with a Dirichlet rim, L = K1 (x) M1 + M1 (x) K1 and M = M1 (x) M1 for the 1D pencil (K1, M1) of the interior
+    nodes, so the eigenvalues of (L, M) are alpha_i + alpha_j with alpha_j = (6/h^2)(1-cos(j pi/N))/(2+cos(j pi/N))
+    (the 1D closed form of SPEC.md:196 / pencil_1d_k5_h025). A single Kronecker term, a wrong facet mass or
+    stiffness scale (3D scales as h^0 for L and h^2 for M) all break it."""
+    p = _single_plane(N, h)
+    T = build_topology(p)
+    phi = np.arange(1, N) * np.pi / N
+    alpha = 6.0 / h ** 2 * (1 - np.cos(phi)) / (2 + np.cos(phi))
+    expect = np.sort((alpha[:, None] + alpha[None, :]).ravel())
+    for sk in component_skeletons(p, T):
+        M, L, sing = component_trace_matrices(p, sk)
+        assert M.shape == ((N - 1) ** 2,) * 2 and not sing
+        np.testing.assert_allclose(np.sort(sla.eigh(L.toarray(), M.toarray(), eigvals_only=True)), expect,
+                                   rtol=1e-11)
+        # the mass alone: eigenvalues mu_i mu_j of M1 (x) M1, M1 = tridiag(h/6, 4h/6, h/6) -> (h/3)(2 + cos phi)
+        mu = h / 3.0 * (2 + np.cos(phi))
+        np.testing.assert_allclose(np.sort(np.linalg.eigvalsh(M.toarray())),
+                                   np.sort((mu[:, None] * mu[None, :]).ravel()), rtol=1e-12)
+
+
 @pytest.mark.parametrize("name,kw", [("c2", dict(nel=(16, 8), sub=(4, 4))),
                                      ("c4", dict(nel=(6, 4, 4), sub=(2, 2, 2)))])
 def test_trace_row_sums_and_measure(name, kw):
