@@ -476,6 +476,7 @@ de_status_t upload_prec_impl(de_ctx* c) {
         }
         mfac = std::min(mfac, 0x7fff);
         D.maxface = (mfac << 16) | mf;
+        D.maxld = maxb + 1;
         TRY(dupload(c, &D.face_off, E.face_off));
         TRY(dupload(c, &D.face_nodes, E.face_nodes));
         TRY(dupload(c, &D.face_band, E.face_band));

@@ -235,8 +235,17 @@ __device__ __forceinline__ double spmv_elim(const CsrDev& M, const CsrDev& L, in
     return xi;
 }
 
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+
 // Warp solve of one face block (L then M = P L^T P forward sweeps, b <= 31, row window in registers).
-// rhs = scale * b_F (mode 0) or scale * b_F - X_FC xC (mode 1).
+// rhs = scale * b_F (mode 0) or scale * b_F - X_FC xC (mode 1). The factor columns stream through a two-chunk
+// shared-memory ring (32 columns per chunk, cp.async issued one chunk ahead), so no load sits on the per-row
+// dependency chain (measured: per-row global loads made the 3D face phases 37-92 us).
 __device__ void face_warp(const CoopArgs& a, const ElimDev& E, int F, const double* __restrict__ b,
                           const double* scl, const double* __restrict__ xC, double* __restrict__ out, int mode,
                           double* wsm, int lane) {
@@ -246,13 +255,9 @@ __device__ void face_warp(const CoopArgs& a, const ElimDev& E, int F, const doub
     double* rb = wsm;
     double* ys = wsm + a.mf;
     int* idx = reinterpret_cast<int*>(wsm + 2 * a.mf);
+    double* cbuf = wsm + 3 * a.mf;                // [2][32 * ld] column chunks
+    const int cstride = 32 * ld;
     const double* gf = E.face_fac + E.face_fac_off[F];
-    const double* fac0 = gf;
-    if (a.stage) {
-        double* fs = wsm + 3 * a.mf;
-        for (int i = lane; i < 2 * n * ld; i += 32) fs[i] = gf[i];
-        fac0 = fs;
-    }
     const double sc = scl[ccomp(P.comp_off, P.ncomp, E.face_nodes[o])];
     for (int i = lane; i < n; i += 32) {
         const int node = E.face_nodes[o + i];
@@ -264,21 +269,38 @@ __device__ void face_warp(const CoopArgs& a, const ElimDev& E, int F, const doub
     }
     __syncwarp();
     for (int sw = 0; sw < 2; ++sw) {
-        const double* __restrict__ fac = fac0 + (sw == 0 ? 0 : size_t(n) * ld);
+        const double* __restrict__ fac = gf + (sw == 0 ? 0 : size_t(n) * ld);
         const double* __restrict__ src = sw == 0 ? rb : ys;
         double* dst = sw == 0 ? ys : rb;          // both in shared memory; y reversed, then x reversed back
+        const int nch = (n + 31) / 32;
+        {   // chunk 0
+            const int cnt = min(32, n) * ld;
+            for (int i = lane; i < cnt; i += 32) cp_async8(cbuf + i, fac + i);
+            cp_async_commit();
+        }
         double v = lane < n ? src[lane] : 0.0;
         double outv = 0.0;                        // lane l keeps the solution of rows = l (mod 32)
         __syncwarp();
-        for (int j0 = 0; j0 < n; j0 += 32) {      // 32-row blocks: the loop body has loads only
-            const int jn = min(32, n - j0);
+        for (int ch = 0; ch < nch; ++ch) {
+            const int j0 = 32 * ch, jn = min(32, n - j0);
+            if (ch + 1 < nch) {                   // next chunk into the other buffer (its last reader was ch - 1)
+                const int cnt = min(32, n - j0 - 32) * ld;
+                double* nb = cbuf + ((ch + 1) & 1) * cstride;
+                const double* gs = fac + size_t(j0 + 32) * ld;
+                for (int i = lane; i < cnt; i += 32) cp_async8(nb + i, gs + i);
+            }
+            cp_async_commit();                    // (possibly empty) group: wait_group 1 then covers chunk ch
+            cp_async_wait1();
+            __syncwarp();
+            const double* cb = cbuf + (ch & 1) * cstride;
 #pragma unroll 4
             for (int jj = 0; jj < jn; ++jj) {
                 const int j = j0 + jj;
-                const double* col = fac + size_t(j) * ld;
+                const double* col = cb + jj * ld;
                 const double cl = (lane >= 1 && lane <= bw) ? col[lane] : 0.0;
+                const double c0 = col[0];
                 const double nxt = (j + 32 < n) ? src[j + 32] : 0.0;   // row entering lane 31 (uniform load)
-                const double yj = __shfl_sync(0xffffffffu, v, 0) * col[0];
+                const double yj = __shfl_sync(0xffffffffu, v, 0) * c0;
                 v = fma(-cl, yj, v);
                 const double vs = __shfl_down_sync(0xffffffffu, v, 1);
                 v = (lane == 31) ? nxt : vs;                           // branch-free: keeps the warp converged
@@ -425,7 +447,7 @@ __device__ void elim_coop(cg::grid_group& grid, const CoopArgs& a, const ElimDev
     const int gt = gw * 32 + lane, nthr = nwarps * 32;
     double* y = P.y;
     double* xC = P.y + P.nflat;
-    double* wsm = dsm + size_t(w) * a.per_warp;
+    double* wsm = dsm + size_t(w > 0 ? w - 1 : 0) * a.per_warp;   // warp 0 (barrier host) does no face solves
     long long tf0 = clock64();
     if (E.tri && E.fuse) {   // warp per face (PCR); each face lies in one component
         if (w > 0)
@@ -480,7 +502,7 @@ __device__ void elim_coop(cg::grid_group& grid, const CoopArgs& a, const ElimDev
     __syncwarp();   // lane 0 spun in the barrier: reconverge before warp-synchronous code
     STAMP(stamp++);
     // cross points of this block's component: t_C = scl*b_C - X_CF y in smem, then rows of S_C^-1 t_C
-    const bool dbg2 = TIM && a.timers && blockIdx.x == 0 && threadIdx.x == 32 && stamp == 26;   // E2 of Lanczos step 5 (fused path)
+    const bool dbg2 = TIM && a.timers && blockIdx.x == 0 && threadIdx.x == 32;   // E2 sub-phases (the last elimination wins)
     if (dbg2) a.timers[180] = gtimer();
     {
         const int base = E.cross_comp_off[c], ncc = E.cross_comp_off[c + 1] - base;
@@ -1254,13 +1276,15 @@ bool prec_coop_prepare(const PrecDev& P, int device, CoopBuffers& B) {
     cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device);
     if (!coop) return false;
     const int mf = std::max(P.eK.maxface & 0xffff, P.eM.maxface & 0xffff);
-    const int mfac = std::max(P.eK.maxface >> 16, P.eM.maxface >> 16);
     int ncmax = 1;
     for (const ElimDev* E : {&P.eK, &P.eM})
         for (int c = 0; c < P.ncomp; ++c) ncmax = std::max(ncmax, E->cross_comp_off[c + 1] - E->cross_comp_off[c]);
-    const bool stage = size_t(CW) * (3 * mf + mfac) * 8 <= 96 * 1024;
-    const int per_warp = stage ? 3 * mf + mfac : 3 * mf;
-    size_t smem = size_t(CW) * per_warp * 8;
+    // per face-solving warp (warps 1..CW-1): rhs / y / node ids (mf each) + the two-chunk column ring of face_warp
+    int maxld = 1;
+    for (const ElimDev* E : {&P.eK, &P.eM}) maxld = std::max(maxld, E->maxld);
+    const bool stage = false;
+    const int per_warp = 3 * mf + 2 * 32 * maxld;
+    size_t smem = size_t(CW - 1) * per_warp * 8;
     {   // t_C plus the per-warp partials of the rows one block owns in the cross-point GEMV (>= 1 block per SM)
         const int nbc_lo = std::max(1, nsm / std::max(1, P.ncomp));
         smem = std::max(smem, (size_t(ncmax) + size_t(CW) * ((ncmax + nbc_lo - 1) / nbc_lo)) * 8);

@@ -28,4 +28,8 @@ if os.environ.get("DE_PREC_TIMERS"):
     L.de_debug_prec_timers(S.ctx, t, 200 + 8192)
     st = [x for x in list(t)[:100] if x]
     print("phases us:", " ".join(f"{(b - a) / 1e3:.1f}" for a, b in zip(st, st[1:])), "total", (st[-1] - st[0]) / 1e3)
+    e = list(t)[180:186]
+    if all(e):
+        print("last elimination, cross phase (block 0) us: t_C", (e[1] - e[0]) / 1e3, "gemv", (e[2] - e[1]) / 1e3,
+              "syncthreads", (e[3] - e[2]) / 1e3, "sums+fold", (e[4] - e[3]) / 1e3, "grid.sync", (e[5] - e[4]) / 1e3)
 S.close()
