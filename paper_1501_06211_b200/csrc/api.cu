@@ -477,6 +477,13 @@ de_status_t upload_prec_impl(de_ctx* c) {
         mfac = std::min(mfac, 0x7fff);
         D.maxface = (mfac << 16) | mf;
         D.maxld = maxb + 1;
+        D.face_comp_off[0] = 0;
+        for (int cc = 0; cc < MAXC; ++cc)
+            D.face_comp_off[cc + 1] = D.face_comp_off[cc] + (cc < hs.ncomp ? int32_t(hs.n_faces_c[cc]) : 0);
+        if (D.face_comp_off[hs.ncomp] != E.nfaces) {
+            set_error("internal: faces are not grouped by component");
+            return DE_EINVAL;
+        }
         TRY(dupload(c, &D.face_off, E.face_off));
         TRY(dupload(c, &D.face_nodes, E.face_nodes));
         TRY(dupload(c, &D.face_band, E.face_band));

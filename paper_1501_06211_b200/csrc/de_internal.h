@@ -160,6 +160,7 @@ struct OcState {
 struct ElimDev {
     int32_t nfaces, ncross, ncomp, maxface;
     int32_t maxld;               // max face band + 1 (column length of the face factors)
+    int32_t face_comp_off[MAXC + 1];   // faces are grouped by component: [face_comp_off[c], face_comp_off[c+1])
     int32_t *face_off, *face_nodes, *face_band;
     int64_t* face_fac_off;
     double* face_fac;

@@ -391,17 +391,19 @@ __device__ void face_thread_tridiag(const CoopArgs& a, const ElimDev& E, int F, 
 // Warp solve of one tridiagonal face block by parallel cyclic reduction (lane j = node j; coefficients
 // precomputed per level, ElimDev::pcr): y_F = X_FF^-1 (scale * b_F). Same result as the Cholesky sweeps up to
 // rounding (X_FF is diagonally dominant: K = L (+ M) and M on a path).
-// NF faces per call (F0 + f * stride, f < NF; F >= nfaces skipped) with every load issued before the first use.
-template <int NF>
-__device__ __forceinline__ void face_warp_pcr(const PrecDev& P, const ElimDev& E, int F0, int stride,
+// NF faces per call (F0 + f * stride, f < NF; F >= fend skipped) with every load issued before the first use.
+// KH > 0 (R22 fold): also accumulate this lane's share of the face part of h_t = (M W_t)^T x, i.e.
+// hl[t] += MW_t[i] y_i over the face nodes i it solved, t < kc.
+template <int NF, int KH>
+__device__ __forceinline__ void face_warp_pcr(const PrecDev& P, const ElimDev& E, int F0, int stride, int fend,
                                               const double* __restrict__ b, const double* scl,
-                                              double* __restrict__ y, int lane) {
+                                              double* __restrict__ y, int lane, double* hl = nullptr, int kc = 0) {
     int n[NF], node[NF];
     double co[NF][PCR_Q], x[NF];
 #pragma unroll
     for (int f = 0; f < NF; ++f) {
         const int F = F0 + f * stride;
-        const bool ok = F < E.nfaces;
+        const bool ok = F < fend;
         const int Fc = ok ? F : 0;
         n[f] = ok ? E.tri_n[Fc] : 0;
         node[f] = E.pcr_node[size_t(Fc) * 32 + lane];
@@ -414,6 +416,12 @@ __device__ __forceinline__ void face_warp_pcr(const PrecDev& P, const ElimDev& E
         const double sc = scl[ccomp(P.comp_off, P.ncomp, __shfl_sync(0xffffffffu, node[f], 0))];
         x[f] = lane < n[f] ? sc * b[node[f]] : 0.0;
     }
+    if (KH > 0)   // the fold's M W_t rows of these nodes into L1 now, so their loads after the reduction hit
+#pragma unroll
+        for (int f = 0; f < NF; ++f)
+            if (lane < n[f])
+                for (int t = 0; t < kc; ++t)
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(P.MW + size_t(t) * P.nflat + node[f]));
 #pragma unroll
     for (int l = 0; l < PCR_L; ++l) {
         const int sg = 1 << l;
@@ -424,8 +432,17 @@ __device__ __forceinline__ void face_warp_pcr(const PrecDev& P, const ElimDev& E
         }
     }
 #pragma unroll
-    for (int f = 0; f < NF; ++f)
-        if (lane < n[f]) y[node[f]] = x[f] * co[f][2 * PCR_L];
+    for (int f = 0; f < NF; ++f) {
+        const double yv = x[f] * co[f][2 * PCR_L];
+        if (lane < n[f]) y[node[f]] = yv;
+        if (KH > 0 && lane < n[f]) {
+            double mw[KH > 0 ? KH : 1];
+#pragma unroll
+            for (int t = 0; t < KH; ++t) mw[t] = t < kc ? P.MW[size_t(t) * P.nflat + node[f]] : 0.0;
+#pragma unroll
+            for (int t = 0; t < KH; ++t) hl[t] = fma(mw[t], yv, hl[t]);
+        }
+    }
 }
 
 // x = X^-1 (scl * b) by exact elimination (faces -> cross points -> faces); 3 grid barriers.
@@ -433,7 +450,7 @@ __device__ __forceinline__ void face_warp_pcr(const PrecDev& P, const ElimDev& E
 // (b = M W_{j-1} raw), and the second phase accumulates the block partials of h_t = (M W_t) . x for t < kc,
 // x = X^-1 (scl b) = y - G x_C (R22): h_t = sum_i MW_t[i] y_i + sum_k (MW_t[cf_k] - u_t[k]) x_C[k],
 // written to the reduction slots (pp, c, 1 + t) like block_partials.
-template <bool TIM>
+template <int KM, bool TIM>
 __device__ void elim_coop(cg::grid_group& grid, const CoopArgs& a, const ElimDev& E, const double* b,
                           const double* scl, double* out, double* dsm, int c, int lb, int nbc, int& stamp,
                           int fold_j = 0, int kc = 0, int pp = 0, int64_t r0 = 0, int64_t rs = 1) {
@@ -449,9 +466,24 @@ __device__ void elim_coop(cg::grid_group& grid, const CoopArgs& a, const ElimDev
     double* xC = P.y + P.nflat;
     double* wsm = dsm + size_t(w > 0 ? w - 1 : 0) * a.per_warp;   // warp 0 (barrier host) does no face solves
     long long tf0 = clock64();
-    if (E.tri && E.fuse) {   // warp per face (PCR); each face lies in one component
-        if (w > 0)
-            for (int F = gw; F < E.nfaces; F += 2 * nwarps) face_warp_pcr<2>(P, E, F, nwarps, b, scl, y, lane);
+    if (E.tri && E.fuse) {   // warp per face (PCR); each face lies in one component, solved by that component's blocks
+        const int lw = (w - 1) * nbc + lb, nwc = (CW - 1) * nbc;
+        const int fb = E.face_comp_off[c], fe = E.face_comp_off[c + 1];
+        if (fold_j > 0) {   // R22: the face part of h_t = (M W_t)^T x summed here, where y_F is in registers
+            double hl[KM];
+#pragma unroll
+            for (int t = 0; t < KM; ++t) hl[t] = 0.0;
+            if (w > 0)
+                for (int F = fb + lw; F < fe; F += 2 * nwc) face_warp_pcr<2, KM>(P, E, F, nwc, fe, b, scl, y, lane, hl, kc);
+            double* hfw = dsm + FOLD_OFF + KMAX * CT;   // [CW][KMAX] warp sums, read after the barrier
+#pragma unroll
+            for (int t = 0; t < KM; ++t) {
+                const double v = warp_sum(hl[t]);
+                if (lane == 0) hfw[w * KMAX + t] = v;
+            }
+        } else if (w > 0) {
+            for (int F = fb + lw; F < fe; F += 2 * nwc) face_warp_pcr<2, 0>(P, E, F, nwc, fe, b, scl, y, lane);
+        }
         // t_C = scale (b_C - G^T b_F) once per cross point (needs only b), two cross points per warp in flight
         if (w > 0) {
             double* tCg = P.y + P.nflat + E.ncross;
@@ -561,20 +593,24 @@ __device__ void elim_coop(cg::grid_group& grid, const CoopArgs& a, const ElimDev
             if (dbg2) a.timers[181] = gtimer();
             const double* S = E.Sinv + E.sc_off[c];
 
-            // block lb owns the contiguous rows [rlo, rhi); warp w takes one column slice of all of them (two
-            // rows at a time, NA loads per row per lane in flight); warp partials are summed in fixed order
+            // block lb owns the contiguous rows [rlo, rhi); warp w takes one column slice of all of them (RB rows
+            // at a time, NA loads per row per lane in flight: RB * NA independent loads per batch, so a block's
+            // ~13 rows (c5) take 4 dependent batches instead of 7); warp partials are summed in fixed order
             const int rlo = int(int64_t(lb) * ncc / nbc), rhi = int(int64_t(lb + 1) * ncc / nbc), nr = rhi - rlo;
             const int cw = ((ncc + CW * 32 - 1) / (CW * 32)) * 32;
             const int c0 = w * cw, c1 = min(ncc, c0 + cw);
             double* part = tC + ncc;   // [CW][nr]
-            constexpr int NA = 8;
-            for (int r = rlo; r < rhi; r += 2) {
-                const bool two = r + 1 < rhi;
-                const double* __restrict__ row0 = S + size_t(r) * ncc;
-                const double* __restrict__ row1 = S + size_t(two ? r + 1 : r) * ncc;
-                double s0 = 0.0, s1 = 0.0;
+            constexpr int NA = 8, RB = 4;
+            for (int r = rlo; r < rhi; r += RB) {
+                const double* __restrict__ row[RB];
+                double sr[RB];
+#pragma unroll
+                for (int u = 0; u < RB; ++u) {
+                    row[u] = S + size_t(r + u < rhi ? r + u : r) * ncc;
+                    sr[u] = 0.0;
+                }
                 for (int j = c0 + lane; j < c1; j += 32 * NA) {
-                    double v0[NA], v1[NA], t[NA];
+                    double v[RB][NA], t[NA];
 #pragma unroll
                     for (int q = 0; q < NA; ++q) {
                         const int jj = j + 32 * q;
@@ -582,21 +618,19 @@ __device__ void elim_coop(cg::grid_group& grid, const CoopArgs& a, const ElimDev
                         // streamed once per step (evict-first); a shared S_C^-1 (HElim::sc_shared) is read by the
                         // blocks of every component at about the same time, and evict-first lines still serve the
                         // partner (measured: L2-cached loads evict the basis and are slower)
-                        v0[q] = ok ? __ldcs(row0 + jj) : 0.0;
-                        v1[q] = (ok && two) ? __ldcs(row1 + jj) : 0.0;
+#pragma unroll
+                        for (int u = 0; u < RB; ++u) v[u][q] = (ok && r + u < rhi) ? __ldcs(row[u] + jj) : 0.0;
                         t[q] = ok ? tC[jj] : 0.0;
                     }
 #pragma unroll
-                    for (int q = 0; q < NA; ++q) {
-                        s0 += v0[q] * t[q];
-                        s1 += v1[q] * t[q];
-                    }
+                    for (int q = 0; q < NA; ++q)
+#pragma unroll
+                        for (int u = 0; u < RB; ++u) sr[u] += v[u][q] * t[q];
                 }
-                s0 = warp_sum(s0);
-                s1 = warp_sum(s1);
-                if (lane == 0) {
-                    part[w * nr + (r - rlo)] = s0;
-                    if (two) part[w * nr + (r + 1 - rlo)] = s1;
+#pragma unroll
+                for (int u = 0; u < RB; ++u) {
+                    const double su = warp_sum(sr[u]);
+                    if (lane == 0 && r + u < rhi) part[w * nr + (r + u - rlo)] = su;
                 }
             }
             if (dbg2) a.timers[182] = gtimer();
@@ -620,20 +654,19 @@ __device__ void elim_coop(cg::grid_group& grid, const CoopArgs& a, const ElimDev
         }
         if (fold_j > 0) {
             double* hacc = dsm + FOLD_OFF;
+            const double* hfw = dsm + FOLD_OFF + KMAX * CT;   // the face part, summed per warp in the face phase
             if (ncc <= 0)
                 for (int t = 0; t < KMAX; ++t) hacc[t * CT + threadIdx.x] = 0.0;
-            // face part: sum_i MW_t[i] y_i over this block's rows (y = 0 on cross rows)
-            for (int64_t i = r0; i < P.comp_off[c + 1]; i += rs) {
-                const double yi = y[i];
-                for (int t = 0; t < kc; ++t) hacc[t * CT + threadIdx.x] += P.MW[size_t(t) * P.nflat + i] * yi;
-            }
             __syncthreads();
-            // block sums (fixed order) into the reduction slots (pp, c, 1 + t); slot 0 (unused) = 0
+            // block sums (fixed order: cross part over threads, then the face part over warps) into the reduction
+            // slots (pp, c, 1 + t); slot 0 (unused) = 0
             for (int v = w; v <= kc; v += CW) {
                 double t_ = 0.0;
                 if (v > 0)
                     for (int q = 0; q < CW; ++q) t_ += hacc[(v - 1) * CT + q * 32 + lane];
                 t_ = warp_sum(t_);
+                if (v > 0)
+                    for (int q = 1; q < CW; ++q) t_ += hfw[q * KMAX + v - 1];
                 if (lane == 0) a.red[((size_t(pp) * MAXC + c) * NRED + v) * a.nbc_max + lb] = t_;
             }
             __syncthreads();
@@ -934,7 +967,7 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
     // Basis vectors are stored unnormalised (W_t = sclh_t * Wraw_t, likewise M W_t and L W_t): every
     // consumer folds sclh_t into its coefficients, so no normalisation pass over the rows is needed.
     // ---- s = M^-1 r (exact) = Wraw_0
-    elim_coop<TIM>(grid, a, P.eM, P.rf, scl, P.W, dsm, c, lb, nbc, stamp);
+    elim_coop<KM, TIM>(grid, a, P.eM, P.rf, scl, P.W, dsm, c, lb, nbc, stamp);
     // ---- Ms, Ls, ||s||_M; q_1 = s / ||s||_M; rhs of the next solve M q_1 = Ms / ||s||_M
     ZERO_VALS();
     double* gacc = dsm;   // per-thread Gram accumulators [GW][CT] (dsm is free outside face solves / Ritz)
@@ -977,7 +1010,7 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
     const bool fuseK = P.eK.tri && P.eK.fuse;
     for (int j = 1; j < P.kmax; ++j) {
         const bool fold = a.fold && fuseK;   // h summed inside the elimination (R22): no phase A, no barrier
-        elim_coop<TIM>(grid, a, P.eK, j == 1 ? P.MW : P.Mw, scl, P.w, dsm, c, lb, nbc, stamp,
+        elim_coop<KM, TIM>(grid, a, P.eK, j == 1 ? P.MW : P.Mw, scl, P.w, dsm, c, lb, nbc, stamp,
                        fold ? j : 0, kcs[c], pp, r0, rs);   // w = K^-1 M q_j
         const bool part = act[c] && !brk[c];
         const int kc = kcs[c];
@@ -1326,7 +1359,7 @@ bool prec_coop_prepare(const PrecDev& P, int device, CoopBuffers& B) {
     // fold h into the elimination (R22): 2D fused eliminations, one-pass Gram-Schmidt, room for the accumulators
     B.fold = (B.gram_cgs2 && P.eK.tri && P.eK.fuse && !getenv("DE_NO_FOLD") &&
               size_t(ncmax) + size_t(CW) * B.nbc_max + 2 <= size_t(FOLD_OFF) &&
-              (size_t(FOLD_OFF) + size_t(KMAX) * CT) * 8 <= B.smem) ? 1 : 0;
+              (size_t(FOLD_OFF) + size_t(KMAX) * CT + size_t(CW) * KMAX) * 8 <= B.smem) ? 1 : 0;
     if (getenv("DE_VERBOSE")) fprintf(stderr, "[de] k_prec_coop: fold %d (R22)\n", B.fold);
     return true;
 }
