@@ -4,11 +4,14 @@
 A "step" is one pass of the whole hot path over one batch of synthetic input: the BASELINE
 config-5 topology-optimisation sequence step (2048x1024 Q1 elements, 64x32 subdomains): new
 densities (seeded +-5 % perturbation, clipped) -> de_factor (SIMP assembly + 2048 band Cholesky
-factorisations) -> warm-started de_solve (condense, interface PCG with the inverse-Lanczos
-H^_theta preconditioner to rtol 1e-10, back-substitution, true residual).
-value = n_free * (PCG iterations) / step time / 1e6 over the K timed steps (whole job, all ranks).
+factorisations + explicit local Schur complements) -> warm-started de_solve (condense, interface PCG
+with the inverse-Lanczos H^_theta preconditioner to rtol 1e-10, double-double refinement, back-substitution,
+true residual). Every step must return DE_OK (R17); failures are recorded in the line.
+value = n_free * (PCG iterations) / step time / 1e6 over the K timed steps (whole job, all ranks),
+timed with kernel profiling off; the roofline's per-launch times come from separate profiled steps.
+cpu_baseline / --impl reference: the oracle on all host cores (bench_oracle.py).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--impl native|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5|c4] [--impl native|reference]
 Multi-GPU: launched by torch.distributed.run; ranks shard subdomain columns, NCCL allreduce.
 """
 from __future__ import annotations

@@ -166,9 +166,15 @@ de_status_t de_setup(const de_mesh_t* mesh, const double* density, double E0, do
                      double p, double nu, const de_partition_t* part, const de_options_t* opt,
                      de_ctx_t** out);
 
-/* Replace the element densities (host array, prod(nel)); de_factor must be called next. */
+/* Replace the element densities rho_e (host array, prod(nel), element order of the header comment; every value
+ * positive and finite, else DE_EINVAL). The stiffness K(rho) = sum_e E_e(rho_e) K_e^0 changes with them
+ * (Eq. (10), read as SIMP: DESIGN.md R1); this is the density update of the topology-optimisation
+ * loop between two analyses (BASELINE config 5). Copies the array; the context is marked
+ * unfactored, so de_factor must be called before the next de_solve (else DE_ESTATE). With weighted_trace the
+ * preconditioner is rebuilt by that de_factor (R19). */
 de_status_t de_update_densities(de_ctx_t* ctx, const double* density);
-/* Same with a device pointer (float64, prod(nel)) on options.device. */
+/* Same with a device pointer (float64, prod(nel)) on options.device, borrowed for the call (stream-ordered copy);
+ * the values are not validated on the host. */
 de_status_t de_update_densities_device(de_ctx_t* ctx, const double* d_density);
 
 /* SIMP scaling + subdomain blocks A_II (band), A_IG, A_GG (ring) + batched band Cholesky
@@ -201,6 +207,11 @@ de_status_t de_get_skeleton(const de_ctx_t* ctx, int32_t c, int32_t* nodes, int3
  * to query the count; available for host_only contexts as well. */
 de_status_t de_get_owned(const de_ctx_t* ctx, int32_t* ids, int32_t* n);
 
+/* Fill *stats with the sizes of this context (dof counts, interface skeleton per component: SURVEY.md Appendix A
+ * quantities) and the figures of the last de_factor / de_solve (iterations, residuals, times,
+ * the algorithmic byte counts of SURVEY.md §8(d) used by bench.py's rooflines). Host bookkeeping, except that with
+ * inner_mode 0 the inner face-PCG iteration counter is read from the device (a stream synchronisation).
+ * DE_EINVAL on null arguments. */
 de_status_t de_get_stats(const de_ctx_t* ctx, de_stats_t* stats);
 
 /* ---- component-level entry points (parity tests and profiling) --------------------------

@@ -436,6 +436,7 @@ de_status_t upload_prec_impl(de_ctx* c) {
     P.ncomp = hs.ncomp;
     P.nflat = int32_t(hs.comp_off[hs.ncomp]);
     P.kmax = std::min(std::max(1, c->opt.lanczos_k), KMAX);
+    P.jacobi_reg = getenv("DE_JACOBI_REG") ? 1 : 0;
     for (int i = 0; i <= MAXC; ++i) P.comp_off[i] = hs.comp_off[std::min(i, hs.ncomp)];
     for (int i = 0; i < MAXC; ++i) P.singular[i] = (hs.singular_mask >> i) & 1;
     P.theta = c->opt.theta;
@@ -508,6 +509,26 @@ de_status_t upload_prec_impl(de_ctx* c) {
         for (int cc = 0; cc < (E.sc_shared ? 1 : hs.ncomp); ++cc) {   // S_C^-1 by Gauss-Jordan (setup only)
             const int nc = E.cross_comp_off[cc + 1] - E.cross_comp_off[cc];
             if (nc > 0) launch_gauss_jordan(D.Sinv + E.sc_off[cc], gjbuf, nc, c->st);
+        }
+        {   // padded X_CF for the general (non-tridiagonal) path
+            int w = 0;
+            for (int ci = 0; ci < E.ncross; ++ci) w = std::max(w, E.XCF.ptr[ci + 1] - E.XCF.ptr[ci]);
+            w = (w + 7) / 8 * 8;
+            D.xcf_w = 0;
+            D.xcfw_col = nullptr;
+            D.xcfw_val = nullptr;
+            if (w > 0 && w <= 64 && E.ncross > 0) {
+                std::vector<int32_t> wc(size_t(w) * E.ncross, 0);
+                std::vector<double> wv(size_t(w) * E.ncross, 0.0);
+                for (int ci = 0; ci < E.ncross; ++ci)
+                    for (int e = E.XCF.ptr[ci], k = 0; e < E.XCF.ptr[ci + 1]; ++e, ++k) {
+                        wc[size_t(k) * E.ncross + ci] = E.XCF.col[e];
+                        wv[size_t(k) * E.ncross + ci] = E.XCF.val[e];
+                    }
+                TRY(dupload(c, &D.xcfw_col, wc));
+                TRY(dupload(c, &D.xcfw_val, wv));
+                D.xcf_w = w;
+            }
         }
         // face-interleaved tridiagonal copy (2D faces are paths): coalesced thread-per-face solves
         D.tri = 1;
@@ -591,6 +612,40 @@ de_status_t upload_prec_impl(de_ctx* c) {
             TRY(dupload(c, &D.g_c1, gc1));
             TRY(dupload(c, &D.g_v0, gv0));
             TRY(dupload(c, &D.g_v1, gv1));
+            D.fell_col = nullptr;
+            if (&D == &P.eK && !getenv("DE_NO_FELL")) {   // fold ELL of the M/L rows with eK's couplings
+                const HCsr& Mh = hs.M;
+                const HCsr& Lh = hs.L;
+                std::vector<int32_t> fc(FELL_W * nfl, 0), f0(FELL_W * nfl, 0), f1(FELL_W * nfl, 0);
+                std::vector<double> v0(FELL_W * nfl, 0.0), v1(FELL_W * nfl, 0.0), fm(FELL_W * nfl, 0.0),
+                    fl(FELL_W * nfl, 0.0);
+                for (size_t i = 0; i < nfl; ++i) {
+                    const int e0 = Mh.ptr[i], e1 = Mh.ptr[i + 1];
+                    if (e1 - e0 > FELL_W) {
+                        fc[i] = -1;   // CSR fallback (cross points with > FELL_W neighbours)
+                        continue;
+                    }
+                    for (int k = 0; k < FELL_W; ++k) {
+                        const size_t at = size_t(k) * nfl + i;
+                        const int e = e0 + k;
+                        const int col = e < e1 ? Mh.col[e] : int(i);
+                        fc[at] = col;
+                        f0[at] = gc0[col];
+                        f1[at] = gc1[col];
+                        v0[at] = gv0[col];
+                        v1[at] = gv1[col];
+                        fm[at] = e < e1 ? Mh.val[e] : 0.0;
+                        fl[at] = e < e1 ? Lh.val[e] : 0.0;
+                    }
+                }
+                TRY(dupload(c, &D.fell_col, fc));
+                TRY(dupload(c, &D.fell_c0, f0));
+                TRY(dupload(c, &D.fell_c1, f1));
+                TRY(dupload(c, &D.fell_v0, v0));
+                TRY(dupload(c, &D.fell_v1, v1));
+                TRY(dupload(c, &D.fell_m, fm));
+                TRY(dupload(c, &D.fell_l, fl));
+            }
             D.fuse = getenv("DE_NO_E3_FUSE") ? 0 : 1;
             std::vector<int32_t> x4c(size_t(XCF_W) * E.ncross, 0);
             std::vector<double> x4v(size_t(XCF_W) * E.ncross, 0.0);

@@ -191,6 +191,11 @@ struct ElimDev {
     // X_CF padded to XCF_W entries per cross point ([XCF_W][ncross], col 0 / val 0 padding), tri only
     int32_t* xcf4_col;
     double* xcf4_val;
+    // X_CF padded to xcf_w entries per cross point ([xcf_w][ncross], col 0 / val 0 padding), non-tri (3D): the
+    // per-block t_C formation issues every load of a chunk together instead of walking CSR rows
+    int32_t xcf_w;
+    int32_t* xcfw_col;
+    double* xcfw_val;
     // warp-per-face parallel cyclic reduction of X_FF y = b (tri only): lane j = face node j, 32 lanes per face
     // (identity rows past the face end); per face [PCR_Q][32] doubles: (alpha, gamma) of the 5 reduction
     // levels, then 1/d after the last level; pcr_node[F*32 + j] = flat index (0 past the end)
@@ -200,7 +205,14 @@ struct ElimDev {
     // the right-hand side, so the first face phase forms it once per component (fuse only)
     int32_t *gt_ptr, *gt_col;
     double* gt_val;
+    // fold ELL (fuse only, eK): rows of M and L with <= FELL_W entries, every entry carrying its column's
+    // elimination couplings, so the consumer's x = y - G x_C of each neighbour is two dependent load levels
+    // instead of four (CSR ptr -> col -> g[col] -> xC[g]); [FELL_W][nflat] each; fell_col[0][i] = -1: CSR row
+    int32_t* fell_col;
+    int32_t *fell_c0, *fell_c1;
+    double *fell_v0, *fell_v1, *fell_m, *fell_l;
 };
+constexpr int FELL_W = 3;
 constexpr int PCR_L = 5;             // log2(32) reduction levels
 constexpr int PCR_Q = 2 * PCR_L + 1;
 constexpr int XCF_W = 4;
@@ -332,6 +344,7 @@ void launch_zero_dirichlet(const int8_t* cls, double* u, int64_t ndof, cudaStrea
 // preconditioner
 struct PrecDev {
     int32_t ncomp, nflat, kmax;
+    int32_t jacobi_reg;         // 1: the register Jacobi of the Ritz step (A/B switch DE_JACOBI_REG), else shared-memory
     int32_t max_face_band;      // max half bandwidth over all face blocks (1: tridiagonal, 2D)
     int64_t comp_off[MAXC + 1];
     int32_t singular[MAXC];

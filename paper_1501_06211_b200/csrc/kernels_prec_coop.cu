@@ -242,6 +242,39 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 
+// spmv_elim through the fold ELL (ElimDev::fell_*): all entry data of row i in one level, then y / x_C in the
+// second; rows flagged -1 take the CSR path. Same arithmetic and summation order as spmv_elim.
+__device__ __forceinline__ double spmv_elim_fell(const CsrDev& M, const CsrDev& L, int64_t i, const ElimDev& E,
+                                                 const double* __restrict__ y, const double* __restrict__ xC,
+                                                 int64_t nfl, double& yM, double& yL) {
+    const int c0 = E.fell_col[i];
+    if (c0 < 0) return spmv_elim(M, L, i, E, y, xC, yM, yL);
+    int col[FELL_W], g0[FELL_W], g1[FELL_W];
+    double v0[FELL_W], v1[FELL_W], mv[FELL_W], lv[FELL_W];
+#pragma unroll
+    for (int k = 0; k < FELL_W; ++k) {
+        const int64_t at = k * nfl + i;
+        col[k] = k == 0 ? c0 : E.fell_col[at];
+        g0[k] = E.fell_c0[at];
+        g1[k] = E.fell_c1[at];
+        v0[k] = E.fell_v0[at];
+        v1[k] = E.fell_v1[at];
+        mv[k] = E.fell_m[at];
+        lv[k] = E.fell_l[at];
+    }
+    double am = 0.0, al = 0.0, xi = 0.0;
+#pragma unroll
+    for (int k = 0; k < FELL_W; ++k) {
+        const double x = y[col[k]] - v0[k] * xC[g0[k]] - v1[k] * xC[g1[k]];
+        am += mv[k] * x;
+        al += lv[k] * x;
+        if (col[k] == i) xi = x;   // padding repeats column i: the same value
+    }
+    yM = am;
+    yL = al;
+    return xi;
+}
+
 // Warp solve of one face block (L then M = P L^T P forward sweeps, b <= 31, row window in registers).
 // rhs = scale * b_F (mode 0) or scale * b_F - X_FC xC (mode 1). The factor columns stream through a two-chunk
 // shared-memory ring (32 columns per chunk, cp.async issued one chunk ahead), so no load sits on the per-row
@@ -581,6 +614,44 @@ __device__ void elim_coop(cg::grid_group& grid, const CoopArgs& a, const ElimDev
                         if (i < ncc) tC[i + rot < ncc ? i + rot : i + rot - ncc] = t;
                     }
                 }
+            } else if (E.xcf_w > 0) {   // padded X_CF (3D): UC rows per thread, every load of an 8-entry chunk together
+                constexpr int UC = 2, CH = 8;
+                const double sc = scl[c];
+                const int rot = int((int64_t(lb) * 224) % ncc);   // blocks start at different rows (L2 queuing)
+                for (int i0 = threadIdx.x; i0 < ncc; i0 += CT * UC) {
+                    int ci[UC], ii[UC];
+                    double acc[UC];
+#pragma unroll
+                    for (int u = 0; u < UC; ++u) {
+                        const int i = i0 + u * CT;
+                        ii[u] = i < ncc ? (i + rot < ncc ? i + rot : i + rot - ncc) : -1;
+                        ci[u] = base + (ii[u] >= 0 ? ii[u] : 0);
+                        acc[u] = ii[u] >= 0 ? sc * b[E.cross_flat[ci[u]]] : 0.0;
+                    }
+                    for (int k0 = 0; k0 < E.xcf_w; k0 += CH) {
+                        int col[UC][CH];
+                        double v[UC][CH], yv[UC][CH];
+#pragma unroll
+                        for (int u = 0; u < UC; ++u)
+#pragma unroll
+                            for (int q = 0; q < CH; ++q) {
+                                const size_t at = size_t(k0 + q) * E.ncross + ci[u];
+                                col[u][q] = E.xcfw_col[at];
+                                v[u][q] = E.xcfw_val[at];
+                            }
+#pragma unroll
+                        for (int u = 0; u < UC; ++u)
+#pragma unroll
+                            for (int q = 0; q < CH; ++q) yv[u][q] = y[col[u][q]];
+#pragma unroll
+                        for (int u = 0; u < UC; ++u)
+#pragma unroll
+                            for (int q = 0; q < CH; ++q) acc[u] -= v[u][q] * yv[u][q];
+                    }
+#pragma unroll
+                    for (int u = 0; u < UC; ++u)
+                        if (ii[u] >= 0) tC[ii[u]] = acc[u];
+                }
             } else {
                 for (int i = threadIdx.x; i < ncc; i += CT) {
                     const int ci = base + i;
@@ -808,11 +879,121 @@ __device__ int jacobi_reg(double* C, double* V, int n) {
     return nsw;
 }
 
+// Cyclic parallel Jacobi on the symmetric n x n matrix C in shared memory (leading dim KMAX+1), eigenvectors
+// accumulated into V (shared, starts as I); one warp. The same rotations and ordering as jacobi_reg (pairs of the
+// circle method on M = n rounded up to even slots, the small-angle rotation from two rsqrt), but every round is
+// one data-parallel update of all entries: lanes 0..M/2-1 form the M/2 rotations, then each lane rewrites its
+// share of C <- J^T C J and V <- V J from four (two) shared loads per entry. A round costs a few shared-memory
+// latencies instead of ~30 dependent shuffles (jacobi_reg). Returns the sweep count.
+template <int M>
+__device__ int jacobi_smem(double* C, double* V, int n, double* rot) {
+    constexpr int LDK = KMAX + 1, H = M / 2, NE = (M * M + 31) / 32;
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    double* cs = rot;            // [H]
+    double* sn = rot + H;        // [H]
+    if (n < M) {                 // ghost slot of odd n: a decoupled zero row/column
+        for (int i = lane; i < M; i += 32) {
+            C[(M - 1) * LDK + i] = 0.0;
+            C[i * LDK + (M - 1)] = 0.0;
+            V[(M - 1) * LDK + i] = i == M - 1 ? 1.0 : 0.0;
+            V[i * LDK + (M - 1)] = i == M - 1 ? 1.0 : 0.0;
+        }
+        __syncwarp();
+    }
+    int perm[M];                 // perm[pos] = index at slot pos; pairs (perm[2k], perm[2k+1])
+#pragma unroll
+    for (int p = 0; p < M; ++p) perm[p] = p;
+    int nsw = 0;
+    for (int sweep = 0; sweep < 30; ++sweep) {
+        double off = 0.0, dia = 0.0;
+        for (int e = lane; e < M * M; e += 32) {
+            const int i = e / M, j = e - i * M;
+            const double x = C[i * LDK + j];
+            if (i == j) dia += x * x;
+            else off += x * x;
+        }
+        off = warp_sum(off);
+        dia = warp_sum(dia);
+        if (off <= 1e-24 * dia) break;   // ||offdiag||_F <= 1e-12 ||diag||_F (as jacobi_reg)
+        ++nsw;
+        const double thr = 1e-15 * sqrt(dia);
+        int rotated = 0;
+        for (int rnd = 0; rnd < M - 1; ++rnd) {
+            int inv[M];          // slot of each index
+#pragma unroll
+            for (int p = 0; p < M; ++p) inv[perm[p]] = p;
+            if (lane < H) {
+                int p_ = 0, q_ = 0;
+#pragma unroll
+                for (int k = 0; k < H; ++k)
+                    if (k == lane) {
+                        p_ = perm[2 * k];
+                        q_ = perm[2 * k + 1];
+                    }
+                const double app = C[p_ * LDK + p_], aqq = C[q_ * LDK + q_], apq = C[p_ * LDK + q_];
+                double c_ = 1.0, s_ = 0.0;
+                if (fabs(apq) > thr && fabs(apq) > 1e-300) {
+                    const double d = aqq - app;
+                    const double ir = rsqrt(fma(d, d, 4.0 * apq * apq));
+                    const double h = 0.5 * fma(fabs(d), ir, 1.0);
+                    const double ih = rsqrt(h);
+                    c_ = h * ih;
+                    s_ = (d >= 0.0 ? apq : -apq) * ir * ih;
+                }
+                cs[lane] = c_;
+                sn[lane] = s_;
+            }
+            __syncwarp();
+            rotated |= __any_sync(FULL, lane < H && sn[lane < H ? lane : 0] != 0.0);
+            double nc[NE], nv[NE];
+#pragma unroll
+            for (int u = 0; u < NE; ++u) {
+                const int e = lane + 32 * u;
+                nc[u] = 0.0;
+                nv[u] = 0.0;
+                if (e < M * M) {
+                    const int i = e / M, j = e - i * M;
+                    const int si = inv[i], sj = inv[j];
+                    const int ki = si >> 1, kj = sj >> 1;
+                    const int pi = perm[si & ~1], qi = perm[si | 1], pj = perm[sj & ~1], qj = perm[sj | 1];
+                    // J column t of pair k: (J[p][t], J[q][t]) = (c, -s) for t = p, (s, c) for t = q
+                    const double ci_ = cs[ki], si_ = sn[ki], cj_ = cs[kj], sj_ = sn[kj];
+                    const double ap = (si & 1) ? si_ : ci_, aq = (si & 1) ? ci_ : -si_;
+                    const double bp = (sj & 1) ? sj_ : cj_, bq = (sj & 1) ? cj_ : -sj_;
+                    const double cpp = C[pi * LDK + pj], cpq = C[pi * LDK + qj], cqp = C[qi * LDK + pj],
+                                 cqq = C[qi * LDK + qj];
+                    nc[u] = ap * (cpp * bp + cpq * bq) + aq * (cqp * bp + cqq * bq);
+                    nv[u] = V[i * LDK + pj] * bp + V[i * LDK + qj] * bq;
+                }
+            }
+            __syncwarp();
+#pragma unroll
+            for (int u = 0; u < NE; ++u) {
+                const int e = lane + 32 * u;
+                if (e < M * M) {
+                    const int i = e / M, j = e - i * M;
+                    C[i * LDK + j] = nc[u];
+                    V[i * LDK + j] = nv[u];
+                }
+            }
+            __syncwarp();
+            int np[M];   // next pairing: the slot contents move by the circle map
+#pragma unroll
+            for (int p = 0; p < M; ++p) np[p] = perm[circle_src(p, M)];
+#pragma unroll
+            for (int p = 0; p < M; ++p) perm[p] = np[p];
+        }
+        if (!rotated) break;
+    }
+    return nsw;
+}
+
 // One warp: generalized eigenproblem A y = theta B y (n <= KMAX) and coef = Y f(Theta) Y^T wr.
 // Returns false on a non-SPD B or a non-positive Ritz value (non-singular component).
 __device__ bool ritz_warp(const double* Ain, const double* Bin, const double* wr, int n, bool sing, double theta,
                           double* coef, double* R, double* C, double* V, double* X, double* rot, int* rpq,
-                          unsigned long long* tm = nullptr) {
+                          unsigned long long* tm = nullptr, int use_reg = 0) {
     const int lane = threadIdx.x & 31;
     if (tm && lane == 0) tm[0] = gtimer();
     constexpr int LDK = KMAX + 1;
@@ -867,7 +1048,19 @@ __device__ bool ritz_warp(const double* Ain, const double* Bin, const double* wr
     __syncwarp();
     if (tm && lane == 0) tm[1] = gtimer();
     int nsw = 0;
-    if (n > 1) {
+    double* jsc = rot + KMAX;   // rotation scratch of jacobi_smem (rot itself keeps 1/L_jj)
+    if (n > 1 && !use_reg) {
+        switch ((n + 1) & ~1) {
+            case 2: nsw = jacobi_smem<2>(C, V, n, jsc); break;
+            case 4: nsw = jacobi_smem<4>(C, V, n, jsc); break;
+            case 6: nsw = jacobi_smem<6>(C, V, n, jsc); break;
+            case 8: nsw = jacobi_smem<8>(C, V, n, jsc); break;
+            case 10: nsw = jacobi_smem<10>(C, V, n, jsc); break;
+            case 12: nsw = jacobi_smem<12>(C, V, n, jsc); break;
+            case 14: nsw = jacobi_smem<14>(C, V, n, jsc); break;
+            default: nsw = jacobi_smem<16>(C, V, n, jsc); break;
+        }
+    } else if (n > 1) {
         switch ((n + 1) & ~1) {
             case 2: nsw = jacobi_reg<2>(C, V, n); break;
             case 4: nsw = jacobi_reg<4>(C, V, n); break;
@@ -1146,7 +1339,8 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
                 }
                 double x, m, l;
                 if (fold) {   // the former phase A on the same row: w_i and (M w)_i, (L w)_i by the fused SpMV
-                    x = spmv_elim(P.M, P.L, i, P.eK, P.y, P.y + nf, m, l);
+                    x = P.eK.fell_col ? spmv_elim_fell(P.M, P.L, i, P.eK, P.y, P.y + nf, nf, m, l)
+                                      : spmv_elim(P.M, P.L, i, P.eK, P.y, P.y + nf, m, l);
                     vals[1] += x * m;   // ||w||_M^2 before the orthogonalisation (breakdown test)
                 } else {
                     x = a.gram_cgs2 ? P.w[i] : a.w1[i];
@@ -1267,7 +1461,7 @@ __global__ void __launch_bounds__(32) k_prec_ritz(PrecDev P, const PcgState* s, 
     int* rpq = reinterpret_cast<int*>(rot + KMAX);
     if (TIM && timers && w == 0 && lane == 0) timers[100] = gtimer();
     const bool ok = ritz_warp(zs.A, zs.B, zs.wr, zs.kc, P.singular[w] != 0, P.theta, zs.coef, R, Cm, V, X, rot, rpq,
-                              (TIM && timers && w == 0) ? timers + 102 : nullptr);
+                              (TIM && timers && w == 0) ? timers + 102 : nullptr, P.jacobi_reg);
     if (TIM && timers && w == 0 && lane == 0) timers[101] = gtimer();
     if (!ok && lane == 0) {
         zs.status = DE_EBREAKDOWN;
