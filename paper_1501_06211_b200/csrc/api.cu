@@ -1228,6 +1228,20 @@ de_status_t true_residual(de_ctx* c, const double* d_f, const double* d_u, doubl
     return DE_OK;
 }
 
+// DE_EBREAKDOWN when the last preconditioner application met a non-positive Ritz value or a non-SPD Gram matrix in
+// some component (reading R9); the caller has synchronised the stream
+de_status_t prec_breakdown_status(de_ctx* c) {
+    if (!c->have_prec) return DE_OK;
+    LzState lz[MAXC];
+    DE_CUDA(cudaMemcpy(lz, c->P.lz, sizeof(lz), cudaMemcpyDeviceToHost));
+    for (int cc = 0; cc < c->hs.ncomp; ++cc)
+        if (lz[cc].status == DE_EBREAKDOWN) {
+            set_error("non-positive Ritz value in component %d", cc);
+            return DE_EBREAKDOWN;
+        }
+    return DE_OK;
+}
+
 // z = P~^-1 v on full dof vectors: z_Gamma = S~^-1 v_Gamma (the interface preconditioner),
 // z_I = K_II^-1 (v_I - K_IGamma z_Gamma) (the back-substitution of the Schur kernels), Dirichlet entries 0
 de_status_t prec_full(de_ctx* c, const double* v, double* z) {
@@ -1303,6 +1317,7 @@ de_status_t fgmres_impl(de_ctx* c, const double* d_f, double rtol, double fnorm,
             TRY(check_launch());
             DE_CUDA(cudaMemcpyAsync(hb.data(), hd, sizeof(double) * (2 * FG_ND + 1), cudaMemcpyDeviceToHost, c->st));
             DE_CUDA(cudaStreamSynchronize(c->st));
+            TRY(prec_breakdown_status(c));   // z_Gamma = 0 from a broken-down application is not a direction
             for (int i = 0; i <= j; ++i) H[size_t(i) * m + j] = hb[i] + hb[FG_ND + i];
             H[size_t(j + 1) * m + j] = std::sqrt(std::max(hb[2 * FG_ND], 0.0));
             for (int i = 0; i < j; ++i) {   // previous rotations
@@ -1668,16 +1683,7 @@ de_status_t de_precond_apply_device(de_ctx_t* c, const double* d_r, double* d_z)
     DE_CUDA(cudaSetDevice(c->opt.device));
     TRY(precond(c, d_r, d_z, nullptr, nullptr));
     DE_CUDA(cudaStreamSynchronize(c->st));
-    if (c->have_prec) {
-        LzState lz[MAXC];
-        DE_CUDA(cudaMemcpy(lz, c->P.lz, sizeof(lz), cudaMemcpyDeviceToHost));
-        for (int cc = 0; cc < c->hs.ncomp; ++cc)
-            if (lz[cc].status == DE_EBREAKDOWN) {
-                set_error("non-positive Ritz value in component %d", cc);
-                return DE_EBREAKDOWN;
-            }
-    }
-    return DE_OK;
+    return prec_breakdown_status(c);
 }
 
 de_status_t de_get_factor_band(const de_ctx_t* c, int32_t sl, double* out, int32_t* n_I_s) {
