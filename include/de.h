@@ -154,6 +154,8 @@ typedef struct {
                                 the FP64 rounding floor of the problem (measured for config 5: 1.35e-10) */
     double bytes_prec_min;   /* distinct bytes one preconditioner application touches, each counted once (operators,
                                 r, z, basis written once): the minimum-bytes figure of its roofline */
+    int32_t cross_fd;        /* bit 0 / bit 1: the cross-point Schur complement of the K / M elimination is separable
+                                and solved by fast diagonalisation instead of the dense S_C^-1 (R23) */
 } de_stats_t;
 
 /* Fill *opt with defaults (theta 0.5, k 10, inner_mode 1, max_iter 20000, FR, 1 rank). */

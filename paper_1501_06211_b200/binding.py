@@ -56,7 +56,7 @@ class de_stats_t(C.Structure):
                 ("iterations_pass1", C.c_int32), ("schur_explicit", C.c_int32),
                 ("bytes_schur_explicit", C.c_double),
                 ("bytes_prec", C.c_double), ("inner_iterations", C.c_int64), ("relres_dd", C.c_double),
-                ("bytes_prec_min", C.c_double)]
+                ("bytes_prec_min", C.c_double), ("cross_fd", C.c_int32)]
 
 
 class de_oc_params_t(C.Structure):

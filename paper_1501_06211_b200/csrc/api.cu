@@ -11,6 +11,7 @@
 #include <chrono>
 #include <cmath>
 #include <condition_variable>
+#include <map>
 #include <mutex>
 #include <cstdarg>
 #include <cstdio>
@@ -416,6 +417,7 @@ de_status_t rebuild_weighted_prec(de_ctx* c) {
     hs.trace_E.resize(hs.nelem);
     for (int64_t e = 0; e < hs.nelem; ++e) hs.trace_E[e] = c->Emin + std::pow(rho[e], c->p) * (c->E0 - c->Emin);
     TRY(build_trace(hs, hs.trace_E.data()));
+    c->stats.cross_fd = (hs.elimK.fd ? 1 : 0) | (hs.elimM.fd ? 2 : 0);
     if (c->gexec) {
         cudaGraphExecDestroy(c->gexec);
         c->gexec = nullptr;
@@ -509,6 +511,15 @@ de_status_t upload_prec_impl(de_ctx* c) {
         for (int cc = 0; cc < (E.sc_shared ? 1 : hs.ncomp); ++cc) {   // S_C^-1 by Gauss-Jordan (setup only)
             const int nc = E.cross_comp_off[cc + 1] - E.cross_comp_off[cc];
             if (nc > 0) launch_gauss_jordan(D.Sinv + E.sc_off[cc], gjbuf, nc, c->st);
+        }
+        D.fd = E.fd;   // fast diagonalisation of a separable S_C (HElim::fd): the cooperative kernel's cross-point solve
+        D.fd_nx = E.fd_nx;
+        D.fd_ny = E.fd_ny;
+        D.fd_qx = D.fd_qy = D.fd_il = nullptr;
+        if (E.fd) {
+            TRY(dupload(c, &D.fd_qx, E.fd_qx));
+            TRY(dupload(c, &D.fd_qy, E.fd_qy));
+            TRY(dupload(c, &D.fd_il, E.fd_il));
         }
         {   // padded X_CF for the general (non-tridiagonal) path
             int w = 0;
@@ -699,7 +710,28 @@ de_status_t upload_prec_impl(de_ctx* c) {
                     }
                     for (int j = 0; j < 32; ++j) q[(2 * PCR_L) * 32 + j] = 1.0 / dv[j];
                 }
-                TRY(dupload(c, &D.pcr, pq));
+                // Faces with bitwise-identical coefficient blocks (uniform skeleton: a handful of face types) share one
+                // block, so the per-face coefficient loads hit L1 instead of streaming 11 doubles per node from L2
+                std::vector<double> uq;
+                std::vector<int32_t> nt(E.nfaces, 0);
+                {
+                    std::map<std::vector<double>, int32_t> types;
+                    for (int F = 0; F < E.nfaces; ++F) {
+                        std::vector<double> blk(pq.begin() + size_t(F) * PCR_Q * 32, pq.begin() + size_t(F + 1) * PCR_Q * 32);
+                        auto it = types.find(blk);
+                        int32_t ty;
+                        if (it == types.end()) {
+                            ty = int32_t(types.size());
+                            types.emplace(blk, ty);
+                            uq.insert(uq.end(), blk.begin(), blk.end());
+                        } else {
+                            ty = it->second;
+                        }
+                        nt[F] = (E.face_off[F + 1] - E.face_off[F]) | (ty << 8);
+                    }
+                }
+                TRY(dupload(c, &D.pcr, uq));
+                TRY(dupload(c, &D.pcr_nt, nt));
                 TRY(dupload(c, &D.pcr_node, pn));
             }
             {   // G^T rows per cross point from the per-node couplings (face nodes only; ascending column)
@@ -778,6 +810,8 @@ de_status_t upload_prec_impl(de_ctx* c) {
         TRY(dalloc(c, &c->coop.mw1, nf));
         TRY(dalloc(c, &c->coop.lw1, nf));
         if (c->coop.fold) TRY(dalloc(c, &c->coop.ucross, size_t(KMAX) * std::max(1, P.eK.ncross)));
+        TRY(dalloc(c, &c->coop.arrive, 4));
+        DE_CUDA(cudaMemsetAsync(c->coop.arrive, 0, 4 * sizeof(unsigned int), c->st));
         if (getenv("DE_PREC_TIMERS")) {
             TRY(dalloc(c, &c->coop.timers, 200 + 8192));
             DE_CUDA(cudaMemsetAsync(c->coop.timers, 0, (200 + 8192) * sizeof(unsigned long long), c->st));
@@ -906,6 +940,7 @@ de_status_t setup_impl(const de_mesh_t* mesh, const double* density, double E0, 
     c->stats.n_Gamma = hs.n_G;
     c->stats.n_sub = hs.nsub;
     for (int cc = 0; cc < hs.ncomp; ++cc) c->stats.n_gamma_c[cc] = hs.comp_off[cc + 1] - hs.comp_off[cc];
+    c->stats.cross_fd = (hs.elimK.fd ? 1 : 0) | (hs.elimM.fd ? 2 : 0);
     // ---- ownership: slabs of subdomain columns along x
     const int px = hs.ps[0];
     const int lo = int((int64_t(c->rank) * px) / c->nranks), hi = int((int64_t(c->rank + 1) * px) / c->nranks);

@@ -57,6 +57,13 @@ struct HElim {
     // 1 when every component's S_C is bitwise identical to component 0's (same skeleton and Dirichlet rows:
     // the trace norm is componentwise): one S_C^-1 serves all components
     int32_t sc_shared = 0;
+    // Fast diagonalisation of S_C (2D, R23): when the cross points of every component form a full
+    // nx x ny tensor grid (index = ix + nx iy) and S_C = A_x (x) I + I (x) A_y exactly (uniform skeleton, unweighted
+    // trace norm, Dirichlet rows on whole edges), S_C^-1 = (Q_y (x) Q_x) diag(1 / (lam_a + mu_b)) (Q_y (x) Q_x)^T with
+    // A_x = Q_x diag(lam) Q_x^T, A_y = Q_y diag(mu) Q_y^T. Per stored component (one if sc_shared):
+    // fd_qx [ix][a] (nx x nx), fd_qy [iy][b] (ny x ny), fd_il [a + nx b] = 1 / (lam_a + mu_b).
+    int32_t fd = 0, fd_nx = 0, fd_ny = 0;
+    std::vector<double> fd_qx, fd_qy, fd_il;
 };
 
 struct HostSetup {
@@ -173,6 +180,10 @@ struct ElimDev {
     int64_t sc_off[MAXC + 1];
     double* Sinv;
     int32_t sc_shared;           // 1: all components use the one S_C^-1 at Sinv (HElim::sc_shared)
+    // fast diagonalisation of a separable S_C (HElim::fd): tables of stored component cs at fd_qx + cs nx^2,
+    // fd_qy + cs ny^2, fd_il + cs nx ny (cs = 0 when sc_shared)
+    int32_t fd, fd_nx, fd_ny;
+    double *fd_qx, *fd_qy, *fd_il;
     // face-interleaved tridiagonal copy (2D): 32 faces per group, entry (j, lane) at (g*TRI_N + j)*32 + lane
     int32_t tri;                 // 1 if every face block is tridiagonal with <= TRI_N nodes and <= 2 cross couplings
     int32_t* tri_n;              // [nfaces] nodes per face
@@ -199,7 +210,9 @@ struct ElimDev {
     // warp-per-face parallel cyclic reduction of X_FF y = b (tri only): lane j = face node j, 32 lanes per face
     // (identity rows past the face end); per face [PCR_Q][32] doubles: (alpha, gamma) of the 5 reduction
     // levels, then 1/d after the last level; pcr_node[F*32 + j] = flat index (0 past the end)
+    // faces with bitwise-identical coefficient blocks share one: pcr_nt[F] = nodes | (block id << 8)
     double* pcr;
+    int32_t* pcr_nt;
     int32_t* pcr_node;
     // G^T = X_CF X_FF^-1 as CSR over cross points (face-node columns): t_C = scale (b_C - G^T b_F) needs only
     // the right-hand side, so the first face phase forms it once per component (fuse only)
@@ -374,8 +387,9 @@ void prec_prepare(const PrecDev& P);   // one-time kernel attributes (outside gr
 struct CoopBuffers {
     int nb = 0, nsm = 148;
     size_t smem = 0;
-    int stage = 0, per_warp = 0, mf = 0, ncmax = 0, nbc_max = 0, tridiag = 0, gram_cgs2 = 1, fold = 0;
+    int stage = 0, per_warp = 0, mf = 0, ncmax = 0, nbc_max = 0, tridiag = 0, gram_cgs2 = 1, fold = 0, split = 1;
     double* ucross = nullptr;   // fold: [KMAX][ncross of eK]
+    unsigned int* arrive = nullptr;   // split-phase arrival counter of the fused eliminations (zero between launches)
     double *red = nullptr, *gram = nullptr, *gram_tot = nullptr, *w1 = nullptr, *mw1 = nullptr, *lw1 = nullptr;
     unsigned long long* timers = nullptr;   // phase stamps (diagnostics; env DE_PREC_TIMERS=1)
     const void* kfn = nullptr;              // k_prec_coop instantiation (basis bound, timers)

@@ -152,6 +152,116 @@ void small_band_solve(int n, int b, const double* fac, double* x) {
     }
 }
 
+// Eigen-decomposition of a symmetric n x n matrix (row-major A, destroyed) by cyclic Jacobi: A = Q diag(lam) Q^T,
+// Q row-major [i][a]. Setup only (n = cross points per skeleton line).
+void sym_eig_jacobi(int n, std::vector<double>& A, std::vector<double>& Q, std::vector<double>& lam) {
+    Q.assign(size_t(n) * n, 0.0);
+    for (int i = 0; i < n; ++i) Q[size_t(i) * n + i] = 1.0;
+    for (int sweep = 0; sweep < 60; ++sweep) {
+        double off = 0.0, dia = 0.0;
+        for (int i = 0; i < n; ++i)
+            for (int j = 0; j < n; ++j) (i == j ? dia : off) += A[size_t(i) * n + j] * A[size_t(i) * n + j];
+        if (off <= 1e-32 * dia) break;
+        for (int p = 0; p < n - 1; ++p)
+            for (int q = p + 1; q < n; ++q) {
+                const double apq = A[size_t(p) * n + q];
+                if (apq == 0.0) continue;
+                const double d = A[size_t(q) * n + q] - A[size_t(p) * n + p];
+                const double t = (d >= 0.0 ? 2.0 : -2.0) * apq / (std::fabs(d) + std::sqrt(d * d + 4.0 * apq * apq));
+                const double cs = 1.0 / std::sqrt(1.0 + t * t), sn = t * cs;
+                for (int k = 0; k < n; ++k) {   // columns p, q of A and Q
+                    const double x = A[size_t(k) * n + p], y = A[size_t(k) * n + q];
+                    A[size_t(k) * n + p] = cs * x - sn * y;
+                    A[size_t(k) * n + q] = sn * x + cs * y;
+                    const double u = Q[size_t(k) * n + p], v = Q[size_t(k) * n + q];
+                    Q[size_t(k) * n + p] = cs * u - sn * v;
+                    Q[size_t(k) * n + q] = sn * u + cs * v;
+                }
+                for (int k = 0; k < n; ++k) {   // rows p, q of A
+                    const double x = A[size_t(p) * n + k], y = A[size_t(q) * n + k];
+                    A[size_t(p) * n + k] = cs * x - sn * y;
+                    A[size_t(q) * n + k] = sn * x + cs * y;
+                }
+            }
+    }
+    lam.resize(n);
+    for (int i = 0; i < n; ++i) lam[i] = A[size_t(i) * n + i];
+}
+
+// Fast-diagonalisation tables of a separable S_C (HElim::fd; R23). Leaves E.fd = 0 unless every
+// component's cross points form a full tensor grid in index order and its dense S_C equals the Kronecker sum
+// A_x (x) I + I (x) A_y entry by entry (relative 1e-13), with every lam_a + mu_b > 0.
+void detect_fd(const HostSetup& hs, HElim& E) {
+    E.fd = 0;
+    // Opt-in (env DE_FD=1): measured on B200 (c5) the redundant per-block forward transforms cost 11.4 us per
+    // elimination against 6.7 us for the dense S_C^-1 GEMV stream, although they save 0.3 GB of DRAM traffic per
+    // application (R23)
+    if (hs.dim != 2 || E.ncross == 0 || !getenv("DE_FD")) return;
+    const int nstore = E.sc_shared ? 1 : hs.ncomp;
+    int nx = 0, ny = 0;
+    std::vector<double> qx, qy, il;
+    for (int c = 0; c < hs.ncomp; ++c) {
+        const int32_t base = E.cross_comp_off[c], nc = E.cross_comp_off[c + 1] - base;
+        if (nc < 4) return;
+        std::vector<int> xs, ys;
+        for (int k = 0; k < nc; ++k) {
+            const int64_t node = hs.cnode[E.cross_flat[base + k]];
+            xs.push_back(int(node % hs.nn[0]));
+            ys.push_back(int(node / hs.nn[0]));
+        }
+        std::vector<int> ux(xs), uy(ys);
+        std::sort(ux.begin(), ux.end());
+        ux.erase(std::unique(ux.begin(), ux.end()), ux.end());
+        std::sort(uy.begin(), uy.end());
+        uy.erase(std::unique(uy.begin(), uy.end()), uy.end());
+        const int cnx = int(ux.size()), cny = int(uy.size());
+        if (int64_t(cnx) * cny != nc || (c > 0 && (cnx != nx || cny != ny))) return;
+        nx = cnx;
+        ny = cny;
+        for (int k = 0; k < nc; ++k)
+            if (xs[k] != ux[k % nx] || ys[k] != uy[k / nx]) return;
+        if (c >= nstore) continue;   // shared S_C: tables of component 0 only (grid layout checked for all)
+        const double* S = &E.SC[E.sc_off[c]];
+        auto at = [&](int ix, int iy, int jx, int jy) { return S[size_t(ix + nx * iy) * nc + (jx + nx * jy)]; };
+        std::vector<double> Ax(size_t(nx) * nx, 0.0), Ay(size_t(ny) * ny, 0.0);
+        const double d00 = at(0, 0, 0, 0);
+        for (int ix = 0; ix < nx; ++ix) {
+            Ax[size_t(ix) * nx + ix] = at(ix, 0, ix, 0) - 0.5 * d00;
+            if (ix + 1 < nx) Ax[size_t(ix) * nx + ix + 1] = Ax[size_t(ix + 1) * nx + ix] = at(ix, 0, ix + 1, 0);
+        }
+        for (int iy = 0; iy < ny; ++iy) {
+            Ay[size_t(iy) * ny + iy] = at(0, iy, 0, iy) - 0.5 * d00;
+            if (iy + 1 < ny) Ay[size_t(iy) * ny + iy + 1] = Ay[size_t(iy + 1) * ny + iy] = at(0, iy, 0, iy + 1);
+        }
+        double smax = 0.0;
+        for (size_t e = 0; e < size_t(nc) * nc; ++e) smax = std::max(smax, std::fabs(S[e]));
+        for (int iy = 0; iy < ny; ++iy)
+            for (int ix = 0; ix < nx; ++ix)
+                for (int jy = 0; jy < ny; ++jy)
+                    for (int jx = 0; jx < nx; ++jx) {
+                        const double want = (iy == jy ? Ax[size_t(ix) * nx + jx] : 0.0) + (ix == jx ? Ay[size_t(iy) * ny + jy] : 0.0);
+                        if (std::fabs(at(ix, iy, jx, jy) - want) > 1e-13 * smax) return;
+                    }
+        std::vector<double> Qx, Qy, lam, mu;
+        sym_eig_jacobi(nx, Ax, Qx, lam);
+        sym_eig_jacobi(ny, Ay, Qy, mu);
+        for (int b = 0; b < ny; ++b)
+            for (int a = 0; a < nx; ++a) {
+                const double s = lam[a] + mu[b];
+                if (!(s > 1e-12 * smax)) return;
+                il.push_back(1.0 / s);
+            }
+        qx.insert(qx.end(), Qx.begin(), Qx.end());
+        qy.insert(qy.end(), Qy.begin(), Qy.end());
+    }
+    E.fd = 1;
+    E.fd_nx = nx;
+    E.fd_ny = ny;
+    E.fd_qx.swap(qx);
+    E.fd_qy.swap(qy);
+    E.fd_il.swap(il);
+}
+
 de_status_t build_elim(const HostSetup& hs, const HCsr& X, HElim& E) {
     // faces: grouped per component in (component, face id) order; nodes ascending
     const int64_t nflat = hs.comp_off[hs.ncomp];
@@ -294,6 +404,7 @@ de_status_t build_elim(const HostSetup& hs, const HCsr& X, HElim& E) {
             !std::equal(E.SC.begin() + E.sc_off[c], E.SC.begin() + E.sc_off[c + 1], E.SC.begin()))
             E.sc_shared = 0;
     if (getenv("DE_NO_SC_SHARE")) E.sc_shared = 0;   // A/B switch
+    detect_fd(hs, E);
     return DE_OK;
 }
 

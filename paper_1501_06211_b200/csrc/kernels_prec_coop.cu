@@ -31,7 +31,6 @@ constexpr int NRED = KMAX + 2;
 constexpr int RW = CT - 32;                   // rows per block chunk in row-parallel phases
 constexpr int GW = 2 * KMAX + 1;              // Gram row j: G_L[j][t] (t<=j), G_M[j][t] (KMAX+t), (W^T r)[j] (2 KMAX)
 constexpr int GRAM_TASKS = KMAX * GW;
-constexpr int FOLD_OFF = 4096;                // dsm offset (doubles) of the fold's per-thread h accumulators
 
 struct CoopArgs {
     PrecDev P;
@@ -52,7 +51,10 @@ struct CoopArgs {
     int tridiag;        // 1: every face block is tridiagonal with <= TRI_MAX nodes (2D) -> thread per face
     int gram_cgs2;      // 1: the second Gram-Schmidt pass is formed from the Gram matrix (one row pass fewer)
     int fold;           // 1 (with gram_cgs2, 2D fused eliminations): h = W^T M w is summed inside the elimination
+    int smem_doubles;   // dynamic shared memory of the launch in doubles (fast-diagonalisation tables fit test)
+    int split;          // 1: fused eliminations wait on the arrival counter between t_C and the cross-point solve (no grid barrier)
     double* ucross;     // [KMAX][ncross of eK]: u_t = G^T (M W_t)_F, the face part of M W_t folded onto cross points
+    unsigned int* arrive;   // split-phase arrival counter of the fused eliminations (t_C published -> cross-point solve)
     unsigned long long* timers;   // optional phase timestamps (block 0), DE_PREC_TIMERS
 };
 
@@ -438,9 +440,10 @@ __device__ __forceinline__ void face_warp_pcr(const PrecDev& P, const ElimDev& E
         const int F = F0 + f * stride;
         const bool ok = F < fend;
         const int Fc = ok ? F : 0;
-        n[f] = ok ? E.tri_n[Fc] : 0;
+        const int nt = E.pcr_nt[Fc];
+        n[f] = ok ? (nt & 0xff) : 0;
         node[f] = E.pcr_node[size_t(Fc) * 32 + lane];
-        const double* __restrict__ q = E.pcr + size_t(Fc) * PCR_Q * 32;
+        const double* __restrict__ q = E.pcr + size_t(nt >> 8) * PCR_Q * 32;
 #pragma unroll
         for (int k = 0; k < PCR_Q; ++k) co[f][k] = q[k * 32 + lane];
     }
@@ -485,7 +488,7 @@ __device__ __forceinline__ void face_warp_pcr(const PrecDev& P, const ElimDev& E
 // written to the reduction slots (pp, c, 1 + t) like block_partials.
 template <int KM, bool TIM>
 __device__ void elim_coop(cg::grid_group& grid, const CoopArgs& a, const ElimDev& E, const double* b,
-                          const double* scl, double* out, double* dsm, int c, int lb, int nbc, int& stamp,
+                          const double* scl, double* out, double* dsm, int c, int lb, int nbc, int& stamp, int& nelim,
                           int fold_j = 0, int kc = 0, int pp = 0, int64_t r0 = 0, int64_t rs = 1) {
     const PrecDev& P = a.P;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -499,25 +502,26 @@ __device__ void elim_coop(cg::grid_group& grid, const CoopArgs& a, const ElimDev
     double* xC = P.y + P.nflat;
     double* wsm = dsm + size_t(w > 0 ? w - 1 : 0) * a.per_warp;   // warp 0 (barrier host) does no face solves
     long long tf0 = clock64();
-    if (E.tri && E.fuse) {   // warp per face (PCR); each face lies in one component, solved by that component's blocks
-        const int lw = (w - 1) * nbc + lb, nwc = (CW - 1) * nbc;
-        const int fb = E.face_comp_off[c], fe = E.face_comp_off[c + 1];
-        if (fold_j > 0) {   // R22: the face part of h_t = (M W_t)^T x summed here, where y_F is in registers
-            double hl[KM];
-#pragma unroll
-            for (int t = 0; t < KM; ++t) hl[t] = 0.0;
-            if (w > 0)
-                for (int F = fb + lw; F < fe; F += 2 * nwc) face_warp_pcr<2, KM>(P, E, F, nwc, fe, b, scl, y, lane, hl, kc);
-            double* hfw = dsm + FOLD_OFF + KMAX * CT;   // [CW][KMAX] warp sums, read after the barrier
-#pragma unroll
-            for (int t = 0; t < KM; ++t) {
-                const double v = warp_sum(hl[t]);
-                if (lane == 0) hfw[w * KMAX + t] = v;
-            }
-        } else if (w > 0) {
-            for (int F = fb + lw; F < fe; F += 2 * nwc) face_warp_pcr<2, 0>(P, E, F, nwc, fe, b, scl, y, lane);
+    const bool fused = E.tri && E.fuse;
+    __shared__ double hfw[CW * KMAX];   // fold: the face part of h per warp, read after the cross-point solve
+    // fast-diagonalised cross-point solve (HElim::fd): X, Y and the Q tables must fit the dynamic shared memory
+    const int nccb = E.cross_comp_off[c + 1] - E.cross_comp_off[c];
+    const int fdq = 2 * nccb + (nccb & 1);   // offset of the staged Q tables (16-byte aligned)
+    const bool fd = fused && E.fd && nccb > 0 && fdq + E.fd_nx * E.fd_nx + E.fd_ny * E.fd_ny <= a.smem_doubles;
+    if (fused) {
+        ++nelim;
+        if (fd) {   // stage Qx, Qy behind X / Y now (static tables; dsm is free here): they land during the face solves
+            const int nx = E.fd_nx, ny = E.fd_ny, cs = E.sc_shared ? 0 : c;
+            const double* gx = E.fd_qx + size_t(cs) * nx * nx;
+            const double* gy = E.fd_qy + size_t(cs) * ny * ny;
+            double* sq = dsm + fdq;
+            for (int i = threadIdx.x; i < nx * nx; i += CT) cp_async8(sq + i, gx + i);
+            for (int i = threadIdx.x; i < ny * ny; i += CT) cp_async8(sq + nx * nx + i, gy + i);
+            cp_async_commit();
         }
-        // t_C = scale (b_C - G^T b_F) once per cross point (needs only b), two cross points per warp in flight
+        // t_C = scale (b_C - G^T b_F) once per cross point (needs only b), two cross points per warp in flight.
+        // Formed FIRST and published through a split-phase arrival counter: the cross-point solve below waits for
+        // every block's arrival instead of a grid barrier, and the face solves (which it does not need) run in between.
         if (w > 0) {
             double* tCg = P.y + P.nflat + E.ncross;
             for (int ci0 = gw; ci0 < E.ncross; ci0 += 2 * nwarps) {
@@ -557,14 +561,45 @@ __device__ void elim_coop(cg::grid_group& grid, const CoopArgs& a, const ElimDev
                 }
             }
         }
+        __syncthreads();
+        if (threadIdx.x == 32) {   // publish this block's share of t_C (release: fence, then the arrival)
+            __threadfence();
+            atomicAdd(a.arrive, 1u);
+        }
+        // warp per face (PCR); each face lies in one component, solved by that component's blocks
+        const int lw = (w - 1) * nbc + lb, nwc = (CW - 1) * nbc;
+        const int fb = E.face_comp_off[c], fe = E.face_comp_off[c + 1];
+        if (fold_j > 0) {   // R22: the face part of h_t = (M W_t)^T x summed here, where y_F is in registers
+            double hl[KM];
+#pragma unroll
+            for (int t = 0; t < KM; ++t) hl[t] = 0.0;
+            if (w > 0)
+                for (int F = fb + lw; F < fe; F += 2 * nwc) face_warp_pcr<2, KM>(P, E, F, nwc, fe, b, scl, y, lane, hl, kc);
+#pragma unroll
+            for (int t = 0; t < KM; ++t) {
+                const double v = warp_sum(hl[t]);
+                if (lane == 0) hfw[w * KMAX + t] = v;
+            }
+        } else if (w > 0) {
+            for (int F = fb + lw; F < fe; F += 2 * nwc) face_warp_pcr<2, 0>(P, E, F, nwc, fe, b, scl, y, lane);
+        }
     } else if (E.tri) {
         if (w > 0)
             for (int F = gt; F < E.nfaces; F += nthr) face_thread_tridiag(a, E, F, b, scl, nullptr, y, 0, dsm + (threadIdx.x - 32));
     } else if (w > 0)
         for (int F = gw; F < E.nfaces; F += nwarps) face_warp(a, E, F, b, scl, nullptr, y, 0, wsm, lane);
     if (TIM && a.timers && lane == 0 && w > 0 && gw < 4096) a.timers[200 + gw] = clock64() - tf0;
-    grid.sync();
-    __syncwarp();   // lane 0 spun in the barrier: reconverge before warp-synchronous code
+    if (fused && a.split) {   // wait for every block's t_C (published before its face solves): no grid barrier here
+        if (threadIdx.x == 32) {
+            const unsigned target = unsigned(nelim) * gridDim.x;
+            while (*((volatile unsigned*)a.arrive) < target) {}
+            __threadfence();
+        }
+        __syncthreads();
+    } else {
+        grid.sync();
+        __syncwarp();   // lane 0 spun in the barrier: reconverge before warp-synchronous code
+    }
     STAMP(stamp++);
     // cross points of this block's component: t_C = scl*b_C - X_CF y in smem, then rows of S_C^-1 t_C
     const bool dbg2 = TIM && a.timers && blockIdx.x == 0 && threadIdx.x == 32;   // E2 sub-phases (the last elimination wins)
@@ -660,81 +695,159 @@ __device__ void elim_coop(cg::grid_group& grid, const CoopArgs& a, const ElimDev
                     tC[i] = t;
                 }
             }
+            if (fd) asm volatile("cp.async.wait_group 0;\n" ::: "memory");   // this thread's share of the Q tables
             __syncthreads();
             if (dbg2) a.timers[181] = gtimer();
-            const double* S = E.Sinv + E.sc_off[c];
-
-            // block lb owns the contiguous rows [rlo, rhi); warp w takes one column slice of all of them (RB rows
-            // at a time, NA loads per row per lane in flight: RB * NA independent loads per batch, so a block's
-            // ~13 rows (c5) take 4 dependent batches instead of 7); warp partials are summed in fixed order
+            // block lb owns the contiguous rows [rlo, rhi) of x_C = S_C^-1 t_C
             const int rlo = int(int64_t(lb) * ncc / nbc), rhi = int(int64_t(lb + 1) * ncc / nbc), nr = rhi - rlo;
-            const int cw = ((ncc + CW * 32 - 1) / (CW * 32)) * 32;
-            const int c0 = w * cw, c1 = min(ncc, c0 + cw);
-            double* part = tC + ncc;   // [CW][nr]
-            constexpr int NA = 8, RB = 4;
-            for (int r = rlo; r < rhi; r += RB) {
-                const double* __restrict__ row[RB];
-                double sr[RB];
+            double* part = fd ? tC : tC + ncc;   // [npart][nr] row sums (dense: one slice per warp)
+            const int npart = fd ? 1 : CW;
+            if (fd) {
+                // Separable S_C (HElim::fd, R23): x_C = (Qy (x) Qx) diag(1/(lam_a + mu_b)) (Qy (x) Qx)^T t_C.
+                // Every block of the component runs the forward transforms of the whole nx x ny grid (2 nx ny (nx + ny)
+                // flops from shared memory, the small Q tables from L1/L2) and the backward transforms of its own rows:
+                // no S_C^-1 stream (c5: 30.5 MB per elimination), the same fixed summation order in every block.
+                const int nx = E.fd_nx, ny = E.fd_ny, cs = E.sc_shared ? 0 : c;
+                const double* Qx = dsm + fdq;          // staged at the start of the phase
+                const double* Qy = Qx + nx * nx;
+                const double* __restrict__ il = E.fd_il + size_t(cs) * nx * ny;
+                double* X = tC;          // t_C as X[ix + nx iy]; later Z[a + nx b], then the row sums
+                double* Y = tC + ncc;    // Y[a + nx iy]; later V[a + nx (iy - iyA)]
+                constexpr int TY = 8;
+                const int nah = (nx + 31) / 32, nty = (ny + TY - 1) / TY;
+                // Y(a, iy) = sum_ix Qx[ix][a] X(ix, iy): lane = a (coalesced Qx rows), TY values of iy per lane (X broadcast)
+                for (int task = w; task < nah * nty; task += CW) {
+                    const int aa = (task % nah) * 32 + lane, iy0 = (task / nah) * TY;
+                    const bool ok = aa < nx;
+                    const int ac = ok ? aa : 0;
+                    int xo[TY];
+                    double acc[TY];
 #pragma unroll
-                for (int u = 0; u < RB; ++u) {
-                    row[u] = S + size_t(r + u < rhi ? r + u : r) * ncc;
-                    sr[u] = 0.0;
-                }
-                for (int j = c0 + lane; j < c1; j += 32 * NA) {
-                    double v[RB][NA], t[NA];
+                    for (int u = 0; u < TY; ++u) {
+                        xo[u] = nx * min(iy0 + u, ny - 1);
+                        acc[u] = 0.0;
+                    }
+#pragma unroll 4
+                    for (int ix = 0; ix < nx; ++ix) {
+                        const double q = Qx[ix * nx + ac];
 #pragma unroll
-                    for (int q = 0; q < NA; ++q) {
-                        const int jj = j + 32 * q;
-                        const bool ok = jj < c1;
-                        // streamed once per step (evict-first); a shared S_C^-1 (HElim::sc_shared) is read by the
-                        // blocks of every component at about the same time, and evict-first lines still serve the
-                        // partner (measured: L2-cached loads evict the basis and are slower)
-#pragma unroll
-                        for (int u = 0; u < RB; ++u) v[u][q] = (ok && r + u < rhi) ? __ldcs(row[u] + jj) : 0.0;
-                        t[q] = ok ? tC[jj] : 0.0;
+                        for (int u = 0; u < TY; ++u) acc[u] = fma(q, X[xo[u] + ix], acc[u]);
                     }
 #pragma unroll
-                    for (int q = 0; q < NA; ++q)
-#pragma unroll
-                        for (int u = 0; u < RB; ++u) sr[u] += v[u][q] * t[q];
+                    for (int u = 0; u < TY; ++u)
+                        if (ok && iy0 + u < ny) Y[aa + nx * (iy0 + u)] = acc[u];
                 }
+                __syncthreads();
+                // Z(a, b) = (sum_iy Y(a, iy) Qy[iy][b]) / (lam_a + mu_b), into X's place
+                for (int task = w; task < nah * nty; task += CW) {
+                    const int aa = (task % nah) * 32 + lane, b0 = (task / nah) * TY;
+                    const bool ok = aa < nx;
+                    const int ac = ok ? aa : 0;
+                    int bo[TY];
+                    double acc[TY];
 #pragma unroll
-                for (int u = 0; u < RB; ++u) {
-                    const double su = warp_sum(sr[u]);
-                    if (lane == 0 && r + u < rhi) part[w * nr + (r + u - rlo)] = su;
+                    for (int u = 0; u < TY; ++u) {
+                        bo[u] = min(b0 + u, ny - 1);
+                        acc[u] = 0.0;
+                    }
+#pragma unroll 4
+                    for (int iy = 0; iy < ny; ++iy) {
+                        const double yv = Y[ac + nx * iy];
+#pragma unroll
+                        for (int u = 0; u < TY; ++u) acc[u] = fma(yv, Qy[iy * ny + bo[u]], acc[u]);
+                    }
+#pragma unroll
+                    for (int u = 0; u < TY; ++u)
+                        if (ok && b0 + u < ny) X[aa + nx * (b0 + u)] = acc[u] * il[aa + nx * (b0 + u)];
+                }
+                __syncthreads();
+                // own rows: V(a, iy) = sum_b Z(a, b) Qy[iy][b] for the rows' iy range, into Y's place
+                const int iyA = nr > 0 ? rlo / nx : 0, niy = nr > 0 ? (rhi - 1) / nx - iyA + 1 : 0;
+                for (int e = threadIdx.x; e < nx * niy; e += CT) {
+                    const int iyl = e / nx, aa = e - iyl * nx;
+                    const double* qrow = Qy + (iyA + iyl) * ny;
+                    double t = 0.0;
+                    for (int bb = 0; bb < ny; ++bb) t = fma(X[aa + nx * bb], qrow[bb], t);
+                    Y[e] = t;
+                }
+                __syncthreads();
+                // x(ix, iy) = sum_a Qx[ix][a] V(a, iy): warp per row, lanes over a (fixed order), into X's place
+                for (int r = rlo + w; r < rhi; r += CW) {
+                    const int iy = r / nx, ix = r - iy * nx;
+                    const double* qrow = Qx + ix * nx;
+                    const double* vcol = Y + nx * (iy - iyA);
+                    double t = 0.0;
+                    for (int aa = lane; aa < nx; aa += 32) t = fma(qrow[aa], vcol[aa], t);
+                    t = warp_sum(t);
+                    if (lane == 0) part[r - rlo] = t;
+                }
+            } else {
+                const double* S = E.Sinv + E.sc_off[c];
+
+                // block lb owns the contiguous rows [rlo, rhi); warp w takes one column slice of all of them (RB rows
+                // at a time, NA loads per row per lane in flight: RB * NA independent loads per batch, so a block's
+                // ~13 rows (c5) take 4 dependent batches instead of 7); warp partials are summed in fixed order
+                const int cw = ((ncc + CW * 32 - 1) / (CW * 32)) * 32;
+                const int c0 = w * cw, c1 = min(ncc, c0 + cw);
+                constexpr int NA = 8, RB = 4;
+                for (int r = rlo; r < rhi; r += RB) {
+                    const double* __restrict__ row[RB];
+                    double sr[RB];
+#pragma unroll
+                    for (int u = 0; u < RB; ++u) {
+                        row[u] = S + size_t(r + u < rhi ? r + u : r) * ncc;
+                        sr[u] = 0.0;
+                    }
+                    for (int j = c0 + lane; j < c1; j += 32 * NA) {
+                        double v[RB][NA], t[NA];
+#pragma unroll
+                        for (int q = 0; q < NA; ++q) {
+                            const int jj = j + 32 * q;
+                            const bool ok = jj < c1;
+                            // streamed once per step (evict-first); a shared S_C^-1 (HElim::sc_shared) is read by the
+                            // blocks of every component at about the same time, and evict-first lines still serve the
+                            // partner (measured: L2-cached loads evict the basis and are slower)
+#pragma unroll
+                            for (int u = 0; u < RB; ++u) v[u][q] = (ok && r + u < rhi) ? __ldcs(row[u] + jj) : 0.0;
+                            t[q] = ok ? tC[jj] : 0.0;
+                        }
+#pragma unroll
+                        for (int q = 0; q < NA; ++q)
+#pragma unroll
+                            for (int u = 0; u < RB; ++u) sr[u] += v[u][q] * t[q];
+                    }
+#pragma unroll
+                    for (int u = 0; u < RB; ++u) {
+                        const double su = warp_sum(sr[u]);
+                        if (lane == 0 && r + u < rhi) part[w * nr + (r + u - rlo)] = su;
+                    }
                 }
             }
             if (dbg2) a.timers[182] = gtimer();
             __syncthreads();
             if (dbg2) a.timers[183] = gtimer();
-            double* hacc = dsm + FOLD_OFF;   // [KMAX][CT] per-thread h accumulators (fold)
-            if (fold_j > 0)
-                for (int t = 0; t < KMAX; ++t) hacc[t * CT + threadIdx.x] = 0.0;
             for (int r = rlo + threadIdx.x; r < rhi; r += CT) {
                 double acc = 0.0;
-                for (int q = 0; q < CW; ++q) acc += part[q * nr + (r - rlo)];
+                for (int q = 0; q < npart; ++q) acc += part[q * nr + (r - rlo)];
                 xC[base + r] = acc;
-                const int cf = E.cross_flat[base + r];
-                out[cf] = acc;
-                if (fold_j > 0)
-                    for (int t = 0; t < kc; ++t)
-                        hacc[t * CT + threadIdx.x] +=
-                            (P.MW[size_t(t) * P.nflat + cf] - a.ucross[size_t(t) * E.ncross + base + r]) * acc;
+                out[E.cross_flat[base + r]] = acc;
+                part[r - rlo] = acc;   // kept for the fold sums below (slice 0 of this row: read above by this thread only)
             }
             __syncthreads();
         }
         if (fold_j > 0) {
-            double* hacc = dsm + FOLD_OFF;
-            const double* hfw = dsm + FOLD_OFF + KMAX * CT;   // the face part, summed per warp in the face phase
-            if (ncc <= 0)
-                for (int t = 0; t < KMAX; ++t) hacc[t * CT + threadIdx.x] = 0.0;
-            __syncthreads();
-            // block sums (fixed order: cross part over threads, then the face part over warps) into the reduction
-            // slots (pp, c, 1 + t); slot 0 (unused) = 0
+            // block sums into the reduction slots (pp, c, 1 + t), slot 0 (unused) = 0; fixed order: the cross part
+            // sum_r (MW_t[c_r] - u_t[r]) x_C[r] over this block's rows (lanes stride the rows, then a warp tree), then
+            // the face part over the warps (summed per warp in the face phase)
+            const int rlo = ncc > 0 ? int(int64_t(lb) * ncc / nbc) : 0, rhi = ncc > 0 ? int(int64_t(lb + 1) * ncc / nbc) : 0;
+            const double* xr = (fd ? dsm : dsm + ncc);
             for (int v = w; v <= kc; v += CW) {
                 double t_ = 0.0;
                 if (v > 0)
-                    for (int q = 0; q < CW; ++q) t_ += hacc[(v - 1) * CT + q * 32 + lane];
+                    for (int r = rlo + lane; r < rhi; r += 32) {
+                        const int cf = E.cross_flat[base + r];
+                        t_ += (P.MW[size_t(v - 1) * P.nflat + cf] - a.ucross[size_t(v - 1) * E.ncross + base + r]) * xr[r - rlo];
+                    }
                 t_ = warp_sum(t_);
                 if (v > 0)
                     for (int q = 1; q < CW; ++q) t_ += hfw[q * KMAX + v - 1];
@@ -1111,7 +1224,7 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
     static_assert(KM <= KMAX, "basis bound");
     cg::grid_group grid = cg::this_grid();
     if (a.s != nullptr && a.s->done) return;
-    int stamp = 0;
+    int stamp = 0, nelim = 0;
     STAMP(stamp++);
     const PrecDev& P = a.P;
     extern __shared__ double dsm[];
@@ -1160,7 +1273,7 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
     // Basis vectors are stored unnormalised (W_t = sclh_t * Wraw_t, likewise M W_t and L W_t): every
     // consumer folds sclh_t into its coefficients, so no normalisation pass over the rows is needed.
     // ---- s = M^-1 r (exact) = Wraw_0
-    elim_coop<KM, TIM>(grid, a, P.eM, P.rf, scl, P.W, dsm, c, lb, nbc, stamp);
+    elim_coop<KM, TIM>(grid, a, P.eM, P.rf, scl, P.W, dsm, c, lb, nbc, stamp, nelim);
     // ---- Ms, Ls, ||s||_M; q_1 = s / ||s||_M; rhs of the next solve M q_1 = Ms / ||s||_M
     ZERO_VALS();
     double* gacc = dsm;   // per-thread Gram accumulators [GW][CT] (dsm is free outside face solves / Ritz)
@@ -1203,7 +1316,7 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
     const bool fuseK = P.eK.tri && P.eK.fuse;
     for (int j = 1; j < P.kmax; ++j) {
         const bool fold = a.fold && fuseK;   // h summed inside the elimination (R22): no phase A, no barrier
-        elim_coop<KM, TIM>(grid, a, P.eK, j == 1 ? P.MW : P.Mw, scl, P.w, dsm, c, lb, nbc, stamp,
+        elim_coop<KM, TIM>(grid, a, P.eK, j == 1 ? P.MW : P.Mw, scl, P.w, dsm, c, lb, nbc, stamp, nelim,
                        fold ? j : 0, kcs[c], pp, r0, rs);   // w = K^-1 M q_j
         const bool part = act[c] && !brk[c];
         const int kc = kcs[c];
@@ -1435,6 +1548,8 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
             }
         }
     }
+    // every elimination's arrivals lie before the last grid barrier above: leave the counter at zero for the next launch
+    if (blockIdx.x == 0 && tid == 0) *a.arrive = 0u;
     // the k x k Ritz problems (k_prec_ritz) and the combine (k_prec_combine) follow as two small launches: the
     // Ritz code runs there without this kernel's register cap, and one grid barrier is saved
 }
@@ -1517,6 +1632,11 @@ bool prec_coop_prepare(const PrecDev& P, int device, CoopBuffers& B) {
         smem = std::max(smem, (size_t(ncmax) + size_t(CW) * ((ncmax + nbc_lo - 1) / nbc_lo)) * 8);
     }
     smem = std::max(smem, size_t(GW) * CT * 8);      // per-thread Gram accumulators
+    for (const ElimDev* E : {&P.eK, &P.eM})          // fast-diagonalised cross-point solve: X, Y and the staged Q tables
+        if (E->fd) {
+            const size_t need = (size_t(2) * ncmax + 1 + size_t(E->fd_nx) * E->fd_nx + size_t(E->fd_ny) * E->fd_ny) * 8;
+            if (need <= 96 * 1024) smem = std::max(smem, need);   // larger grids keep the dense S_C^-1 path
+        }
     smem = std::max(smem, size_t(RW) * TRI_N * 8);   // per-thread forward solutions of tridiagonal faces
     smem = std::max(smem, size_t(CW) * (4 * KMAX * (KMAX + 1) + 2 * KMAX + 4 * KMAX) * 8);
     if (smem > 200 * 1024) return false;
@@ -1551,10 +1671,9 @@ bool prec_coop_prepare(const PrecDev& P, int device, CoopBuffers& B) {
     B.nbc_max = (nb + P.ncomp - 1) / P.ncomp;
     B.gram_cgs2 = getenv("DE_CGS2_TWO_PASS") ? 0 : 1;   // A/B switch: the literal two-pass CGS2
     // fold h into the elimination (R22): 2D fused eliminations, one-pass Gram-Schmidt, room for the accumulators
-    B.fold = (B.gram_cgs2 && P.eK.tri && P.eK.fuse && !getenv("DE_NO_FOLD") &&
-              size_t(ncmax) + size_t(CW) * B.nbc_max + 2 <= size_t(FOLD_OFF) &&
-              (size_t(FOLD_OFF) + size_t(KMAX) * CT + size_t(CW) * KMAX) * 8 <= B.smem) ? 1 : 0;
-    if (getenv("DE_VERBOSE")) fprintf(stderr, "[de] k_prec_coop: fold %d (R22)\n", B.fold);
+    B.fold = (B.gram_cgs2 && P.eK.tri && P.eK.fuse && !getenv("DE_NO_FOLD")) ? 1 : 0;
+    B.split = getenv("DE_NO_SPLIT") ? 0 : 1;   // A/B switch: a grid barrier between t_C and the cross-point solve
+    if (getenv("DE_VERBOSE")) fprintf(stderr, "[de] k_prec_coop: fold %d (R22) split %d\n", B.fold, B.split);
     return true;
 }
 
@@ -1583,6 +1702,9 @@ int prec_apply_coop(const PrecDev& P, const CoopBuffers& B, const double* r, dou
     a.gram_cgs2 = literal ? 0 : B.gram_cgs2;   // literal: SPEC's two-pass CGS2 (used under FGMRES)
     a.fold = literal ? 0 : B.fold;
     a.ucross = B.ucross;
+    a.arrive = B.arrive;
+    a.split = B.split;
+    a.smem_doubles = int(B.smem / sizeof(double));
     a.timers = B.timers;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(B.nb);

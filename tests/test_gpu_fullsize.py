@@ -3,14 +3,23 @@
 Reference answers come from the oracle only:
   * u_ref: the plain definition u = K_ff^-1 f (Eq. (4)) by oracle.direct (nested-dissection
     Cholesky; SuperLU cannot factor c4/c5) with extended-precision refinement; fl(u_ref) is the FP64 rounding
-    of the exact solution and its residual is the measured FP64 floor of the problem (DESIGN.md R17);
+    of the exact solution and its residual is the measured FP64 floor of the problem (R17). The direct
+    solves of c3, c4 and c5 (three density states) take minutes each on a host, so they are computed once by the
+    committed script tools/make_fullsize_goldens.py (which calls only oracle/ and synthetic/) and stored, sampled at
+    16,384 seeded free dofs, under tests/golden/fullsize_*.npz together with ||u_ref||, the floor and a hash of the
+    inputs; c2 is also solved live and compared on the whole vector;
+  * the residual of the GPU's u is recomputed here by the oracle in extended precision (oracle.direct.relres_ext);
   * the Schur apply and the preconditioner: oracle.dd.schur_apply / oracle.precond.apply_precond on the full
     c5 geometry, compared element by element.
-Gates (BASELINE.json north_star): ||u - u_ref|| <= 1e-8 ||u_ref||; de_solve returns DE_OK (the refined
-double-double iterate meets rtol 1e-10); the returned FP64 u has relres <= max(1e-10, 1.25 x the measured
-floor of fl(u_ref)) -- no FP64 vector can do materially better than fl(u_ref).
-Config 3 (FP64-ill-posed, R15/SURVEY Q15): normwise backward error <= 1e-12 for both solvers.
+Gates (BASELINE.json north_star): ||u - u_ref|| <= 1e-8 ||u_ref|| (on the samples, and | ||u|| - ||u_ref|| | on the
+whole vector); de_solve returns DE_OK (the refined double-double iterate meets rtol 1e-10); the returned FP64 u has
+relres <= max(1e-10, 1.25 x the measured floor of fl(u_ref)) -- no FP64 vector can do materially better than fl(u_ref).
+Config 3 (FP64-ill-posed, R15/SURVEY Q15): normwise backward error <= 1e-12 for the direct solve, the budgeted value
+for the interface PCG.
 """
+import hashlib
+import os
+
 import numpy as np
 import pytest
 
@@ -21,7 +30,7 @@ from synthetic import make_config, density_sequence_step  # noqa: E402
 from oracle.topology import build_topology  # noqa: E402
 from oracle.dd import subdomain_blocks, factor_subdomains, schur_apply  # noqa: E402
 from oracle.precond import build_components, apply_precond  # noqa: E402
-from oracle.direct import refine_dd, relres_ext, direct_solve  # noqa: E402
+from oracle.direct import refine_dd, relres_ext  # noqa: E402
 from oracle.fem import free_system  # noqa: E402
 
 FLOOR_FACTOR = 1.25
@@ -41,17 +50,41 @@ def _solver(p, **kw):
     return B.Solver.from_problem(p, device=0, **kw)
 
 
-def _check_against_direct(p, u, relres, st):
-    hi, lo, hist = refine_dd(p, rounds=2)
-    floor = hist[-1]                                   # relres of fl(u_ref), the FP64 floor
-    err = np.linalg.norm(u - hi) / np.linalg.norm(hi)
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def _input_sha(p):
+    h = hashlib.sha256()
+    h.update(np.ascontiguousarray(p.density, dtype=np.float64).tobytes())
+    h.update(np.ascontiguousarray(p.rhs, dtype=np.float64).tobytes())
+    return h.hexdigest()
+
+
+def _golden(case, p):
+    g = np.load(os.path.join(GOLD, f"fullsize_{case}.npz"))
+    assert str(g["sha"]) == _input_sha(p), "golden was generated from other inputs: rerun tools/make_fullsize_goldens.py"
+    return g
+
+
+def _check_against_direct(case, p, u, relres, st, live=False):
+    g = _golden(case, p)
+    idx, ref, floor = g["idx"], g["u_hi"], float(g["floor"])      # fl(u_ref) samples; relres of fl(u_ref)
+    err = np.linalg.norm(u[idx] - ref) / np.linalg.norm(ref)
+    errmax = np.abs(u[idx] - ref).max() / np.abs(ref).max()
+    nrm = abs(np.linalg.norm(u) - float(g["norm_u"])) / float(g["norm_u"])
     gate = max(1e-10, FLOOR_FACTOR * floor)
-    print(f"{p.name}: ||u-u_ref||/||u_ref|| = {err:.3e}, relres(u) = {relres:.4e} (oracle {relres_ext(p, u):.4e}), "
-          f"relres_dd = {st.relres_dd:.3e}, floor fl(u_ref) = {floor:.4e}")
-    assert err <= 1e-8
+    rel_o = relres_ext(p, u)                                       # the oracle's own residual of the GPU u
+    print(f"{case}: ||u-u_ref||/||u_ref|| = {err:.3e} (max-norm {errmax:.3e}, | ||u|| - ||u_ref|| | {nrm:.3e}) on "
+          f"{len(idx)} samples, relres(u) = {relres:.4e} (oracle {rel_o:.4e}), relres_dd = {st.relres_dd:.3e}, "
+          f"floor fl(u_ref) = {floor:.4e}")
+    assert err <= 1e-8 and errmax <= 1e-8 and nrm <= 1e-8
     assert st.relres_dd <= 1e-10
     assert relres <= gate
-    assert relres_ext(p, u) <= gate                     # the oracle's own residual of the GPU u
+    assert rel_o <= gate
+    if live:   # small enough to solve here: the whole vector, and the stored samples against the live solve
+        hi, lo, hist = refine_dd(p, rounds=2)
+        assert np.linalg.norm(u - hi) <= 1e-8 * np.linalg.norm(hi)
+        assert np.array_equal(hi[idx], ref) or np.linalg.norm(hi[idx] - ref) <= 1e-13 * np.linalg.norm(ref)
     return floor
 
 
@@ -81,7 +114,7 @@ def test_full_size_solution_matches_direct_oracle(name):
     try:
         _sampled_blocks(p, T, S)
         u, its, relres, _ = S.solve(p.rhs, p.rtol)        # raises DEError unless DE_OK
-        _check_against_direct(p, u, relres, S.stats())
+        _check_against_direct(name, p, u, relres, S.stats(), live=(name == "c2"))
     finally:
         S.close()
 
@@ -104,7 +137,7 @@ def test_c5_sequence_full_size_solves_1_25_50():
             u, its, relres, _ = S.solve(p.rhs, p.rtol)    # DE_OK required at every step
             its_all.append(its)
             if t in (0, 24, 49):
-                _check_against_direct(p.with_density(rho), u, relres, S.stats())
+                _check_against_direct(f"c5_t{t}", p.with_density(rho), u, relres, S.stats())
         print("iterations per solve:", its_all)
         assert np.mean(its_all[1:]) < its_all[0]          # warm starts pay
     finally:
@@ -168,7 +201,8 @@ def test_c3_full_size_backward_error():
     p = make_config("c3")
     K, f, free = free_system(p)
     normK1 = abs(K).sum(axis=0).max()
-    u_ref = direct_solve(p)
+    g = _golden("c3", p)
+    idx, u_ref_s, be_ref = g["idx"], g["u_hi"], float(g["backward"])
 
     def bwd(u):
         r = f - K @ u[free]
@@ -180,8 +214,8 @@ def test_c3_full_size_backward_error():
         # the budget ends the solve (DE_ENOCONV is the expected status on this instance, R15)
         u, its, relres, status = S.solve(p.rhs, p.rtol, allow_noconv=True)
         assert status in (B.DE_OK, B.DE_ENOCONV)
-        be_gpu, be_ref = bwd(u), bwd(u_ref)
-        fwd = np.linalg.norm(u - u_ref) / np.linalg.norm(u_ref)
+        be_gpu = bwd(u)
+        fwd = np.linalg.norm(u[idx] - u_ref_s) / np.linalg.norm(u_ref_s)
         print(f"c3: its {its}, relres {relres:.3e}, backward error GPU {be_gpu:.3e} oracle {be_ref:.3e}, "
               f"forward difference {fwd:.3e}")
         assert be_ref <= 1e-12 and be_gpu <= 2e-9
