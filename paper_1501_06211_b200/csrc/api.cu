@@ -542,6 +542,7 @@ de_status_t upload_prec_impl(de_ctx* c) {
             }
         }
         // face-interleaved tridiagonal copy (2D faces are paths): coalesced thread-per-face solves
+        D.pat_id = nullptr;
         D.tri = 1;
         for (int F = 0; F < E.nfaces && D.tri; ++F) {
             const int o = E.face_off[F], n = E.face_off[F + 1] - o;
@@ -623,6 +624,77 @@ de_status_t upload_prec_impl(de_ctx* c) {
             TRY(dupload(c, &D.g_c1, gc1));
             TRY(dupload(c, &D.g_v0, gv0));
             TRY(dupload(c, &D.g_v1, gv1));
+            // Row patterns of the fused consumer (x = y - G x_C of a row's neighbours, then (M x)_i, (L x)_i): a face
+            // node's neighbours are its flat neighbours i-1, i+1 in the same face and the face's own end cross points, so
+            // its x values need only row i's couplings; the (source codes, M values, L values) triples of a uniform
+            // skeleton take a handful of distinct values, kept in a small table that stays in L1. pat_id[i] = -1
+            // (cross points, irregular rows) -> the general path. Source codes: 0 / 1 / 2 = flat i-1 / i / i+1,
+            // 3 / 4 = x_C of the face's first / second coupling, 7 = unused entry; 3 bits per entry.
+            D.pat_id = nullptr;
+            D.pat_code = nullptr;
+            D.pat_m = D.pat_l = nullptr;
+            if (!getenv("DE_NO_PAT")) {
+                const HCsr& Mh = hs.M;
+                const HCsr& Lh = hs.L;
+                std::vector<int32_t> faceid(nfl, -1), pid(nfl, -1), codes;
+                std::vector<double> pm, pl;
+                for (int F = 0; F < E.nfaces; ++F)
+                    for (int sl = E.face_off[F]; sl < E.face_off[F + 1]; ++sl) faceid[E.face_nodes[sl]] = F;
+                std::vector<int32_t> cross_of(nfl, -1);
+                for (int ci = 0; ci < E.ncross; ++ci) cross_of[E.cross_flat[ci]] = ci;
+                std::map<std::vector<double>, int32_t> pats;
+                bool ok = true;
+                for (size_t i = 0; i < nfl && ok; ++i) {
+                    const int F = faceid[i];
+                    if (F < 0) continue;
+                    const int e0 = Mh.ptr[i], e1 = Mh.ptr[i + 1];
+                    if (e1 - e0 > 3) continue;
+                    int code = 0;
+                    std::vector<double> key;
+                    bool fast = true;
+                    for (int k = 0; k < 3 && fast; ++k) {
+                        const int e = e0 + k;
+                        int src = 7;
+                        double mv = 0.0, lv = 0.0;
+                        if (e < e1) {
+                            const int col = Mh.col[e];
+                            if (Lh.col[e] != col) fast = false;
+                            mv = Mh.val[e];
+                            lv = Lh.val[e];
+                            if (faceid[col] == F && std::abs(col - int(i)) <= 1) src = col - int(i) + 1;
+                            else if (cross_of[col] >= 0 && txj[2 * F] >= 0 && txc[2 * F] == cross_of[col]) src = 3;
+                            else if (cross_of[col] >= 0 && txj[2 * F + 1] >= 0 && txc[2 * F + 1] == cross_of[col]) src = 4;
+                            else fast = false;
+                        }
+                        code |= src << (3 * k);
+                        key.push_back(double(src));
+                        key.push_back(mv);
+                        key.push_back(lv);
+                    }
+                    if (!fast) continue;
+                    auto it = pats.find(key);
+                    if (it == pats.end()) {
+                        if (pats.size() >= 4096) {   // no small table (e.g. the weighted trace norm): general path
+                            ok = false;
+                            break;
+                        }
+                        it = pats.emplace(key, int32_t(pats.size())).first;
+                        codes.push_back(code);
+                        for (int k = 0; k < 3; ++k) {
+                            pm.push_back(key[3 * k + 1]);
+                            pl.push_back(key[3 * k + 2]);
+                        }
+                    }
+                    pid[i] = it->second;
+                }
+                if (ok && !pats.empty()) {
+                    TRY(dupload(c, &D.pat_id, pid));
+                    TRY(dupload(c, &D.pat_code, codes));
+                    TRY(dupload(c, &D.pat_m, pm));
+                    TRY(dupload(c, &D.pat_l, pl));
+                    if (getenv("DE_VERBOSE")) fprintf(stderr, "[de] consumer row patterns: %zu\n", pats.size());
+                }
+            }
             D.fell_col = nullptr;
             if (&D == &P.eK && !getenv("DE_NO_FELL")) {   // fold ELL of the M/L rows with eK's couplings
                 const HCsr& Mh = hs.M;

@@ -222,6 +222,10 @@ struct ElimDev {
     // elimination couplings, so the consumer's x = y - G x_C of each neighbour is two dependent load levels
     // instead of four (CSR ptr -> col -> g[col] -> xC[g]); [FELL_W][nflat] each; fell_col[0][i] = -1: CSR row
     int32_t* fell_col;
+    // consumer row patterns (fuse only; api.cu up_elim): pat_id[i] >= 0 indexes (pat_code, pat_m[3], pat_l[3]); the
+    // row's neighbour values come from flat i-1, i, i+1 and the face's two x_C with row i's own couplings
+    int32_t *pat_id, *pat_code;
+    double *pat_m, *pat_l;
     int32_t *fell_c0, *fell_c1;
     double *fell_v0, *fell_v1, *fell_m, *fell_l;
 };

@@ -277,6 +277,43 @@ __device__ __forceinline__ double spmv_elim_fell(const CsrDev& M, const CsrDev& 
     return xi;
 }
 
+// spmv_elim through the row patterns (ElimDev::pat_*): every address of the first load level follows from i alone
+// (the row's couplings, y and the couplings of its flat neighbours), the second level is the face's two x_C values
+// and the pattern table (L1); rows without a pattern (cross points) take the general path. 36 distinct bytes per row
+// instead of the fold ELL's 132 + nine gathers.
+__device__ __forceinline__ double spmv_elim_pat(const CsrDev& M, const CsrDev& L, int64_t i, const ElimDev& E,
+                                                const double* __restrict__ y, const double* __restrict__ xC,
+                                                int64_t nfl, double& yM, double& yL) {
+    const int pid = E.pat_id[i];
+    const int64_t im = i > 0 ? i - 1 : i, ip = i + 1 < nfl ? i + 1 : i;
+    const int c0 = E.g_c0[i], c1 = E.g_c1[i];
+    const double ym = y[im], y0 = y[i], yp = y[ip];
+    const double am0 = E.g_v0[im], a00 = E.g_v0[i], ap0 = E.g_v0[ip];
+    const double am1 = E.g_v1[im], a01 = E.g_v1[i], ap1 = E.g_v1[ip];
+    if (pid < 0)
+        return E.fell_col ? spmv_elim_fell(M, L, i, E, y, xC, nfl, yM, yL) : spmv_elim(M, L, i, E, y, xC, yM, yL);
+    const double xa = xC[c0], xb = xC[c1];
+    const int code = E.pat_code[pid];
+    double pm[3], pl[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        pm[k] = E.pat_m[3 * pid + k];
+        pl[k] = E.pat_l[3 * pid + k];
+    }
+    const double xm = ym - am0 * xa - am1 * xb, x0 = y0 - a00 * xa - a01 * xb, xp = yp - ap0 * xa - ap1 * xb;
+    double am = 0.0, al = 0.0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const int src = (code >> (3 * k)) & 7;
+        const double x = src == 0 ? xm : (src == 1 ? x0 : (src == 2 ? xp : (src == 3 ? xa : (src == 4 ? xb : 0.0))));
+        am = fma(pm[k], x, am);
+        al = fma(pl[k], x, al);
+    }
+    yM = am;
+    yL = al;
+    return x0;
+}
+
 // Warp solve of one face block (L then M = P L^T P forward sweeps, b <= 31, row window in registers).
 // rhs = scale * b_F (mode 0) or scale * b_F - X_FC xC (mode 1). The factor columns stream through a two-chunk
 // shared-memory ring (32 columns per chunk, cp.async issued one chunk ahead), so no load sits on the per-row
@@ -1282,7 +1319,8 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
     for (int64_t i = r0; i < hi; i += rs) {
         double m, l, sv;
         if (fuseM) {
-            sv = spmv_elim(P.M, P.L, i, P.eM, P.y, P.y + nf, m, l);
+            sv = P.eM.pat_id ? spmv_elim_pat(P.M, P.L, i, P.eM, P.y, P.y + nf, nf, m, l)
+                             : spmv_elim(P.M, P.L, i, P.eM, P.y, P.y + nf, m, l);
             P.W[i] = sv;
         } else {
             spmv_ml(P.M, P.L, i, P.W, m, l);
@@ -1452,8 +1490,9 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
                 }
                 double x, m, l;
                 if (fold) {   // the former phase A on the same row: w_i and (M w)_i, (L w)_i by the fused SpMV
-                    x = P.eK.fell_col ? spmv_elim_fell(P.M, P.L, i, P.eK, P.y, P.y + nf, nf, m, l)
-                                      : spmv_elim(P.M, P.L, i, P.eK, P.y, P.y + nf, m, l);
+                    x = P.eK.pat_id ? spmv_elim_pat(P.M, P.L, i, P.eK, P.y, P.y + nf, nf, m, l)
+                        : (P.eK.fell_col ? spmv_elim_fell(P.M, P.L, i, P.eK, P.y, P.y + nf, nf, m, l)
+                                         : spmv_elim(P.M, P.L, i, P.eK, P.y, P.y + nf, m, l));
                     vals[1] += x * m;   // ||w||_M^2 before the orthogonalisation (breakdown test)
                 } else {
                     x = a.gram_cgs2 ? P.w[i] : a.w1[i];
