@@ -438,7 +438,7 @@ de_status_t upload_prec_impl(de_ctx* c) {
     P.ncomp = hs.ncomp;
     P.nflat = int32_t(hs.comp_off[hs.ncomp]);
     P.kmax = std::min(std::max(1, c->opt.lanczos_k), KMAX);
-    P.jacobi_reg = getenv("DE_JACOBI_REG") ? 1 : 0;
+    P.jacobi_reg = getenv("DE_JACOBI_REG") ? 1 : (getenv("DE_JACOBI_WARP") ? 2 : 0);   // A/B: one-warp Jacobi variants
     for (int i = 0; i <= MAXC; ++i) P.comp_off[i] = hs.comp_off[std::min(i, hs.ncomp)];
     for (int i = 0; i < MAXC; ++i) P.singular[i] = (hs.singular_mask >> i) & 1;
     P.theta = c->opt.theta;

@@ -361,7 +361,7 @@ void launch_zero_dirichlet(const int8_t* cls, double* u, int64_t ndof, cudaStrea
 // preconditioner
 struct PrecDev {
     int32_t ncomp, nflat, kmax;
-    int32_t jacobi_reg;         // 1: the register Jacobi of the Ritz step (A/B switch DE_JACOBI_REG), else shared-memory
+    int32_t jacobi_reg;         // Ritz-step Jacobi: 0 = whole CTA (default), 1 = one warp in registers (DE_JACOBI_REG), 2 = one warp from shared memory (DE_JACOBI_WARP)
     int32_t max_face_band;      // max half bandwidth over all face blocks (1: tridiagonal, 2D)
     int64_t comp_off[MAXC + 1];
     int32_t singular[MAXC];

@@ -469,7 +469,8 @@ __device__ void face_thread_tridiag(const CoopArgs& a, const ElimDev& E, int F, 
 template <int NF, int KH>
 __device__ __forceinline__ void face_warp_pcr(const PrecDev& P, const ElimDev& E, int F0, int stride, int fend,
                                               const double* __restrict__ b, const double* scl,
-                                              double* __restrict__ y, int lane, double* hl = nullptr, int kc = 0) {
+                                              double* __restrict__ y, int lane, double* hl = nullptr, int kc = 0,
+                                              const int32_t* __restrict__ bmap = nullptr) {
     int n[NF], node[NF];
     double co[NF][PCR_Q], x[NF];
 #pragma unroll
@@ -487,7 +488,7 @@ __device__ __forceinline__ void face_warp_pcr(const PrecDev& P, const ElimDev& E
 #pragma unroll
     for (int f = 0; f < NF; ++f) {
         const double sc = scl[ccomp(P.comp_off, P.ncomp, __shfl_sync(0xffffffffu, node[f], 0))];
-        x[f] = lane < n[f] ? sc * b[node[f]] : 0.0;
+        x[f] = lane < n[f] ? sc * b[bmap ? bmap[node[f]] : node[f]] : 0.0;
     }
     if (KH > 0)   // the fold's M W_t rows of these nodes into L1 now, so their loads after the reduction hit
 #pragma unroll
@@ -526,7 +527,10 @@ __device__ __forceinline__ void face_warp_pcr(const PrecDev& P, const ElimDev& E
 template <int KM, bool TIM>
 __device__ void elim_coop(cg::grid_group& grid, const CoopArgs& a, const ElimDev& E, const double* b,
                           const double* scl, double* out, double* dsm, int c, int lb, int nbc, int& stamp, int& nelim,
-                          int fold_j = 0, int kc = 0, int pp = 0, int64_t r0 = 0, int64_t rs = 1) {
+                          int fold_j = 0, int kc = 0, int pp = 0, int64_t r0 = 0, int64_t rs = 1,
+                          const int32_t* __restrict__ bmap = nullptr) {
+    // bmap (fused path only): the right-hand side is b[bmap[i]] -- the seed solve reads r through the skeleton map,
+    // so no gather phase (and barrier) precedes it
     const PrecDev& P = a.P;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     // warp 0 hosts the grid-barrier thread; it comes out of every barrier late, so face solves run
@@ -582,7 +586,7 @@ __device__ void elim_coop(cg::grid_group& grid, const CoopArgs& a, const ElimDev
                             const int e = e0[u] + k + 32 * h;
                             const bool ok = e < e1[u];
                             v[u][h] = ok ? E.gt_val[e] : 0.0;
-                            x[u][h] = ok ? b[E.gt_col[e]] : 0.0;
+                            x[u][h] = ok ? b[bmap ? bmap[E.gt_col[e]] : E.gt_col[e]] : 0.0;
                         }
 #pragma unroll
                     for (int u = 0; u < 2; ++u) acc[u] += v[u][0] * x[u][0] + v[u][1] * x[u][1];
@@ -592,7 +596,7 @@ __device__ void elim_coop(cg::grid_group& grid, const CoopArgs& a, const ElimDev
                     const int ci = ci0 + u * nwarps;
                     const double sgt = warp_sum(acc[u]);
                     if (lane == 0 && ci < E.ncross) {
-                        tCg[ci] = scl[ccomp(P.comp_off, P.ncomp, cf[u])] * (b[cf[u]] - sgt);
+                        tCg[ci] = scl[ccomp(P.comp_off, P.ncomp, cf[u])] * (b[bmap ? bmap[cf[u]] : cf[u]] - sgt);
                         if (fold_j > 0) a.ucross[size_t(fold_j - 1) * E.ncross + ci] = sgt;
                     }
                 }
@@ -618,7 +622,7 @@ __device__ void elim_coop(cg::grid_group& grid, const CoopArgs& a, const ElimDev
                 if (lane == 0) hfw[w * KMAX + t] = v;
             }
         } else if (w > 0) {
-            for (int F = fb + lw; F < fe; F += 2 * nwc) face_warp_pcr<2, 0>(P, E, F, nwc, fe, b, scl, y, lane);
+            for (int F = fb + lw; F < fe; F += 2 * nwc) face_warp_pcr<2, 0>(P, E, F, nwc, fe, b, scl, y, lane, nullptr, 0, bmap);
         }
     } else if (E.tri) {
         if (w > 0)
@@ -843,7 +847,7 @@ __device__ void elim_coop(cg::grid_group& grid, const CoopArgs& a, const ElimDev
                             const bool ok = jj < c1;
                             // streamed once per step (evict-first); a shared S_C^-1 (HElim::sc_shared) is read by the
                             // blocks of every component at about the same time, and evict-first lines still serve the
-                            // partner (measured: L2-cached loads evict the basis and are slower)
+                            // partner (measured again in round 2 with the lighter consumer: cached loads 0.615 vs 0.578 ms)
 #pragma unroll
                             for (int u = 0; u < RB; ++u) v[u][q] = (ok && r + u < rhi) ? __ldcs(row[u] + jj) : 0.0;
                             t[q] = ok ? tC[jj] : 0.0;
@@ -1139,14 +1143,126 @@ __device__ int jacobi_smem(double* C, double* V, int n, double* rot) {
     return nsw;
 }
 
+// Cyclic parallel Jacobi of jacobi_smem (the same pairs, rotations and update formulas, entry by entry) run by the
+// whole CTA: one thread per entry of C and V, the circle-method schedule of all rounds tabulated once in shared
+// memory (the content of slot ring[k] after r rounds is ring[(k + r) mod (M-1)], slot 0 stays). A round is a
+// rotation phase (M/2 threads), the entry updates and the write-back: three CTA barriers instead of one warp
+// walking 4 entries per lane with register-array index maps (35 us -> measured in profiles/). Returns the sweeps.
+__device__ int jacobi_block(double* C, double* V, int n, int* sched, int* slot_of, double* csn, double* red, int* flag) {
+    constexpr int LDK = KMAX + 1;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int M = (n + 1) & ~1, H = M / 2;
+    double* cs = csn;
+    double* sn = csn + KMAX / 2;
+    if (n < M) {   // ghost slot of odd n: a decoupled zero row/column
+        for (int i = tid; i < M; i += CT) {
+            C[(M - 1) * LDK + i] = 0.0;
+            C[i * LDK + (M - 1)] = 0.0;
+            V[(M - 1) * LDK + i] = i == M - 1 ? 1.0 : 0.0;
+            V[i * LDK + (M - 1)] = i == M - 1 ? 1.0 : 0.0;
+        }
+    }
+    int* ring = slot_of;   // scratch until the first round
+    if (tid == 0) {
+        int p = 1;
+        for (int k = 0; k < M - 1; ++k) {
+            ring[k] = p;
+            p = circle_src(p, M);
+        }
+    }
+    __syncthreads();
+    for (int e = tid; e < (M - 1) * (M - 1); e += CT) {
+        const int rnd = e / (M - 1), k = e - rnd * (M - 1);
+        sched[rnd * KMAX + ring[k]] = ring[(k + rnd) % (M - 1)];
+    }
+    if (tid < M - 1) sched[tid * KMAX] = 0;
+    __syncthreads();
+    const int i = tid / M, j = tid - i * M;
+    const bool mine = tid < M * M;
+    int nsw = 0;
+    for (int sweep = 0; sweep < 30; ++sweep) {
+        double off = 0.0, dia = 0.0;
+        if (mine) {
+            const double x = C[i * LDK + j];
+            if (i == j) dia = x * x;
+            else off = x * x;
+        }
+        off = warp_sum(off);
+        dia = warp_sum(dia);
+        if (lane == 0) {
+            red[wid] = off;
+            red[CW + wid] = dia;
+        }
+        if (tid == 0) *flag = 0;
+        __syncthreads();
+        off = 0.0;
+        dia = 0.0;
+        for (int q = 0; q < CW; ++q) {
+            off += red[q];
+            dia += red[CW + q];
+        }
+        if (off <= 1e-24 * dia) break;   // ||offdiag||_F <= 1e-12 ||diag||_F (as jacobi_reg / jacobi_smem)
+        ++nsw;
+        const double thr = 1e-15 * sqrt(dia);
+        for (int rnd = 0; rnd < M - 1; ++rnd) {
+            if (tid < H) {
+                const int p_ = sched[rnd * KMAX + 2 * tid], q_ = sched[rnd * KMAX + 2 * tid + 1];
+                const double app = C[p_ * LDK + p_], aqq = C[q_ * LDK + q_], apq = C[p_ * LDK + q_];
+                double c_ = 1.0, s_ = 0.0;
+                if (fabs(apq) > thr && fabs(apq) > 1e-300) {
+                    const double d = aqq - app;
+                    const double ir = rsqrt(fma(d, d, 4.0 * apq * apq));
+                    const double h = 0.5 * fma(fabs(d), ir, 1.0);
+                    const double ih = rsqrt(h);
+                    c_ = h * ih;
+                    s_ = (d >= 0.0 ? apq : -apq) * ir * ih;
+                    *flag = 1;
+                }
+                cs[tid] = c_;
+                sn[tid] = s_;
+                slot_of[p_] = 2 * tid;
+                slot_of[q_] = 2 * tid + 1;
+            }
+            __syncthreads();
+            double ncv = 0.0, nvv = 0.0;
+            if (mine) {
+                const int si = slot_of[i], sj = slot_of[j];
+                const int ki = si >> 1, kj = sj >> 1;
+                const int pi = sched[rnd * KMAX + (si & ~1)], qi = sched[rnd * KMAX + (si | 1)];
+                const int pj = sched[rnd * KMAX + (sj & ~1)], qj = sched[rnd * KMAX + (sj | 1)];
+                const double ci_ = cs[ki], si_ = sn[ki], cj_ = cs[kj], sj_ = sn[kj];
+                const double ap = (si & 1) ? si_ : ci_, aq = (si & 1) ? ci_ : -si_;
+                const double bp = (sj & 1) ? sj_ : cj_, bq = (sj & 1) ? cj_ : -sj_;
+                const double cpp = C[pi * LDK + pj], cpq = C[pi * LDK + qj], cqp = C[qi * LDK + pj], cqq = C[qi * LDK + qj];
+                ncv = ap * (cpp * bp + cpq * bq) + aq * (cqp * bp + cqq * bq);
+                nvv = V[i * LDK + pj] * bp + V[i * LDK + qj] * bq;
+            }
+            __syncthreads();
+            if (mine) {
+                C[i * LDK + j] = ncv;
+                V[i * LDK + j] = nvv;
+            }
+            __syncthreads();
+        }
+        if (!*flag) break;   // every pair below threshold: converged (read after the round's last barrier)
+        __syncthreads();     // before the next sweep clears the flag
+    }
+    return nsw;
+}
+
 // One warp: generalized eigenproblem A y = theta B y (n <= KMAX) and coef = Y f(Theta) Y^T wr.
 // Returns false on a non-SPD B or a non-positive Ritz value (non-singular component).
 __device__ bool ritz_warp(const double* Ain, const double* Bin, const double* wr, int n, bool sing, double theta,
                           double* coef, double* R, double* C, double* V, double* X, double* rot, int* rpq,
-                          unsigned long long* tm = nullptr, int use_reg = 0) {
+                          unsigned long long* tm = nullptr, int use_reg = 0, int stage = 0) {
+    // stage 0: everything on this warp; 1: stop before the Jacobi (the CTA runs jacobi_block); 2: resume after it
     const int lane = threadIdx.x & 31;
-    if (tm && lane == 0) tm[0] = gtimer();
     constexpr int LDK = KMAX + 1;
+    double* rinv = rot;   // 1/L_jj of the Cholesky factor of B (the three triangular solves multiply)
+    double* jsc = rot + KMAX;   // rotation scratch of jacobi_smem
+    int nsw = 0;
+    if (stage != 2) {
+    if (tm && lane == 0) tm[0] = gtimer();
     for (int idx = lane; idx < n * n; idx += 32) {
         const int i = idx / n, j = idx - i * n;
         C[i * LDK + j] = 0.5 * (Ain[i * KMAX + j] + Ain[j * KMAX + i]);
@@ -1154,8 +1270,6 @@ __device__ bool ritz_warp(const double* Ain, const double* Bin, const double* wr
         V[i * LDK + j] = (i == j) ? 1.0 : 0.0;
     }
     __syncwarp();
-    // rinv (the unused rot scratch) keeps 1/L_jj: the three triangular solves multiply instead of divide
-    double* rinv = rot;
     for (int j = 0; j < n; ++j) {
         const double d = R[j * LDK + j];
         if (!(d > 0.0)) return false;
@@ -1197,9 +1311,10 @@ __device__ bool ritz_warp(const double* Ain, const double* Bin, const double* wr
     }
     __syncwarp();
     if (tm && lane == 0) tm[1] = gtimer();
-    int nsw = 0;
-    double* jsc = rot + KMAX;   // rotation scratch of jacobi_smem (rot itself keeps 1/L_jj)
-    if (n > 1 && !use_reg) {
+    }   // stage != 2
+    if (stage == 1) return true;
+    if (stage == 2) {
+    } else if (n > 1 && use_reg != 1) {
         switch ((n + 1) & ~1) {
             case 2: nsw = jacobi_smem<2>(C, V, n, jsc); break;
             case 4: nsw = jacobi_smem<4>(C, V, n, jsc); break;
@@ -1224,7 +1339,7 @@ __device__ bool ritz_warp(const double* Ain, const double* Bin, const double* wr
     }
     if (tm && lane == 0) {
         tm[2] = gtimer();
-        tm[4] = nsw;
+        if (stage == 0) tm[4] = nsw;
     }
     int bad = 0;
     double g = 0.0;
@@ -1287,21 +1402,25 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
 #define ZERO_VALS()                                    \
     _Pragma("unroll") for (int v_ = 0; v_ < KM + 2; ++v_) vals[v_] = 0.0
 
-    // ---- r_c gather and zero test
-    ZERO_VALS();
-    for (int64_t i = r0; i < hi; i += rs) {
-        const double x = a.r[P.cmap[i]];
-        P.rf[i] = x;
-        vals[0] += x * x;
+    // ---- r_c gather and zero test. Fused seed elimination (2D): no gather phase -- the seed solve reads r through
+    // the skeleton map, the consumer phase below stores r_c, and a zero component shows as ||s||_M = 0 (M is SPD).
+    const bool fuseM = P.eM.tri && P.eM.fuse;
+    if (!fuseM) {
+        ZERO_VALS();
+        for (int64_t i = r0; i < hi; i += rs) {
+            const double x = a.r[P.cmap[i]];
+            P.rf[i] = x;
+            vals[0] += x * x;
+        }
+        block_partials(a, vals, 1, pp, c, lb, sred);
+        grid.sync();
+        __syncwarp();   // lane 0 spun in the barrier: reconverge before warp-synchronous code
+        STAMP(stamp++);
+        read_totals(a, pp, 1, nb, tot);
+        pp ^= 1;
     }
-    block_partials(a, vals, 1, pp, c, lb, sred);
-    grid.sync();
-    __syncwarp();   // lane 0 spun in the barrier: reconverge before warp-synchronous code
-    STAMP(stamp++);
-    read_totals(a, pp, 1, nb, tot);
-    pp ^= 1;
     if (tid < nc) {
-        act[tid] = tot[tid][0] > 0.0 ? 1 : 0;
+        act[tid] = fuseM ? 1 : (tot[tid][0] > 0.0 ? 1 : 0);
         kcs[tid] = 0;
         brk[tid] = 0;
         scl[tid] = 1.0;
@@ -1310,12 +1429,12 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
     // Basis vectors are stored unnormalised (W_t = sclh_t * Wraw_t, likewise M W_t and L W_t): every
     // consumer folds sclh_t into its coefficients, so no normalisation pass over the rows is needed.
     // ---- s = M^-1 r (exact) = Wraw_0
-    elim_coop<KM, TIM>(grid, a, P.eM, P.rf, scl, P.W, dsm, c, lb, nbc, stamp, nelim);
+    if (fuseM) elim_coop<KM, TIM>(grid, a, P.eM, a.r, scl, P.W, dsm, c, lb, nbc, stamp, nelim, 0, 0, 0, 0, 1, P.cmap);
+    else elim_coop<KM, TIM>(grid, a, P.eM, P.rf, scl, P.W, dsm, c, lb, nbc, stamp, nelim);
     // ---- Ms, Ls, ||s||_M; q_1 = s / ||s||_M; rhs of the next solve M q_1 = Ms / ||s||_M
     ZERO_VALS();
     double* gacc = dsm;   // per-thread Gram accumulators [GW][CT] (dsm is free outside face solves / Ritz)
     gram_zero(gacc);
-    const bool fuseM = P.eM.tri && P.eM.fuse;
     for (int64_t i = r0; i < hi; i += rs) {
         double m, l, sv;
         if (fuseM) {
@@ -1331,7 +1450,14 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
         vals[0] += sv * m;
         gacc[0 * CT + tid] += sv * l;            // G_L[0][0] (unscaled)
         gacc[KMAX * CT + tid] += sv * m;         // G_M[0][0]
-        gacc[2 * KMAX * CT + tid] += sv * P.rf[i];   // (W^T r)[0]
+        double rv;
+        if (fuseM) {
+            rv = a.r[P.cmap[i]];
+            P.rf[i] = rv;
+        } else {
+            rv = P.rf[i];
+        }
+        gacc[2 * KMAX * CT + tid] += sv * rv;   // (W^T r)[0]
     }
     gram_partials(a, gacc, c, lb, 0);
     block_partials(a, vals, 1, pp, c, lb, sred);
@@ -1342,6 +1468,7 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
     pp ^= 1;
     if (tid < nc) {
         nrmv[tid] = sqrt(tot[tid][0]);
+        if (fuseM) act[tid] = tot[tid][0] > 0.0 ? 1 : 0;   // r_c = 0 <=> s = M^-1 r_c = 0 <=> ||s||_M = 0
         if (act[tid]) kcs[tid] = 1;
         scl[tid] = act[tid] ? 1.0 / nrmv[tid] : 0.0;
         sclh[tid][0] = scl[tid];
@@ -1354,7 +1481,7 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
     const bool fuseK = P.eK.tri && P.eK.fuse;
     for (int j = 1; j < P.kmax; ++j) {
         const bool fold = a.fold && fuseK;   // h summed inside the elimination (R22): no phase A, no barrier
-        elim_coop<KM, TIM>(grid, a, P.eK, j == 1 ? P.MW : P.Mw, scl, P.w, dsm, c, lb, nbc, stamp, nelim,
+        elim_coop<KM, TIM>(grid, a, P.eK, P.MW + size_t(j - 1) * nf, scl, P.w, dsm, c, lb, nbc, stamp, nelim,
                        fold ? j : 0, kcs[c], pp, r0, rs);   // w = K^-1 M q_j
         const bool part = act[c] && !brk[c];
         const int kc = kcs[c];
@@ -1507,8 +1634,7 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
                     l -= hsm[c][t] * lt[t];
                 }
                 P.W[size_t(j) * nf + i] = x;
-                P.MW[size_t(j) * nf + i] = m;
-                P.Mw[i] = m;
+                P.MW[size_t(j) * nf + i] = m;   // also the next solve's right-hand side (unnormalised, scaled by scl)
                 P.LW[size_t(j) * nf + i] = l;
                 vals[0] += x * m;
 #pragma unroll
@@ -1553,31 +1679,10 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
         __syncthreads();
         if (j + 1 < P.kmax && tid < 32) gram_row_sums(a, j, kcs, blockIdx.x, nb, nb);
     }
-    // block 0: the last Gram row's fixed-order sums, then the Gram matrices (scaled by the normalisation of
-    // each row) into the components' LzState for k_prec_ritz
+    // block 0: per component the basis size, activity and the scales; the last Gram row's fixed-order sums and the
+    // scaled Gram matrices are formed by k_prec_ritz (one CTA per component) instead of serially here
     if (blockIdx.x == 0) {
-        gram_row_sums(a, P.kmax - 1, kcs, tid >> 5, CW, nb);   // rows < kmax-1 were summed in the loop
-        __syncthreads();
-        for (int e = tid; e < nc * KMAX * GW; e += CT) {
-            const int cc = e / (KMAX * GW), rem = e - cc * (KMAX * GW), jr = rem / GW, v = rem - jr * GW;
-            if (jr >= kcs[cc]) continue;
-            const int kind = v < KMAX ? 0 : (v < 2 * KMAX ? 1 : 2), t = kind == 0 ? v : v - KMAX;
-            if (kind < 2 && t > jr) continue;
-            const double acc = *((volatile const double*)(a.gram_tot + (size_t(cc) * KMAX + jr) * GW + v));
-            const double sj = sclh[cc][jr];
-            LzState& zs = P.lz[cc];
-            if (kind == 2) {
-                zs.wr[jr] = sj * acc;
-            } else {
-                const double g = sj * sclh[cc][t] * acc;   // (sclh_j Wraw_j)^T L (sclh_t Wraw_t)
-                double* G = kind == 0 ? zs.A : zs.B;
-                G[jr * KMAX + t] = g;
-                G[t * KMAX + jr] = g;
-            }
-        }
-        __syncthreads();
-        STAMP(stamp++);
-        if (tid < nc * KMAX) {   // per component: basis size, activity and the scales for the combine
+        if (tid < nc * KMAX) {
             const int cc = tid / KMAX, t = tid - cc * KMAX;
             LzState& zs = P.lz[cc];
             zs.sc[t] = t < kcs[cc] ? sclh[cc][t] : 0.0;
@@ -1586,6 +1691,7 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
                 zs.active = act[cc];
             }
         }
+        STAMP(stamp++);
     }
     // every elimination's arrivals lie before the last grid barrier above: leave the counter at zero for the next launch
     if (blockIdx.x == 0 && tid == 0) *a.arrive = 0u;
@@ -1595,27 +1701,78 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
 
 #undef ZERO_VALS
 
-// One warp per component: the k x k Ritz problem of the Gram matrices left by k_prec_coop -> coefficients
-// (no register cap: the Jacobi and the triangular solves stay in registers).
+// One CTA per component: the last Gram row's fixed-order sums (rows < kmax-1 were summed inside k_prec_coop), the
+// Gram matrices scaled by the basis normalisation, then the k x k Ritz problem on warp 0 -> coefficients
+// (no register cap here: the Jacobi and the triangular solves stay in registers / shared memory).
 template <bool TIM>
-__global__ void __launch_bounds__(32) k_prec_ritz(PrecDev P, const PcgState* s, unsigned long long* timers) {
+__global__ void __launch_bounds__(CT) k_prec_ritz(PrecDev P, const double* __restrict__ gram,
+                                                  const double* __restrict__ gram_tot, int nbc_max, int nb,
+                                                  const PcgState* s, unsigned long long* timers) {
     if (s != nullptr && s->done) return;
     extern __shared__ double rsm[];
-    const int w = blockIdx.x, lane = threadIdx.x & 31;   // one single-warp CTA per component
+    __shared__ double As[KMAX * KMAX], Bs[KMAX * KMAX], wrs[KMAX], lastrow[GW], scs[KMAX];
+    const int w = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;   // CTA w = component w
     if (w >= P.ncomp) return;
     LzState& zs = P.lz[w];
-    if (lane < KMAX) zs.coef[lane] = 0.0;
-    __syncwarp();
+    if (tid < KMAX) zs.coef[tid] = 0.0;
     if (!zs.active) return;
+    const int kc = zs.kc, nc = P.ncomp;
+    if (tid < KMAX) scs[tid] = zs.sc[tid];
+    if (TIM && timers && w == 0 && tid == 0) timers[100] = gtimer();
+    if (kc == P.kmax) {   // row kmax-1: lanes add the block partials b = lane, lane+32, .. in order, then a warp tree
+        const int jr = kc - 1, per = 2 * (jr + 1) + 1, nbcc = (nb - w + nc - 1) / nc;
+        for (int q = wid; q < per; q += CW) {
+            const int v = q <= jr ? q : (q < 2 * (jr + 1) ? KMAX + (q - jr - 1) : 2 * KMAX);
+            const double* pg = gram + ((size_t(w) * KMAX + jr) * GW + v) * nbc_max;
+            double acc = 0.0;
+            for (int b = lane; b < nbc_max; b += 32) acc += b < nbcc ? pg[b] : 0.0;
+            acc = warp_sum(acc);
+            if (lane == 0) lastrow[v] = acc;
+        }
+    }
+    __syncthreads();
+    for (int e = tid; e < KMAX * GW; e += CT) {
+        const int jr = e / GW, v = e - jr * GW;
+        if (jr >= kc) continue;
+        const int kind = v < KMAX ? 0 : (v < 2 * KMAX ? 1 : 2), t = kind == 0 ? v : v - KMAX;
+        if (kind < 2 && t > jr) continue;
+        const double acc = jr == P.kmax - 1 ? lastrow[v] : gram_tot[(size_t(w) * KMAX + jr) * GW + v];
+        if (kind == 2) {
+            wrs[jr] = scs[jr] * acc;
+        } else {
+            const double g = scs[jr] * scs[t] * acc;   // (sc_j Wraw_j)^T L (sc_t Wraw_t)
+            double* G = kind == 0 ? As : Bs;
+            G[jr * KMAX + t] = g;
+            G[t * KMAX + jr] = g;
+        }
+    }
+    __syncthreads();
     double* R = rsm;
     double* Cm = R + KMAX * (KMAX + 1);
     double* V = Cm + KMAX * (KMAX + 1);
     double* X = V + KMAX * (KMAX + 1);
     double* rot = X + KMAX * (KMAX + 1);
     int* rpq = reinterpret_cast<int*>(rot + KMAX);
-    if (TIM && timers && w == 0 && lane == 0) timers[100] = gtimer();
-    const bool ok = ritz_warp(zs.A, zs.B, zs.wr, zs.kc, P.singular[w] != 0, P.theta, zs.coef, R, Cm, V, X, rot, rpq,
-                              (TIM && timers && w == 0) ? timers + 102 : nullptr, P.jacobi_reg);
+    unsigned long long* tm = (TIM && timers && w == 0) ? timers + 102 : nullptr;
+    bool ok;
+    if (P.jacobi_reg == 0 && kc > 1) {   // default: Cholesky / C = L^-1 A L^-T on warp 0, the Jacobi by the whole CTA
+        __shared__ int sched[KMAX * KMAX], slot_of[KMAX], jflag, okf;
+        __shared__ double csn[KMAX], jred[2 * CW];
+        if (wid == 0) {
+            const bool o1 = ritz_warp(As, Bs, wrs, kc, P.singular[w] != 0, P.theta, zs.coef, R, Cm, V, X, rot, rpq, tm, 0, 1);
+            if (lane == 0) okf = o1 ? 1 : 0;
+        }
+        __syncthreads();
+        int nsw = 0;
+        if (okf) nsw = jacobi_block(Cm, V, kc, sched, slot_of, csn, jred, &jflag);
+        __syncthreads();
+        if (wid != 0) return;
+        if (tm && lane == 0) tm[4] = nsw;
+        ok = okf && ritz_warp(As, Bs, wrs, kc, P.singular[w] != 0, P.theta, zs.coef, R, Cm, V, X, rot, rpq, tm, 0, 2);
+    } else {
+        if (wid != 0) return;
+        ok = ritz_warp(As, Bs, wrs, kc, P.singular[w] != 0, P.theta, zs.coef, R, Cm, V, X, rot, rpq, tm, P.jacobi_reg);
+    }
     if (TIM && timers && w == 0 && lane == 0) timers[101] = gtimer();
     if (!ok && lane == 0) {
         zs.status = DE_EBREAKDOWN;
@@ -1758,8 +1915,8 @@ int prec_apply_coop(const PrecDev& P, const CoopBuffers& B, const double* r, dou
     cudaError_t e = cudaLaunchKernelEx(&cfg, reinterpret_cast<void (*)(CoopArgs)>(const_cast<void*>(B.kfn)), a);
     if (e != cudaSuccess) return -1;
     const size_t rsm = size_t(4 * KMAX * (KMAX + 1) + 6 * KMAX) * sizeof(double);
-    if (B.timers) k_prec_ritz<true><<<P.ncomp, 32, rsm, st>>>(P, s, B.timers);
-    else k_prec_ritz<false><<<P.ncomp, 32, rsm, st>>>(P, s, nullptr);
+    if (B.timers) k_prec_ritz<true><<<P.ncomp, CT, rsm, st>>>(P, B.gram, B.gram_tot, B.nbc_max, B.nb, s, B.timers);
+    else k_prec_ritz<false><<<P.ncomp, CT, rsm, st>>>(P, B.gram, B.gram_tot, B.nbc_max, B.nb, s, nullptr);
     k_prec_combine<<<B.nsm * 4, 256, 0, st>>>(P, z, s);
     e = cudaGetLastError();
     return e == cudaSuccess ? 3 : -1;
