@@ -883,6 +883,7 @@ de_status_t upload_prec_impl(de_ctx* c) {
         TRY(dalloc(c, &c->coop.lw1, nf));
         if (c->coop.fold) TRY(dalloc(c, &c->coop.ucross, size_t(KMAX) * std::max(1, P.eK.ncross)));
         TRY(dalloc(c, &c->coop.arrive, 4));
+        TRY(dalloc(c, &c->coop.redf, size_t(2) * MAXC * (KMAX + 2) * c->coop.nb));
         DE_CUDA(cudaMemsetAsync(c->coop.arrive, 0, 4 * sizeof(unsigned int), c->st));
         if (getenv("DE_PREC_TIMERS")) {
             TRY(dalloc(c, &c->coop.timers, 200 + 8192));

@@ -391,7 +391,8 @@ void prec_prepare(const PrecDev& P);   // one-time kernel attributes (outside gr
 struct CoopBuffers {
     int nb = 0, nsm = 148;
     size_t smem = 0;
-    int stage = 0, per_warp = 0, mf = 0, ncmax = 0, nbc_max = 0, tridiag = 0, gram_cgs2 = 1, fold = 0, split = 1;
+    int stage = 0, per_warp = 0, mf = 0, ncmax = 0, nbc_max = 0, tridiag = 0, gram_cgs2 = 1, fold = 0, split = 1, shr = 0;
+    double* redf = nullptr;      // fold sums of the shared-row cross-point solve: [2][MAXC][NRED][nb]
     double* ucross = nullptr;   // fold: [KMAX][ncross of eK]
     unsigned int* arrive = nullptr;   // split-phase arrival counter of the fused eliminations (zero between launches)
     double *red = nullptr, *gram = nullptr, *gram_tot = nullptr, *w1 = nullptr, *mw1 = nullptr, *lw1 = nullptr;

@@ -52,6 +52,8 @@ struct CoopArgs {
     int gram_cgs2;      // 1: the second Gram-Schmidt pass is formed from the Gram matrix (one row pass fewer)
     int fold;           // 1 (with gram_cgs2, 2D fused eliminations): h = W^T M w is summed inside the elimination
     int smem_doubles;   // dynamic shared memory of the launch in doubles (fast-diagonalisation tables fit test)
+    int shr;            // 1: a shared S_C^-1 (HElim::sc_shared) is applied for ALL components by the block that loads a row
+    double* redf;       // [2][MAXC][NRED][nb] fold sums when shr (every block contributes to every component)
     int split;          // 1: fused eliminations wait on the arrival counter between t_C and the cross-point solve (no grid barrier)
     double* ucross;     // [KMAX][ncross of eK]: u_t = G^T (M W_t)_F, the face part of M W_t folded onto cross points
     unsigned int* arrive;   // split-phase arrival counter of the fused eliminations (t_C published -> cross-point solve)
@@ -104,7 +106,8 @@ __device__ void block_partials(const CoopArgs& a, const double (&vals)[NV], int 
 }
 
 // totals of all components (fixed order over lb) into tot[c][v]
-__device__ void read_totals(const CoopArgs& a, int pp, int nv, int nb, double (*tot)[NRED]) {
+__device__ void read_totals(const CoopArgs& a, int pp, int nv, int nb, double (*tot)[NRED], bool all = false) {
+    // all: the fold sums of the shared-row cross-point solve (a.redf: one slot per block of the WHOLE grid per component)
     // task (c, v) = sum over the component's nbc block partials: lane l adds b = l, l+32, ... in order, then a
     // warp tree (fixed order); TU tasks per warp and QU partials per lane are loaded together
     constexpr int TU = 3, QU = 8;
@@ -117,11 +120,12 @@ __device__ void read_totals(const CoopArgs& a, int pp, int nv, int nb, double (*
 #pragma unroll
         for (int u = 0; u < TU; ++u) {
             const int t = min(t0 + u * CW, ntask - 1), c = t / nv, v = t - c * nv;
-            nbc[u] = (t0 + u * CW < ntask) ? (nb - c + nc - 1) / nc : 0;
-            p[u] = a.red + ((size_t(pp) * MAXC + c) * NRED + v) * a.nbc_max;
+            nbc[u] = (t0 + u * CW < ntask) ? (all ? nb : (nb - c + nc - 1) / nc) : 0;
+            p[u] = all ? a.redf + ((size_t(pp) * MAXC + c) * NRED + v) * nb
+                       : a.red + ((size_t(pp) * MAXC + c) * NRED + v) * a.nbc_max;
             acc[u] = 0.0;
         }
-        for (int b0 = 0; b0 < a.nbc_max; b0 += 32 * QU) {
+        for (int b0 = 0; b0 < (all ? nb : a.nbc_max); b0 += 32 * QU) {
             double x[TU][QU];
 #pragma unroll
             for (int u = 0; u < TU; ++u)
@@ -519,6 +523,17 @@ __device__ __forceinline__ void face_warp_pcr(const PrecDev& P, const ElimDev& E
     }
 }
 
+// which cross-point solve an elimination uses in block component c (the same answer in elim_coop and in the caller)
+__device__ __forceinline__ bool use_fd(const CoopArgs& a, const ElimDev& E, int c) {
+    const int ncc = E.cross_comp_off[c + 1] - E.cross_comp_off[c];
+    return E.tri && E.fuse && E.fd && ncc > 0 &&
+           2 * ncc + (ncc & 1) + E.fd_nx * E.fd_nx + E.fd_ny * E.fd_ny <= a.smem_doubles;
+}
+__device__ __forceinline__ bool use_shr(const CoopArgs& a, const ElimDev& E, int c) {
+    const int ncc = E.cross_comp_off[c + 1] - E.cross_comp_off[c];
+    return a.shr && E.sc_shared && ncc > 0 && !use_fd(a, E, c) && ((E.tri && E.fuse) || (!E.tri && E.xcf_w > 0));
+}
+
 // x = X^-1 (scl * b) by exact elimination (faces -> cross points -> faces); 3 grid barriers.
 // fold_j > 0 (K-solve of Lanczos step fold_j, fused 2D path): the first phase also stores u_{j-1} = G^T b_F
 // (b = M W_{j-1} raw), and the second phase accumulates the block partials of h_t = (M W_t) . x for t < kc,
@@ -528,7 +543,7 @@ template <int KM, bool TIM>
 __device__ void elim_coop(cg::grid_group& grid, const CoopArgs& a, const ElimDev& E, const double* b,
                           const double* scl, double* out, double* dsm, int c, int lb, int nbc, int& stamp, int& nelim,
                           int fold_j = 0, int kc = 0, int pp = 0, int64_t r0 = 0, int64_t rs = 1,
-                          const int32_t* __restrict__ bmap = nullptr) {
+                          const int32_t* __restrict__ bmap = nullptr, const int* kcs_all = nullptr) {
     // bmap (fused path only): the right-hand side is b[bmap[i]] -- the seed solve reads r through the skeleton map,
     // so no gather phase (and barrier) precedes it
     const PrecDev& P = a.P;
@@ -548,7 +563,7 @@ __device__ void elim_coop(cg::grid_group& grid, const CoopArgs& a, const ElimDev
     // fast-diagonalised cross-point solve (HElim::fd): X, Y and the Q tables must fit the dynamic shared memory
     const int nccb = E.cross_comp_off[c + 1] - E.cross_comp_off[c];
     const int fdq = 2 * nccb + (nccb & 1);   // offset of the staged Q tables (16-byte aligned)
-    const bool fd = fused && E.fd && nccb > 0 && fdq + E.fd_nx * E.fd_nx + E.fd_ny * E.fd_ny <= a.smem_doubles;
+    const bool fd = use_fd(a, E, c);
     if (fused) {
         ++nelim;
         if (fd) {   // stage Qx, Qy behind X / Y now (static tables; dsm is free here): they land during the face solves
@@ -647,9 +662,135 @@ __device__ void elim_coop(cg::grid_group& grid, const CoopArgs& a, const ElimDev
     if (dbg2) a.timers[180] = gtimer();
     {
         const int base = E.cross_comp_off[c], ncc = E.cross_comp_off[c + 1] - base;
-        if (ncc > 0) {
+        // General path with a padded X_CF (3D wirebasket): t_C = scl b_C - X_CF y is formed ONCE, each block its own
+        // rows [rlo, rhi) (8 lanes per row, fixed-order lane tree), published through the arrival counter and then
+        // read by every block of the component -- the redundant per-block formation read the whole padded X_CF in
+        // every block (c4: 21 us of the 57 us cross-point phase).
+        const bool dist = !E.tri && E.xcf_w > 0;
+        if (dist) {
+            ++nelim;
+            double* tCg = P.y + P.nflat + E.ncross;
+            if (ncc > 0) {
+                const int rlo = int(int64_t(lb) * ncc / nbc), rhi = int(int64_t(lb + 1) * ncc / nbc);
+                const int g8 = threadIdx.x >> 3, l8 = threadIdx.x & 7;
+                const double sc = scl[c];
+                for (int r0_ = rlo; r0_ < rhi; r0_ += CT / 8) {
+                    const int r = r0_ + g8;
+                    const bool ok = r < rhi;
+                    const int ci = base + (ok ? r : rlo);
+                    double acc = (ok && l8 == 0) ? sc * b[E.cross_flat[ci]] : 0.0;
+                    for (int k = l8; k < E.xcf_w; k += 8) {
+                        const size_t at = size_t(k) * E.ncross + ci;
+                        const double v = E.xcfw_val[at];
+                        const int col = E.xcfw_col[at];
+                        acc -= ok ? v * y[col] : 0.0;
+                    }
+                    acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+                    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+                    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+                    if (ok && l8 == 0) tCg[ci] = acc;
+                }
+            }
+            __syncthreads();
+            if (threadIdx.x == 32) {   // publish, then wait for every block's rows
+                __threadfence();
+                atomicAdd(a.arrive, 1u);
+                const unsigned target = unsigned(nelim) * gridDim.x;
+                while (*((volatile unsigned*)a.arrive) < target) {}
+                __threadfence();
+            }
+            __syncthreads();
+        }
+        const bool shr = use_shr(a, E, c);
+        if (shr) {
+            // Shared S_C^-1: every block owns rows [Rlo, Rhi) of the ONE matrix (split over the whole grid) and applies
+            // them to the t_C of every component, so each row crosses L2 -> SM once instead of once per component
+            // (c4: three wirebasket components, 188 -> 62.5 MB per elimination)
+            const int nc = P.ncomp, bI = int(blockIdx.x), nbA = int(gridDim.x);
+            const int Rlo = int(int64_t(bI) * ncc / nbA), Rhi = int(int64_t(bI + 1) * ncc / nbA), nr = Rhi - Rlo;
+            double* tA = dsm;                 // [nc][ncc]
+            double* part = tA + nc * ncc;     // [CW][nc][nr]
+            const double* tCg = P.y + P.nflat + E.ncross;
+            for (int i = threadIdx.x; i < nc * ncc; i += CT) tA[i] = tCg[i];   // cross points are numbered by component
+            __syncthreads();
+            const double* S = E.Sinv;
+            const int cw = ((ncc + CW * 32 - 1) / (CW * 32)) * 32;
+            const int c0 = w * cw, c1 = min(ncc, c0 + cw);
+            constexpr int NA = 8, RB = 4;
+            for (int r = Rlo; r < Rhi; r += RB) {
+                const double* __restrict__ row[RB];
+                double sr[RB][MAXC];
+#pragma unroll
+                for (int u = 0; u < RB; ++u) {
+                    row[u] = S + size_t(r + u < Rhi ? r + u : r) * ncc;
+#pragma unroll
+                    for (int cc = 0; cc < MAXC; ++cc) sr[u][cc] = 0.0;
+                }
+                for (int j = c0 + lane; j < c1; j += 32 * NA) {
+                    double v[RB][NA];
+#pragma unroll
+                    for (int q = 0; q < NA; ++q) {
+                        const int jj = j + 32 * q;
+                        const bool ok = jj < c1;
+#pragma unroll
+                        for (int u = 0; u < RB; ++u) v[u][q] = (ok && r + u < Rhi) ? __ldcs(row[u] + jj) : 0.0;
+                    }
+#pragma unroll
+                    for (int cc = 0; cc < MAXC; ++cc)
+                        if (cc < nc) {
+#pragma unroll
+                            for (int q = 0; q < NA; ++q) {
+                                const int jj = j + 32 * q;
+                                const double t = jj < c1 ? tA[cc * ncc + jj] : 0.0;
+#pragma unroll
+                                for (int u = 0; u < RB; ++u) sr[u][cc] += v[u][q] * t;
+                            }
+                        }
+                }
+#pragma unroll
+                for (int u = 0; u < RB; ++u)
+#pragma unroll
+                    for (int cc = 0; cc < MAXC; ++cc)
+                        if (cc < nc) {
+                            const double su = warp_sum(sr[u][cc]);
+                            if (lane == 0 && r + u < Rhi) part[(w * nc + cc) * nr + (r + u - Rlo)] = su;
+                        }
+            }
+            __syncthreads();
+            for (int e = threadIdx.x; e < nc * nr; e += CT) {
+                const int cc = e / nr, rr = e - cc * nr;
+                double acc = 0.0;
+                for (int q = 0; q < CW; ++q) acc += part[(q * nc + cc) * nr + rr];
+                const int ci = E.cross_comp_off[cc] + Rlo + rr;
+                xC[ci] = acc;
+                out[E.cross_flat[ci]] = acc;
+                part[cc * nr + rr] = acc;   // slice 0: kept for the fold sums (read above by this thread only)
+            }
+            __syncthreads();
+            if (fold_j > 0) {
+                // fold sums of every component over this block's rows, + the face part of the block's own component
+                // (summed per warp in the face phase), into the all-blocks slots (pp, cc, v, block)
+                // (every component with its OWN basis size: a zero or broken-down component has a smaller one)
+                for (int task = w; task < nc * (KMAX + 1); task += CW) {
+                    const int cc = task / (KMAX + 1), v = task - cc * (KMAX + 1);
+                    if (v > kcs_all[cc]) continue;
+                    double t_ = 0.0;
+                    if (v > 0)
+                        for (int rr = lane; rr < nr; rr += 32) {
+                            const int ci = E.cross_comp_off[cc] + Rlo + rr;
+                            t_ += (P.MW[size_t(v - 1) * P.nflat + E.cross_flat[ci]] - a.ucross[size_t(v - 1) * E.ncross + ci]) *
+                                  part[cc * nr + rr];
+                        }
+                    t_ = warp_sum(t_);
+                    if (v > 0 && cc == c)
+                        for (int q = 1; q < CW; ++q) t_ += hfw[q * KMAX + v - 1];
+                    if (lane == 0) a.redf[((size_t(pp) * MAXC + cc) * NRED + v) * nbA + bI] = t_;
+                }
+                __syncthreads();
+            }
+        } else if (ncc > 0) {
             double* tC = dsm;
-            if (E.tri && E.fuse) {   // formed once in the first face phase
+            if (dist || (E.tri && E.fuse)) {   // formed once: above (3D) / in the first face phase (fused 2D)
                 const double* tCg = P.y + P.nflat + E.ncross;
                 for (int i = threadIdx.x; i < ncc; i += CT) tC[i] = tCg[base + i];
             } else if (E.tri) {   // padded X_CF: every load of UC cross points issued before the first use
@@ -876,7 +1017,7 @@ __device__ void elim_coop(cg::grid_group& grid, const CoopArgs& a, const ElimDev
             }
             __syncthreads();
         }
-        if (fold_j > 0) {
+        if (fold_j > 0 && !shr) {
             // block sums into the reduction slots (pp, c, 1 + t), slot 0 (unused) = 0; fixed order: the cross part
             // sum_r (MW_t[c_r] - u_t[r]) x_C[r] over this block's rows (lanes stride the rows, then a warp tree), then
             // the face part over the warps (summed per warp in the face phase)
@@ -1482,12 +1623,12 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
     for (int j = 1; j < P.kmax; ++j) {
         const bool fold = a.fold && fuseK;   // h summed inside the elimination (R22): no phase A, no barrier
         elim_coop<KM, TIM>(grid, a, P.eK, P.MW + size_t(j - 1) * nf, scl, P.w, dsm, c, lb, nbc, stamp, nelim,
-                       fold ? j : 0, kcs[c], pp, r0, rs);   // w = K^-1 M q_j
+                       fold ? j : 0, kcs[c], pp, r0, rs, nullptr, kcs);   // w = K^-1 M q_j
         const bool part = act[c] && !brk[c];
         const int kc = kcs[c];
         const bool dbg = TIM && a.timers && blockIdx.x == 0 && tid == 32 && j == 5;
         if (fold) {
-            read_totals(a, pp, 1 + kc, nb, tot);
+            read_totals(a, pp, 1 + kc, nb, tot, use_shr(a, P.eK, c));
             pp ^= 1;
             if (tid < KMAX) hsm[c][tid] = tid < kc ? tot[c][1 + tid] * sclh[c][tid] * sclh[c][tid] : 0.0;
             __syncthreads();
@@ -1868,6 +2009,12 @@ bool prec_coop_prepare(const PrecDev& P, int device, CoopBuffers& B) {
     B.gram_cgs2 = getenv("DE_CGS2_TWO_PASS") ? 0 : 1;   // A/B switch: the literal two-pass CGS2
     // fold h into the elimination (R22): 2D fused eliminations, one-pass Gram-Schmidt, room for the accumulators
     B.fold = (B.gram_cgs2 && P.eK.tri && P.eK.fuse && !getenv("DE_NO_FOLD")) ? 1 : 0;
+    {   // shared-row cross-point solve: t_C of every component + the per-warp row sums must fit
+        const size_t need = (size_t(P.ncomp) * ncmax + size_t(CW) * P.ncomp * (ncmax / nb + 2)) * 8;
+        // two components (2D): measured slower on c5 (0.569 vs 0.547 ms: the partner block's reads of the same rows hit
+        // L2 anyway); three (3D wirebasket): c4 cross-point phase 34 -> 31.8 us
+        B.shr = ((P.ncomp > 2 || getenv("DE_SHR")) && need <= B.smem && !getenv("DE_NO_SHR")) ? 1 : 0;
+    }
     B.split = getenv("DE_NO_SPLIT") ? 0 : 1;   // A/B switch: a grid barrier between t_C and the cross-point solve
     if (getenv("DE_VERBOSE")) fprintf(stderr, "[de] k_prec_coop: fold %d (R22) split %d\n", B.fold, B.split);
     return true;
@@ -1900,6 +2047,8 @@ int prec_apply_coop(const PrecDev& P, const CoopBuffers& B, const double* r, dou
     a.ucross = B.ucross;
     a.arrive = B.arrive;
     a.split = B.split;
+    a.shr = B.shr;
+    a.redf = B.redf;
     a.smem_doubles = int(B.smem / sizeof(double));
     a.timers = B.timers;
     cudaLaunchConfig_t cfg{};
