@@ -512,6 +512,25 @@ de_status_t upload_prec_impl(de_ctx* c) {
             const int nc = E.cross_comp_off[cc + 1] - E.cross_comp_off[cc];
             if (nc > 0) launch_gauss_jordan(D.Sinv + E.sc_off[cc], gjbuf, nc, c->st);
         }
+        D.g3_items = 0;   // 3D: dense G_F = X_FF^-1 X_F,adj per face for the second face phase (HElim::g3)
+        D.g3_item_face = D.g3_item_i0 = D.g3_adj_ptr = D.g3_adj = nullptr;
+        D.g3_off = nullptr;
+        D.g3 = nullptr;
+        if (!E.g3.empty() && int(E.g3_off.size()) == E.nfaces + 1) {
+            std::vector<int32_t> itf, iti;
+            for (int F = 0; F < E.nfaces; ++F)
+                for (int i0 = 0; i0 < E.face_off[F + 1] - E.face_off[F]; i0 += 32) {
+                    itf.push_back(F);
+                    iti.push_back(i0);
+                }
+            TRY(dupload(c, &D.g3_item_face, itf));
+            TRY(dupload(c, &D.g3_item_i0, iti));
+            TRY(dupload(c, &D.g3_off, E.g3_off));
+            TRY(dupload(c, &D.g3, E.g3));
+            TRY(dupload(c, &D.g3_adj_ptr, E.g3_adj_ptr));
+            TRY(dupload(c, &D.g3_adj, E.g3_adj));
+            D.g3_items = int32_t(itf.size());
+        }
         D.fd = E.fd;   // fast diagonalisation of a separable S_C (HElim::fd): the cooperative kernel's cross-point solve
         D.fd_nx = E.fd_nx;
         D.fd_ny = E.fd_ny;

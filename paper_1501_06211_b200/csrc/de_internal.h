@@ -57,6 +57,13 @@ struct HElim {
     // 1 when every component's S_C is bitwise identical to component 0's (same skeleton and Dirichlet rows:
     // the trace norm is componentwise): one S_C^-1 serves all components
     int32_t sc_shared = 0;
+    // 3D: G_F = X_FF^-1 X_F,adj per face (dense, column-major: column e over the face's nodes), adj = the face's
+    // distinct wirebasket neighbours: the second face phase x_F = y_F - G_F x_C(adj) becomes a streaming pass instead of
+    // a second sequential band solve
+    std::vector<int64_t> g3_off;        // [nfaces+1] offsets into g3
+    std::vector<double> g3;
+    std::vector<int32_t> g3_adj_ptr;    // [nfaces+1] into g3_adj
+    std::vector<int32_t> g3_adj;        // cross indices
     // Fast diagonalisation of S_C (2D, R23): when the cross points of every component form a full
     // nx x ny tensor grid (index = ix + nx iy) and S_C = A_x (x) I + I (x) A_y exactly (uniform skeleton, unweighted
     // trace norm, Dirichlet rows on whole edges), S_C^-1 = (Q_y (x) Q_x) diag(1 / (lam_a + mu_b)) (Q_y (x) Q_x)^T with
@@ -207,6 +214,12 @@ struct ElimDev {
     int32_t xcf_w;
     int32_t* xcfw_col;
     double* xcfw_val;
+    // G_F = X_FF^-1 X_F,adj per face (HElim::g3), non-tri only: work items (face, 32-node chunk) for the second face phase
+    int32_t g3_items;
+    int32_t *g3_item_face, *g3_item_i0;
+    int64_t* g3_off;
+    double* g3;
+    int32_t *g3_adj_ptr, *g3_adj;
     // warp-per-face parallel cyclic reduction of X_FF y = b (tri only): lane j = face node j, 32 lanes per face
     // (identity rows past the face end); per face [PCR_Q][32] doubles: (alpha, gamma) of the 5 reduction
     // levels, then 1/d after the last level; pcr_node[F*32 + j] = flat index (0 past the end)

@@ -368,6 +368,11 @@ de_status_t build_elim(const HostSetup& hs, const HCsr& X, HElim& E) {
         }
     }
     std::vector<double> g;
+    const bool keep_g = hs.dim == 3 && !getenv("DE_NO_G3");
+    E.g3_off.assign(1, 0);
+    E.g3.clear();
+    E.g3_adj_ptr.assign(1, 0);
+    E.g3_adj.clear();
     for (int32_t F = 0; F < E.nfaces; ++F) {
         const int32_t o = E.face_off[F], n = E.face_off[F + 1] - o;
         std::vector<int32_t> adj;
@@ -375,6 +380,11 @@ de_status_t build_elim(const HostSetup& hs, const HCsr& X, HElim& E) {
             for (int32_t k = E.XFC.ptr[o + i]; k < E.XFC.ptr[o + i + 1]; ++k) adj.push_back(E.XFC.col[k]);
         std::sort(adj.begin(), adj.end());
         adj.erase(std::unique(adj.begin(), adj.end()), adj.end());
+        if (keep_g) {
+            E.g3_adj.insert(E.g3_adj.end(), adj.begin(), adj.end());
+            E.g3_adj_ptr.push_back(int32_t(E.g3_adj.size()));
+            E.g3_off.push_back(E.g3_off.back() + int64_t(n) * int64_t(adj.size()));
+        }
         if (adj.empty()) continue;
         const int na = int(adj.size());
         std::vector<double> XF(size_t(n) * na, 0.0);   // X_F,adj (column-major: col e contiguous)
@@ -390,6 +400,7 @@ de_status_t build_elim(const HostSetup& hs, const HCsr& X, HElim& E) {
         for (int e = 0; e < na; ++e) {
             for (int32_t i = 0; i < n; ++i) g[i] = XF[size_t(e) * n + i];
             small_band_solve(n, E.face_band[F], &E.face_fac[E.face_fac_off[F]], g.data());
+            if (keep_g) E.g3.insert(E.g3.end(), g.begin(), g.end());   // column e of G_F
             for (int e2 = 0; e2 < na; ++e2) {
                 double t = 0.0;
                 for (int32_t i = 0; i < n; ++i) t += XF[size_t(e2) * n + i] * g[i];

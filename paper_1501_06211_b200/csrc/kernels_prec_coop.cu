@@ -1048,6 +1048,36 @@ __device__ void elim_coop(cg::grid_group& grid, const CoopArgs& a, const ElimDev
     if (E.tri) {
         if (w > 0)
             for (int F = gt; F < E.nfaces; F += nthr) face_thread_tridiag(a, E, F, b, scl, xC, out, 1, dsm + (threadIdx.x - 32));
+    } else if (E.g3_items > 0) {
+        // x_F = y_F - G_F x_C(adj) with the dense G_F = X_FF^-1 X_F,adj of every face (HElim::g3): a streaming pass,
+        // one warp per (face, 32-node chunk), instead of a second sequential band solve per face
+        if (w > 0)
+            for (int it = gw; it < E.g3_items; it += nwarps) {
+                const int F = E.g3_item_face[it], i = E.g3_item_i0[it] + lane;
+                const int o = E.face_off[F], n = E.face_off[F + 1] - o;
+                const int a0 = E.g3_adj_ptr[F], na = E.g3_adj_ptr[F + 1] - a0;
+                const double* __restrict__ G = E.g3 + E.g3_off[F];
+                const bool ok = i < n;
+                const int node = ok ? E.face_nodes[o + i] : 0;
+                double acc = ok ? y[node] : 0.0;
+                for (int e0 = 0; e0 < na; e0 += 32) {
+                    const double xe = e0 + lane < na ? xC[E.g3_adj[a0 + e0 + lane]] : 0.0;   // lane e holds x_C(adj e)
+                    const int ne = min(32, na - e0);
+                    int e = 0;
+                    for (; e + 8 <= ne; e += 8) {
+                        double gv[8];
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) gv[q] = ok ? __ldcs(G + size_t(e0 + e + q) * n + i) : 0.0;   // streamed once
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) acc = fma(-gv[q], __shfl_sync(0xffffffffu, xe, e + q), acc);
+                    }
+                    for (; e < ne; ++e) {
+                        const double gv = ok ? __ldcs(G + size_t(e0 + e) * n + i) : 0.0;
+                        acc = fma(-gv, __shfl_sync(0xffffffffu, xe, e), acc);
+                    }
+                }
+                if (ok) out[node] = acc;
+            }
     } else if (w > 0)
         for (int F = gw; F < E.nfaces; F += nwarps) face_warp(a, E, F, b, scl, xC, out, 1, wsm, lane);
     if (TIM && a.timers && lane == 0 && w > 0 && gw < 4096) a.timers[200 + 4096 + gw] = clock64() - tf0;
