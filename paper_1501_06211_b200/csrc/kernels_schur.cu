@@ -577,7 +577,8 @@ __device__ __forceinline__ double warp_sum_d(double v) {
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     return v;
 }
-constexpr int BK_T = 256, BK_P = 16, BK_S = 2;   // threads, panel columns, ring stages
+constexpr int BK_T = 256;   // threads; BK_P panel columns, BK_S ring stages (template: tuned per band width)
+template <int BK_P, int BK_S>
 __global__ void __launch_bounds__(BK_T, 1) k_schur_blk(SchurArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     if (a.state != nullptr && a.state->done) return;
@@ -696,11 +697,30 @@ __global__ void __launch_bounds__(BK_T, 1) k_schur_blk(SchurArgs a) {
     }
 }
 
+// panel width / ring depth of k_schur_blk: the deepest ring of the narrowest panels that fits shared memory keeps the
+// most bulk copies in flight (measured on c4, ld = 474; env DE_BLK_VARIANT overrides: 0 = 16 x 2, 1 = 8 x 4, 2 = 12 x 3,
+// 3 = 8 x 5, 4 = 4 x 8)
+typedef void (*blk_fn)(SchurArgs);
+struct BlkVariant {
+    blk_fn fn;
+    size_t smem;
+};
+static BlkVariant blk_variant(int ld, int max_nI, int maxG, bool set_attr) {
+    static const int PS[5][2] = {{16, 2}, {8, 4}, {12, 3}, {8, 5}, {4, 8}};
+    static const blk_fn FN[5] = {k_schur_blk<16, 2>, k_schur_blk<8, 4>, k_schur_blk<12, 3>, k_schur_blk<8, 5>, k_schur_blk<4, 8>};
+    int v = 1;
+    if (const char* e = getenv("DE_BLK_VARIANT")) v = std::max(0, std::min(4, atoi(e)));
+    auto need = [&](int k) { return 128 + sizeof(double) * (size_t(PS[k][1]) * PS[k][0] * ld + max_nI + maxG); };
+    if (need(v) > 227 * 1024) v = 0;
+    BlkVariant r{FN[v], need(v)};
+    if (set_attr) cudaFuncSetAttribute(r.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(r.smem));
+    return r;
+}
+
 // once per context, outside any graph capture
 void prepare_schur_blk(int ld, int band_w, int max_nI, int maxG) {
     if ((band_w + 1 + 31) / 32 <= 4) return;
-    const size_t smem = 128 + sizeof(double) * (size_t(BK_S) * BK_P * ld + max_nI + maxG);
-    cudaFuncSetAttribute(k_schur_blk, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    blk_variant(ld, max_nI, maxG, true);
 }
 
 constexpr int COL_R = 8;
@@ -734,8 +754,8 @@ static void launch_t(const SchurArgs& a, int nstage, size_t smem, cudaStream_t s
 int launch_schur_local(const SchurArgs& a, cudaStream_t st) {
     if (a.nsl == 0) return 0;
     if (a.mode != SCHUR_COLUMNS && (a.band_w + 1 + 31) / 32 > 4 && !getenv("DE_SCHUR_WARP")) {   // wide bands
-        const size_t smem = 128 + sizeof(double) * (size_t(BK_S) * BK_P * a.ld + a.max_nI + a.maxG);
-        k_schur_blk<<<unsigned(a.nsl), BK_T, smem, st>>>(a);
+        const BlkVariant bv = blk_variant(a.ld, a.max_nI, a.maxG, false);
+        bv.fn<<<unsigned(a.nsl), BK_T, bv.smem, st>>>(a);
         return 1;
     }
     if (a.mode == SCHUR_COLUMNS && a.band_w + 1 <= SF_W && a.ld % 2 == 0 && !getenv("DE_FORM_WARP") &&
