@@ -109,7 +109,14 @@ WORKLOADS = {
     "c4": "c4: BASELINE config 4 (3D Q1 hex 96x48x48, 8x4x4 subdomains of 12^3, SIMP p=3) as a sequence step "
           "(density update -> refactor -> warm PCG rtol 1e-10)",
 }
-L2_NOTE = {"c5": "inputs larger than L2 (factor bands 2.15 GB, explicit S_s 0.56 GB per step vs 126 MB L2)",
+WORKLOADS["c2"] = ("c2: BASELINE config 2 (2D Q1 plane stress 256x128, 8x4 subdomains of 32x32, SIMP p=3) as a sequence "
+                   "step (density update -> refactor -> warm PCG rtol 1e-10)")
+WORKLOADS["c3"] = ("c3: BASELINE config 3 (half-MBB 1024x512, 32x16 subdomains, disks of density 1 in 1e-3, FP64-ill-posed: "
+                   "DESIGN.md R15) as a sequence step at a fixed budget of 2000 PCG iterations (no convergence to rtol "
+                   "1e-10 by any FP64 solver; every step ends DE_ENOCONV by construction)")
+L2_NOTE = {"c2": "L2 flushed between steps? no: inputs (33 MB factor) fit L2 -- latency-bound small case, reported for the record",
+           "c3": "inputs larger than L2 (factor bands 0.52 GB, explicit S_s 0.14 GB vs 126 MB L2)",
+           "c5": "inputs larger than L2 (factor bands 2.15 GB, explicit S_s 0.56 GB per step vs 126 MB L2)",
            "c4": "inputs larger than L2 (factor bands 1.92 GB vs 126 MB L2)"}
 
 
@@ -227,8 +234,9 @@ def main():
     d_rhs = torch.tensor(prob.rhs, dtype=torch.float64, device="cuda")
     d_u = torch.empty_like(d_rhs)
 
+    extra = dict(max_iter=2000) if args.config == "c3" else {}   # R15: fixed iteration budget on the ill-posed instance
     solver = B.Solver.from_problem(prob.with_density(sched[0]), device=local, warm_start=1,
-                                   rank=rank, nranks=world, nccl_id=nccl_id, stream=stream.cuda_stream)
+                                   rank=rank, nranks=world, nccl_id=nccl_id, stream=stream.cuda_stream, **extra)
     ctx = solver.ctx
     st0 = solver.stats()
     n_free = st0.n_free

@@ -577,6 +577,51 @@ __device__ __forceinline__ double warp_sum_d(double v) {
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     return v;
 }
+// Inverses of the BLK_D x BLK_D diagonal blocks of every local factor (one warp per block, lane c = column c of the
+// inverse by forward substitution): the blocked sweeps below apply them as small dense products, so no 16-step
+// shuffle chain sits between a panel's arrival and its trailing update.
+__global__ void __launch_bounds__(256) k_blk_diag_inv(const SubDesc* sd, int nsl, const double* __restrict__ band, int ld,
+                                                      double* __restrict__ dinv, int np_max) {
+    const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    const int sl = gwarp / np_max, p = gwarp - sl * np_max;
+    if (sl >= nsl) return;
+    const SubDesc d = sd[sl];
+    const int n = d.nI, j0 = p * BLK_D;
+    double* out = dinv + (size_t(sl) * np_max + p) * BLK_D * BLK_D;
+    if (j0 >= n) return;
+    const int nc = min(BLK_D, n - j0);
+    const double* Lb = band + d.band_off;
+    if (lane >= BLK_D) return;
+    double x[BLK_D];
+    const int c = lane;
+#pragma unroll
+    for (int i = 0; i < BLK_D; ++i) {
+        double v = 0.0;
+        if (c < nc && i < nc) {
+            if (i == c) {
+                v = Lb[size_t(j0 + c) * ld];              // slot 0 holds 1 / L_cc
+            } else if (i > c) {
+                double sacc = 0.0;
+#pragma unroll
+                for (int k = 0; k < BLK_D; ++k)
+                    if (k >= c && k < i) sacc = fma(Lb[size_t(j0 + k) * ld + (i - k)], x[k], sacc);
+                v = -sacc * Lb[size_t(j0 + i) * ld];
+            }
+        } else if (i == c) {
+            v = 1.0;                                       // identity padding of the last block
+        }
+        x[i] = v;
+    }
+#pragma unroll
+    for (int i = 0; i < BLK_D; ++i) out[i * BLK_D + c] = x[i];
+}
+
+void launch_blk_diag_inv(const SubDesc* sd, int nsl, const double* band, int ld, double* dinv, int dinv_np, cudaStream_t st) {
+    const long long warps = (long long)nsl * dinv_np;
+    if (warps <= 0) return;
+    k_blk_diag_inv<<<unsigned((warps + 7) / 8), 256, 0, st>>>(sd, nsl, band, ld, dinv, dinv_np);
+}
+
 constexpr int BK_T = 256;   // threads; BK_P panel columns, BK_S ring stages (template: tuned per band width)
 template <int BK_P, int BK_S>
 __global__ void __launch_bounds__(BK_T, 1) k_schur_blk(SchurArgs a) {
@@ -588,7 +633,10 @@ __global__ void __launch_bounds__(BK_T, 1) k_schur_blk(SchurArgs a) {
     const int mode = a.mode;
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
     double* pan = reinterpret_cast<double*>(smem + 128);   // [BK_S][BK_P][ld]
-    double* v = pan + BK_S * BK_P * ld;                    // [n]: rhs, then y, then x
+    double* dblk = pan + BK_S * BK_P * ld;                 // [BK_S][BLK_D][BLK_D] inverse diagonal blocks (use_dinv)
+    double* v = dblk + BK_S * BLK_D * BLK_D;               // [n]: rhs, then y, then x
+    const bool use_dinv = BK_P == BLK_D && a.dinv != nullptr;
+    const double* dsrc = use_dinv ? a.dinv + size_t(blockIdx.x) * a.dinv_np * BLK_D * BLK_D : nullptr;
     double* xl = v + a.max_nI;                             // [nG]
     const double* Lb = a.band + d.band_off;
     const int np = (n + BK_P - 1) / BK_P;
@@ -596,8 +644,11 @@ __global__ void __launch_bounds__(BK_T, 1) k_schur_blk(SchurArgs a) {
     auto issue = [&](int q) {
         const int p = panel_of(q), c0 = p * BK_P, nc = min(BK_P, n - c0);
         const uint32_t bytes = uint32_t(nc) * uint32_t(ld) * 8u;
-        mbar_expect_tx(bar + (q % BK_S), bytes);
+        const uint32_t dbytes = use_dinv ? uint32_t(BLK_D * BLK_D * 8) : 0u;
+        mbar_expect_tx(bar + (q % BK_S), bytes + dbytes);
         tma_load_1d(pan + size_t(q % BK_S) * BK_P * ld, Lb + size_t(c0) * ld, bytes, bar + (q % BK_S));
+        if (use_dinv)
+            tma_load_1d(dblk + size_t(q % BK_S) * BLK_D * BLK_D, dsrc + size_t(p) * BLK_D * BLK_D, dbytes, bar + (q % BK_S));
     };
     if (tid == 0) {
         for (int i = 0; i < BK_S; ++i) mbar_init(bar + i, 1);
@@ -624,7 +675,17 @@ __global__ void __launch_bounds__(BK_T, 1) k_schur_blk(SchurArgs a) {
         const double* P = pan + size_t(q % BK_S) * BK_P * ld;
         const int p = panel_of(q), j0 = p * BK_P, nc = min(BK_P, n - j0);
         if (q < np) {   // forward: diagonal block, then the rows below
-            if (wid == 0) {   // unrolled: every coefficient load is off the shuffle-FMA chain
+            if (wid == 0 && use_dinv) {   // y_blk = L_jj^-1 v_blk: 16 independent row products, no chain
+                const double* D = dblk + size_t(q % BK_S) * BLK_D * BLK_D;
+                double acc = 0.0;
+                if (lane < nc) {
+#pragma unroll
+                    for (int jj = 0; jj < BLK_D; ++jj)
+                        if (jj <= lane) acc = fma(D[lane * BLK_D + jj], v[j0 + jj], acc);
+                }
+                __syncwarp();
+                if (lane < nc) v[j0 + lane] = acc;
+            } else if (wid == 0) {   // unrolled: every coefficient load is off the shuffle-FMA chain
                 double vr = lane < nc ? v[j0 + lane] : 0.0;
                 double cf[BK_P], dg[BK_P];
 #pragma unroll
@@ -659,7 +720,17 @@ __global__ void __launch_bounds__(BK_T, 1) k_schur_blk(SchurArgs a) {
                 if (lane == 0) v[j] -= acc;
             }
             __syncthreads();
-            if (wid == 0) {
+            if (wid == 0 && use_dinv) {   // x_blk = L_jj^-T t_blk
+                const double* D = dblk + size_t(q % BK_S) * BLK_D * BLK_D;
+                double acc = 0.0;
+                if (lane < nc) {
+#pragma unroll
+                    for (int jj = 0; jj < BLK_D; ++jj)
+                        if (jj >= lane && jj < nc) acc = fma(D[jj * BLK_D + lane], v[j0 + jj], acc);
+                }
+                __syncwarp();
+                if (lane < nc) v[j0 + lane] = acc;
+            } else if (wid == 0) {
                 double tr = lane < nc ? v[j0 + lane] : 0.0;
                 double cf[BK_P], dg[BK_P];
 #pragma unroll
@@ -697,9 +768,9 @@ __global__ void __launch_bounds__(BK_T, 1) k_schur_blk(SchurArgs a) {
     }
 }
 
-// panel width / ring depth of k_schur_blk: the deepest ring of the narrowest panels that fits shared memory keeps the
-// most bulk copies in flight (measured on c4, ld = 474; env DE_BLK_VARIANT overrides: 0 = 16 x 2, 1 = 8 x 4, 2 = 12 x 3,
-// 3 = 8 x 5, 4 = 4 x 8)
+// panel width / ring depth of k_schur_blk (env DE_BLK_VARIANT: 0 = 16 x 2 (default), 1 = 8 x 4, 2 = 12 x 3, 3 = 8 x 5,
+// 4 = 4 x 8). Measured on c4 (ld = 474): 1.33 / 1.54 / 1.54 / 1.64 / 2.31 ms per apply -- the time is ~0.6 us of fixed
+// per-panel work (diagonal-block chain, barriers) plus ~0.09 us per column of streaming, so narrower panels lose.
 typedef void (*blk_fn)(SchurArgs);
 struct BlkVariant {
     blk_fn fn;
@@ -708,9 +779,9 @@ struct BlkVariant {
 static BlkVariant blk_variant(int ld, int max_nI, int maxG, bool set_attr) {
     static const int PS[5][2] = {{16, 2}, {8, 4}, {12, 3}, {8, 5}, {4, 8}};
     static const blk_fn FN[5] = {k_schur_blk<16, 2>, k_schur_blk<8, 4>, k_schur_blk<12, 3>, k_schur_blk<8, 5>, k_schur_blk<4, 8>};
-    int v = 1;
+    int v = 0;
     if (const char* e = getenv("DE_BLK_VARIANT")) v = std::max(0, std::min(4, atoi(e)));
-    auto need = [&](int k) { return 128 + sizeof(double) * (size_t(PS[k][1]) * PS[k][0] * ld + max_nI + maxG); };
+    auto need = [&](int k) { return 128 + sizeof(double) * (size_t(PS[k][1]) * (PS[k][0] * ld + BLK_D * BLK_D) + max_nI + maxG); };
     if (need(v) > 227 * 1024) v = 0;
     BlkVariant r{FN[v], need(v)};
     if (set_attr) cudaFuncSetAttribute(r.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(r.smem));

@@ -50,19 +50,30 @@ def full(rep, out_md, title, algo_bytes=None):
 
 
 if __name__ == '__main__':
-    bench = json.loads(open('gpurun_out/bench.json').read().strip().splitlines()[-1])
+    import os
+    rnd = sys.argv[1] if len(sys.argv) > 1 else 'round2'
+    go = 'gpurun_out'
+    bench = json.loads(open(f'{go}/bench_c5.json').read().strip().splitlines()[-1])
     algo = {bench['roofline']['kernel'].split()[0]: bench['roofline']['algorithmic_bytes_per_launch'],
             bench['roofline_secondary']['kernel'].split()[0]: bench['roofline_secondary']['algorithmic_bytes_per_launch']}
-    launches('gpurun_out/launches_bench.csv', 'profiles/round1_launches_bench_c5.md',
-             'Round 1 launch list: `bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline` (config c5)')
+    launches(f'{go}/launches_bench_c5.csv', f'profiles/{rnd}_launches_bench_c5.md',
+             f'{rnd} launch list: `bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline` (config c5)')
+    if os.path.exists(f'{go}/launches_bench_c4.csv') and os.path.getsize(f'{go}/launches_bench_c4.csv') > 1000:
+        launches(f'{go}/launches_bench_c4.csv', f'profiles/{rnd}_launches_bench_c4.md',
+                 f'{rnd} launch list: `bench.py --config c4 --steps 1 --warmup 2 --no-e2e --no-cpu-baseline` (config c4)')
     tr = {}
-    tr['k_prec_coop'] = full('gpurun_out/prec_coop.ncu-rep', 'profiles/round1_prec_coop_c5.md',
-                             'Round 1: k_prec_coop (C5 preconditioner, one cooperative launch), config c5',
-                             algo_bytes=algo['k_prec_coop'])
-    tr['k_schur_explicit'] = full('gpurun_out/schur_explicit.ncu-rep', 'profiles/round1_schur_explicit_c5.md',
-                                  'Round 1: k_schur_explicit (C2 explicit local Schur apply), config c5',
-                                  algo_bytes=algo['k_schur_explicit'])
+    tr['k_prec_coop'] = full(f'{go}/r2_k_prec_coop.ncu-rep', f'profiles/{rnd}_prec_coop_c5.md',
+                             f'{rnd}: k_prec_coop (C5 preconditioner, one cooperative launch), config c5',
+                             algo_bytes=algo.get('k_prec_coop'))
+    tr['k_schur_explicit'] = full(f'{go}/r2_k_schur_explicit.ncu-rep', f'profiles/{rnd}_schur_explicit_c5.md',
+                                  f'{rnd}: k_schur_explicit (C2 explicit local Schur apply), config c5',
+                                  algo_bytes=algo.get('k_schur_explicit'))
     json.dump({"config": "c5", "n_gpus": 1, "dram_bytes_per_launch": tr,
-               "source": ["profiles/round1_prec_coop_c5.md", "profiles/round1_schur_explicit_c5.md"]},
+               "source": [f"profiles/{rnd}_prec_coop_c5.md", f"profiles/{rnd}_schur_explicit_c5.md"]},
               open('profiles/traffic.json', 'w'), indent=1)
     print('traffic', tr)
+    for k in ('k_prec_coop', 'k_schur_blk', 'k_band_chol_panel'):
+        rep = f'{go}/r2_c4_{k}.ncu-rep'
+        if os.path.exists(rep):
+            t = full(rep, f'profiles/{rnd}_c4_{k}.md', f'{rnd}: {k}, config c4 (3D)')
+            print(k, 'c4 traffic', t)
