@@ -74,6 +74,7 @@ using namespace de;
 // Loopback group (include/de.h de_loopback_create): host barrier + device slots [n][cap]
 struct de_loopback {
     int n = 1;
+    std::mutex coop_mu;   // one cooperative kernel of the group on the device at a time (see precond())
     std::mutex m;
     std::condition_variable cv;
     int count = 0;
@@ -81,16 +82,20 @@ struct de_loopback {
     double* slots = nullptr;
     size_t cap = 0;
     int device = 0;
-    void barrier() {
+    // false: the other ranks did not arrive within 60 s (one of them left the collective with an error): the caller
+    // fails instead of blocking forever
+    bool barrier() {
         std::unique_lock<std::mutex> lk(m);
         const long g = gen;
         if (++count == n) {
             count = 0;
             ++gen;
             cv.notify_all();
-        } else {
-            cv.wait(lk, [&] { return gen != g; });
+            return true;
         }
+        if (cv.wait_for(lk, std::chrono::seconds(60), [&] { return gen != g; })) return true;
+        --count;
+        return false;
     }
 };
 
@@ -217,10 +222,16 @@ de_status_t allreduce(de_ctx* c, double* buf, size_t n) {
         DE_CUDA(cudaMemcpyAsync(g->slots + size_t(c->rank) * g->cap, buf, n * sizeof(double),
                                 cudaMemcpyDeviceToDevice, c->st));
         DE_CUDA(cudaStreamSynchronize(c->st));
-        g->barrier();
+        if (!g->barrier()) {
+            set_error("loopback exchange timed out: another rank left the collective");
+            return DE_ENCCL;
+        }
         launch_sum_slots(buf, g->slots, g->n, g->cap, int64_t(n), c->st);
         DE_CUDA(cudaStreamSynchronize(c->st));
-        g->barrier();
+        if (!g->barrier()) {
+            set_error("loopback exchange timed out: another rank left the collective");
+            return DE_ENCCL;
+        }
         return check_launch();
     }
     int r = nccl().allreduce(buf, buf, n, 8 /*ncclFloat64*/, 0 /*ncclSum*/, c->comm, c->st);
@@ -277,10 +288,17 @@ de_status_t schur_apply(de_ctx* c, const double* x, double* q) {
 
 de_status_t precond(de_ctx* c, const double* r, double* z, const PcgState* s, int* nl, bool literal = false) {
     if (c->have_prec && c->use_coop) {
+        // Loopback group: the ranks' host threads would launch whole-device cooperative kernels concurrently on their
+        // own streams; two such grids can each become partially resident and wait in their grid barriers for blocks
+        // the other one keeps off the SMs (observed: an intermittent hang of the 8-rank loopback test). One rank's
+        // application at a time, held until it has finished (test path only; real ranks own their device).
+        std::unique_lock<std::mutex> lk;
+        if (c->lb) lk = std::unique_lock<std::mutex>(c->lb->coop_mu);
         if (prec_apply_coop(c->P, c->coop, r, z, s, c->st, literal) < 0) {
             set_error("cooperative preconditioner launch failed: %s", cudaGetErrorString(cudaGetLastError()));
             return DE_ECUDA;
         }
+        if (c->lb) DE_CUDA(cudaStreamSynchronize(c->st));
         if (nl) *nl = 3;   // k_prec_coop, k_prec_ritz, k_prec_combine
     } else if (c->have_prec) {
         prec_apply(c->P, r, z, s, c->st, nl);

@@ -4,6 +4,8 @@
 #pragma once
 
 #include <cstdint>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 #include <cuda_runtime.h>
@@ -16,6 +18,22 @@ constexpr int KMAX = 16;            // max inverse-Lanczos basis size supported 
 constexpr int MAXC = 3;             // max displacement components
 
 void set_error(const char* fmt, ...);
+
+// Raise (never lower) a kernel's dynamic shared-memory limit. The limit is one value per kernel for the whole process,
+// while the size a launch needs depends on the context (a rank's largest subdomain, its ring entries): two contexts
+// driven from different host threads that each SET their own size could lower the limit between another thread's
+// set and its launch ("invalid argument"; seen as an intermittent hang of the 8-rank loopback test, whose other
+// ranks then waited for the failed ones in an exchange).
+inline void raise_dyn_smem(const void* fn, size_t bytes) {
+    static std::mutex mu;
+    static std::map<const void*, size_t> cur;
+    std::lock_guard<std::mutex> lk(mu);
+    size_t& c = cur[fn];
+    if (bytes > c) {
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+        c = bytes;
+    }
+}
 
 #define DE_CUDA(call)                                                                   \
     do {                                                                                \

@@ -178,7 +178,7 @@ int launch_band_cholesky(const SubDesc* sd, int nsl, double* band, int ld, int b
                          cudaStream_t st) {
     if (nsl == 0) return 0;
     const size_t smem = size_t(NBP) * ld * sizeof(double);
-    cudaFuncSetAttribute(k_band_chol_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    raise_dyn_smem(reinterpret_cast<const void*>(k_band_chol_panel), smem);
     k_band_chol_panel<<<nsl, 512, smem, st>>>(sd, band, ld, band_w, d_fail);
     return 1;
 }

@@ -2011,7 +2011,7 @@ bool prec_coop_prepare(const PrecDev& P, int device, CoopBuffers& B) {
     const bool tim = getenv("DE_PREC_TIMERS") != nullptr;
     coop_fn kfn = P.kmax <= 10 ? (tim ? k_prec_coop<10, true> : k_prec_coop<10, false>) : k_prec_coop<KMAX, false>;
     if (tim && P.kmax > 10) kfn = k_prec_coop<KMAX, true>;
-    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    raise_dyn_smem(reinterpret_cast<const void*>(kfn), smem);
     int per_sm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, CT, smem) != cudaSuccess || per_sm < 1)
         return false;

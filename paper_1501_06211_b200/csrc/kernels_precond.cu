@@ -401,7 +401,7 @@ int fpcg_prepare(PrecDev& P, int device) {
     const int mf = std::max(1, P.eK.maxface & 0xffff);
     const size_t smem = size_t(FP_T / 32) * (4 * mf * sizeof(double) + mf * sizeof(int));
     if (smem > 200 * 1024) return 0;
-    if (smem > 48 * 1024) cudaFuncSetAttribute(k_face_pcg, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (smem > 48 * 1024) raise_dyn_smem(reinterpret_cast<const void*>(k_face_pcg), smem);
     int per_sm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_face_pcg, FP_T, smem) != cudaSuccess || per_sm < 1)
         return 0;
@@ -844,7 +844,7 @@ void prec_prepare(const PrecDev& P) {
         const int per_warp = 3 * (E->maxface & 0xffff) + (E->maxface >> 16);
         mx = std::max(mx, face_warps_per_block(per_warp) * per_warp * 8);
     }
-    if (mx > 48 * 1024) cudaFuncSetAttribute(k_face_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    if (mx > 48 * 1024) raise_dyn_smem(reinterpret_cast<const void*>(k_face_solve), size_t(mx));
 }
 
 // ------------------------------------------------------------------ Gauss-Jordan SPD inverse (setup)

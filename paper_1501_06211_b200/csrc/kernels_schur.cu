@@ -292,8 +292,7 @@ void launch_schur_explicit(const SubDesc* sd, int nsl, const double* sexp, const
 // once per context, outside any graph capture
 void prepare_schur_explicit(int maxG) {
     const int np = (maxG + STS - 1) / STS * STS;
-    cudaFuncSetAttribute(k_schur_explicit, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(size_t(1 + SE_W) * np * sizeof(double)));
+    raise_dyn_smem(reinterpret_cast<const void*>(k_schur_explicit), size_t(1 + SE_W) * np * sizeof(double));
 }
 
 // ------------------------------------------------------------------ explicit S_s formation, R columns per warp
@@ -784,7 +783,7 @@ static BlkVariant blk_variant(int ld, int max_nI, int maxG, bool set_attr) {
     auto need = [&](int k) { return 128 + sizeof(double) * (size_t(PS[k][1]) * (PS[k][0] * ld + BLK_D * BLK_D) + max_nI + maxG); };
     if (need(v) > 227 * 1024) v = 0;
     BlkVariant r{FN[v], need(v)};
-    if (set_attr) cudaFuncSetAttribute(r.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(r.smem));
+    if (set_attr) raise_dyn_smem(reinterpret_cast<const void*>(r.fn), r.smem);
     return r;
 }
 
@@ -798,7 +797,7 @@ constexpr int COL_R = 8;
 
 template <int G, int NS>
 static void launch_cols(const SchurArgs& a, int nstage, size_t smem, cudaStream_t st) {
-    cudaFuncSetAttribute(k_schur_cols<G, NS, COL_R>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    raise_dyn_smem(reinterpret_cast<const void*>(k_schur_cols<G, NS, COL_R>), smem);
     const unsigned wps = unsigned((a.maxG + COL_R - 1) / COL_R);
     k_schur_cols<G, NS, COL_R><<<unsigned(a.nsl) * wps, 32, smem, st>>>(a, nstage);
 }
@@ -814,7 +813,7 @@ static void launch_t(const SchurArgs& a, int nstage, size_t smem, cudaStream_t s
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     cudaStreamIsCapturing(st, &cs);
     if (cs == cudaStreamCaptureStatusNone) {
-        cudaFuncSetAttribute(k_schur_local<G, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        raise_dyn_smem(reinterpret_cast<const void*>(k_schur_local<G, NS>), smem);
         cudaFuncSetAttribute(k_schur_local<G, NS>, cudaFuncAttributePreferredSharedMemoryCarveout,
                              cudaSharedmemCarveoutMaxShared);
     }
@@ -832,7 +831,7 @@ int launch_schur_local(const SchurArgs& a, cudaStream_t st) {
     if (a.mode == SCHUR_COLUMNS && a.band_w + 1 <= SF_W && a.ld % 2 == 0 && !getenv("DE_FORM_WARP") &&
         size_t(2) * SF_CB * a.ld * 8 + size_t(a.max_ig) * 12 + size_t(a.max_nI + 1) * 4 <= 200 * 1024) {
         const size_t smem = size_t(2) * SF_CB * a.ld * sizeof(double) + size_t(a.max_ig) * 12 + size_t(a.max_nI + 1) * 4;
-        cudaFuncSetAttribute(k_schur_form, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        raise_dyn_smem(reinterpret_cast<const void*>(k_schur_form), smem);
         k_schur_form<<<unsigned(a.nsl), SF_T, smem, st>>>(a);
         return 1;
     }

@@ -35,11 +35,17 @@ def _run_ranks(p, G, fn, **opts):
         except Exception as ex:   # noqa: BLE001 - reported below
             err[r] = ex
 
-    th = [threading.Thread(target=work, args=(r,)) for r in range(G)]
+    th = [threading.Thread(target=work, args=(r,), daemon=True) for r in range(G)]
     for t in th:
         t.start()
     for t in th:
-        t.join(timeout=600)
+        t.join(timeout=120)
+    if any(t.is_alive() for t in th):   # a rank is stuck: show where, and do not touch the contexts it is using
+        import faulthandler
+        import sys
+        faulthandler.dump_traceback(file=sys.stderr, all_threads=True)
+        pytest.fail(f"loopback ranks still running after 120 s: {[r for r, t in enumerate(th) if t.is_alive()]}; "
+                    f"errors so far {err}")
     for s in solvers:
         if s is not None:
             s.close()
