@@ -1774,6 +1774,7 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
         // the Rayleigh-Ritz Gram matrices before normalisation: w2.(L W_t), w2.(M W_t) (t < j), w2.L w2,
         // w2.M w2, w2.r
         if (dbg) a.timers[110] = gtimer();
+        if (TIM && a.timers && j == 5 && tid == 32 && fold) a.timers[200 + 4096 + 1024 + blockIdx.x] = gtimer();   // C start
         ZERO_VALS();
         gram_zero(gacc);
         if (part)
@@ -1822,6 +1823,12 @@ __global__ void __launch_bounds__(CT, 2) k_prec_coop(CoopArgs a) {
         if (part) gram_partials(a, gacc, c, lb, j);
         block_partials(a, vals, fold ? 2 : 1, pp, c, lb, sred);
         if (dbg) a.timers[112] = gtimer();
+        if (TIM && a.timers && j == 5 && tid == 32 && fold) {   // per-block arrival at the phase-C barrier (tools/prec_timers.py)
+            a.timers[200 + 4096 + 1536 + blockIdx.x] = gtimer();
+            unsigned sm;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+            a.timers[200 + 4096 + 2048 + blockIdx.x] = sm;
+        }
         grid.sync();
     __syncwarp();   // lane 0 spun in the barrier: reconverge before warp-synchronous code
     STAMP(stamp++);

@@ -41,7 +41,7 @@ slow = np.argsort(-f1all)[:12]
 print("slowest mode1 warps (gw, cycles, block, warp):", [(int(g), int(f1all[g]), int(g) // 8, int(g) % 8) for g in slow])
 f0all = np.array(list(t)[200:200 + 2368], dtype=np.float64)
 print("their mode0 cycles:", [int(f0all[g]) for g in slow])
-# phase A (Lanczos step 5) per block: start (after the E2 barrier) and arrival at the A barrier (globaltimer ns)
+# consumer phase (Lanczos step 5; phase C with the fold, else phase A) per block: start and arrival at its barrier (globaltimer ns)
 st = np.array(list(t)[200 + 4096 + 1024:200 + 4096 + 1024 + 512], dtype=np.float64)
 ar = np.array(list(t)[200 + 4096 + 1536:200 + 4096 + 1536 + 512], dtype=np.float64)
 nbk = int((st > 0).sum())
