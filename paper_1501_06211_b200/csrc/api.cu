@@ -728,6 +728,46 @@ de_status_t upload_prec_impl(de_ctx* c) {
                     }
                     pid[i] = it->second;
                 }
+                // cross-point rows: own value x_C[k] plus up to XELL_W - 1 face-end neighbours, each with its own
+                // couplings, in one ELL (two load levels instead of the CSR walk's four); pat_id = -2 - cross index
+                D.xell_col = nullptr;
+                if (ok && !pats.empty() && E.ncross > 0 && !getenv("DE_NO_XELL")) {
+                    const size_t nx = size_t(E.ncross);
+                    std::vector<int32_t> xc(XELL_W * nx, 0), x0(XELL_W * nx, 0), x1(XELL_W * nx, 0);
+                    std::vector<double> xv0(XELL_W * nx, 0.0), xv1(XELL_W * nx, 0.0), xm(XELL_W * nx, 0.0), xl(XELL_W * nx, 0.0);
+                    bool xok = true;
+                    for (int ci = 0; ci < E.ncross && xok; ++ci) {
+                        const int i = E.cross_flat[ci];
+                        const int e0 = Mh.ptr[i], e1 = Mh.ptr[i + 1];
+                        if (e1 - e0 > XELL_W) {
+                            xok = false;
+                            break;
+                        }
+                        for (int k = 0; k < XELL_W; ++k) {
+                            const size_t at = size_t(k) * nx + ci;
+                            const int e = e0 + k;
+                            const int col = e < e1 ? Mh.col[e] : i;
+                            if (e < e1 && Lh.col[e] != col) xok = false;
+                            xc[at] = col;
+                            x0[at] = gc0[col];
+                            x1[at] = gc1[col];
+                            xv0[at] = gv0[col];
+                            xv1[at] = gv1[col];
+                            xm[at] = e < e1 ? Mh.val[e] : 0.0;
+                            xl[at] = e < e1 ? Lh.val[e] : 0.0;
+                        }
+                    }
+                    if (xok) {
+                        for (int ci = 0; ci < E.ncross; ++ci) pid[E.cross_flat[ci]] = -2 - ci;
+                        TRY(dupload(c, &D.xell_col, xc));
+                        TRY(dupload(c, &D.xell_c0, x0));
+                        TRY(dupload(c, &D.xell_c1, x1));
+                        TRY(dupload(c, &D.xell_v0, xv0));
+                        TRY(dupload(c, &D.xell_v1, xv1));
+                        TRY(dupload(c, &D.xell_m, xm));
+                        TRY(dupload(c, &D.xell_l, xl));
+                    }
+                }
                 if (ok && !pats.empty()) {
                     TRY(dupload(c, &D.pat_id, pid));
                     TRY(dupload(c, &D.pat_code, codes));

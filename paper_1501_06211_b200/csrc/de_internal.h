@@ -257,10 +257,15 @@ struct ElimDev {
     // row's neighbour values come from flat i-1, i, i+1 and the face's two x_C with row i's own couplings
     int32_t *pat_id, *pat_code;
     double *pat_m, *pat_l;
+    // cross-point rows of the consumer (pat_id = -2 - cross index): ELL of width XELL_W over [XELL_W][ncross], every
+    // entry with its column's couplings (as the fold ELL); null = CSR walk
+    int32_t *xell_col, *xell_c0, *xell_c1;
+    double *xell_v0, *xell_v1, *xell_m, *xell_l;
     int32_t *fell_c0, *fell_c1;
     double *fell_v0, *fell_v1, *fell_m, *fell_l;
 };
 constexpr int FELL_W = 3;
+constexpr int XELL_W = 5;            // a 2D cross point: itself + four face-end neighbours
 constexpr int PCR_L = 5;             // log2(32) reduction levels
 constexpr int PCR_Q = 2 * PCR_L + 1;
 constexpr int XCF_W = 4;

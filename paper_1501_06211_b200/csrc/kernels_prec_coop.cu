@@ -294,6 +294,33 @@ __device__ __forceinline__ double spmv_elim_pat(const CsrDev& M, const CsrDev& L
     const double ym = y[im], y0 = y[i], yp = y[ip];
     const double am0 = E.g_v0[im], a00 = E.g_v0[i], ap0 = E.g_v0[ip];
     const double am1 = E.g_v1[im], a01 = E.g_v1[i], ap1 = E.g_v1[ip];
+    if (pid <= -2 && E.xell_col) {   // cross-point row: its ELL (entry data in one level, then y / x_C of each neighbour)
+        const int ci = -2 - pid;
+        int col[XELL_W], g0[XELL_W], g1[XELL_W];
+        double v0[XELL_W], v1[XELL_W], mv[XELL_W], lv[XELL_W];
+#pragma unroll
+        for (int k = 0; k < XELL_W; ++k) {
+            const size_t at = size_t(k) * E.ncross + ci;
+            col[k] = E.xell_col[at];
+            g0[k] = E.xell_c0[at];
+            g1[k] = E.xell_c1[at];
+            v0[k] = E.xell_v0[at];
+            v1[k] = E.xell_v1[at];
+            mv[k] = E.xell_m[at];
+            lv[k] = E.xell_l[at];
+        }
+        double am = 0.0, al = 0.0, xi = 0.0;
+#pragma unroll
+        for (int k = 0; k < XELL_W; ++k) {
+            const double x = y[col[k]] - v0[k] * xC[g0[k]] - v1[k] * xC[g1[k]];
+            am += mv[k] * x;
+            al += lv[k] * x;
+            if (col[k] == i) xi = x;   // padding repeats column i with zero coefficients: the same value
+        }
+        yM = am;
+        yL = al;
+        return xi;
+    }
     if (pid < 0)
         return E.fell_col ? spmv_elim_fell(M, L, i, E, y, xC, nfl, yM, yL) : spmv_elim(M, L, i, E, y, xC, yM, yL);
     const double xa = xC[c0], xb = xC[c1];
