@@ -13,6 +13,8 @@
 //     Storage: column band, ld = b+1 rounded to even, slot 0 = 1/L_jj (the solves multiply).
 #include "de_internal.h"
 
+#include <cstdlib>
+
 namespace de {
 
 __constant__ double c_KE[24 * 24];
@@ -119,6 +121,11 @@ void launch_assemble_pairs(const MeshDev& m, const int32_t* da, const int32_t* d
 // 32-column panels factored in shared memory; trailing update in global memory (2D and 3D; measured on c5:
 // 16 ms against 39 ms for a column-at-a-time shared-memory window).
 constexpr int NBP = 32;
+// TU: trailing update 0 = one thread per entry (two shared loads per DFMA), 1 = FP64 tensor cores: every warp forms
+// 8 x 8 tiles of the rank-32 update W[r][c] = sum_k L[r][k] L[c][k] with mma.sync.m8n8k4.f64 (row fragments of the
+// panel for A, the same panel's column fragments for B: one shared load per operand element, 8 FMAs per lane per
+// load pair), masked to the band, and subtracts them from the band in global memory.
+template <int TU>
 __global__ void __launch_bounds__(512) k_band_chol_panel(const SubDesc* __restrict__ sd, double* __restrict__ band,
                                                          int ld, int bw, int* __restrict__ fail) {
     extern __shared__ double P[];   // NBP * ld
@@ -149,14 +156,66 @@ __global__ void __launch_bounds__(512) k_band_chol_panel(const SubDesc* __restri
             }
             __syncthreads();
         }
-        for (int i = tid; i < nb * ld; i += nt) {
-            base[int64_t(j0) * ld + i] = P[i];
-            const int jj = i / ld, k = i - jj * ld, j = j0 + jj;
-            if (k <= bw && j + k < n) Mb[int64_t(n - 1 - j - k) * ld + k] = P[i];   // M = P L^T P
+        for (int i = tid; i < nb * ld; i += nt) base[int64_t(j0) * ld + i] = P[i];
+        // M = P L^T P: row r of L is column n-1-r of M (entry L[r][j] at slot k = r - j). Written row-wise: the nb
+        // entries of row r that lie in this panel are nb CONSECUTIVE slots of one M column (consecutive threads ->
+        // consecutive addresses; the shared reads stride ld - 1, odd: no bank conflicts). The former per-entry write
+        // (consecutive k -> stride ld - 1 in M) made the 3D factorisation move 34.7 GB of DRAM traffic for a 1.9 GB
+        // factor (ncu, profiles/round2_c4_k_band_chol_panel.md).
+        for (int idx = tid; idx < (bw + nb) * nb; idx += nt) {
+            const int rr = idx / nb, jj = nb - 1 - (idx - rr * nb), r = j0 + rr, k = rr - jj;
+            if (k >= 0 && k <= bw && r < n) Mb[int64_t(n - 1 - r) * ld + k] = P[jj * ld + k];
         }
         // trailing update of columns c in [j0+nb, j0+nb-1+bw], rows r = c + rr (rr in [0,bw])
         const int c_lo = j0 + nb, c_hi = min(j0 + nb - 1 + bw, n - 1);
         const int ncol = c_hi - c_lo + 1;
+        if constexpr (TU == 1) {
+            const int lane = tid & 31, wid = tid >> 5, nwarp = nt >> 5;
+            const int ntc = (ncol + 7) / 8, ntr = (bw + 8 + 7) / 8 + 1;   // column tiles; row tiles per column tile
+            const int ai = lane >> 2, ak = lane & 3;                      // A: row ai, k ak; B: k ak, column ai
+            // TG tiles per warp in flight: the old band values are loaded first (the global read-modify-write latency
+            // of one tile at a time was the whole cost of this loop: measured, the tensor-core update alone changed
+            // nothing), accumulated into with the negated A fragments, and stored
+            constexpr int TG = 4;
+            for (int t0 = wid * TG; t0 < ntc * ntr; t0 += nwarp * TG) {
+                int C0[TG], R0[TG];
+                bool live[TG];
+                double d0[TG], d1[TG];
+#pragma unroll
+                for (int g = 0; g < TG; ++g) {
+                    const int t = t0 + g, tc = t / ntr, tr = t - tc * ntr;
+                    C0[g] = c_lo + 8 * tc;
+                    R0[g] = C0[g] + 8 * tr;               // tile rows start at the tile's first column
+                    live[g] = t < ntc * ntr && R0[g] <= min(C0[g] + 7, c_hi) + bw && R0[g] < n;   // warp-uniform
+                    const int r = R0[g] + ai, c = C0[g] + 2 * ak;
+                    const bool w0 = live[g] && c <= c_hi && r >= c && r - c <= bw && r < n;
+                    const bool w1 = live[g] && c + 1 <= c_hi && r >= c + 1 && r - c - 1 <= bw && r < n;
+                    d0[g] = w0 ? base[int64_t(c) * ld + (r - c)] : 0.0;
+                    d1[g] = w1 ? base[int64_t(c + 1) * ld + (r - c - 1)] : 0.0;
+                }
+#pragma unroll
+                for (int g = 0; g < TG; ++g) {   // (k outer / g inner, interleaving the TG chains, measured slower: 67.3 vs 57.9 ms)
+                    if (!live[g]) continue;      // warp-uniform
+                    const int ra = R0[g] + ai, cb = C0[g] + ai;
+#pragma unroll
+                    for (int k0 = 0; k0 < NBP; k0 += 4) {
+                        const int kk = k0 + ak, kcol = j0 + kk;
+                        const int oa = ra - kcol, ob = cb - kcol;
+                        const double av = (kk < nb && ra < n && oa <= bw) ? -P[kk * ld + oa] : 0.0;
+                        const double bv = (kk < nb && cb <= c_hi && ob <= bw) ? P[kk * ld + ob] : 0.0;
+                        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                                     : "+d"(d0[g]), "+d"(d1[g])
+                                     : "d"(av), "d"(bv));
+                    }
+                }
+#pragma unroll
+                for (int g = 0; g < TG; ++g) {
+                    const int r = R0[g] + ai, c = C0[g] + 2 * ak;
+                    if (live[g] && c <= c_hi && r >= c && r - c <= bw && r < n) base[int64_t(c) * ld + (r - c)] = d0[g];
+                    if (live[g] && c + 1 <= c_hi && r >= c + 1 && r - c - 1 <= bw && r < n) base[int64_t(c + 1) * ld + (r - c - 1)] = d1[g];
+                }
+            }
+        } else
         for (int t = tid; t < ncol * (bw + 1); t += nt) {
             const int c = c_lo + t / (bw + 1), rr = t % (bw + 1);
             const int r = c + rr;
@@ -178,8 +237,13 @@ int launch_band_cholesky(const SubDesc* sd, int nsl, double* band, int ld, int b
                          cudaStream_t st) {
     if (nsl == 0) return 0;
     const size_t smem = size_t(NBP) * ld * sizeof(double);
-    raise_dyn_smem(reinterpret_cast<const void*>(k_band_chol_panel), smem);
-    k_band_chol_panel<<<nsl, 512, smem, st>>>(sd, band, ld, band_w, d_fail);
+    // trailing update on the FP64 tensor cores (default; env DE_CHOL_SCALAR = the one-thread-per-entry update)
+    // wide bands (3D) only: c4 77.7 -> 57.9 ms; on the 2D bands (b = 67: 99 tiles per panel, mostly masked) it measured
+    // slower (c5 60.7 -> 70.3 ms); DE_CHOL_DMMA / DE_CHOL_SCALAR force either
+    const bool dmma = getenv("DE_CHOL_SCALAR") ? false : (getenv("DE_CHOL_DMMA") ? true : band_w > 127);
+    void (*fn)(const SubDesc*, double*, int, int, int*) = dmma ? k_band_chol_panel<1> : k_band_chol_panel<0>;
+    raise_dyn_smem(reinterpret_cast<const void*>(fn), smem);
+    fn<<<nsl, 512, smem, st>>>(sd, band, ld, band_w, d_fail);
     return 1;
 }
 

@@ -497,6 +497,8 @@ __device__ __forceinline__ void sf_sweep(const double* __restrict__ F, int n, in
                     b = rhs(r);
                 }
                 double acc[4] = {0.0, 0.0, 0.0, 0.0};
+                // (16-byte coefficient loads -- double2 or explicit ld.shared.v2.f64, 544 LDS.128 instead of 1208 LDS.64
+                // in the SASS -- measured SLOWER on c5: refactorisation 60.7 -> 86.7 / 90.2 ms)
 #pragma unroll
                 for (int k = SF_W - 1; k >= 1; --k)   // oldest rows first: the newest terms close the row
                     if (k <= B) acc[k & 3] = fma(-col[k], k <= q ? nz[q - k] : z[k - q - 1], acc[k & 3]);
