@@ -534,6 +534,12 @@ de_status_t upload_prec_impl(de_ctx* c) {
             const int nc = E.cross_comp_off[cc + 1] - E.cross_comp_off[cc];
             if (nc > 0) launch_gauss_jordan(D.Sinv + E.sc_off[cc], gjbuf, nc, c->st);
         }
+        D.fb_off = nullptr;   // 3D: block-bidiagonal face factors (HElim::fb)
+        D.fb = nullptr;
+        if (!E.fb.empty() && int(E.fb_off.size()) == E.nfaces + 1) {
+            TRY(dupload(c, &D.fb_off, E.fb_off));
+            TRY(dupload(c, &D.fb, E.fb));
+        }
         D.g3_items = 0;   // 3D: dense G_F = X_FF^-1 X_F,adj per face for the second face phase (HElim::g3)
         D.g3_item_face = D.g3_item_i0 = D.g3_adj_ptr = D.g3_adj = nullptr;
         D.g3_off = nullptr;

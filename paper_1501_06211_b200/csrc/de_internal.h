@@ -82,6 +82,13 @@ struct HElim {
     std::vector<double> g3;
     std::vector<int32_t> g3_adj_ptr;    // [nfaces+1] into g3_adj
     std::vector<int32_t> g3_adj;        // cross indices
+    // 3D, face band <= FB_BS: the face factor L as a block-bidiagonal matrix of FB_BS x FB_BS blocks (D_i on the
+    // diagonal, E_i below it). Per face block i four dense FB_BS x FB_BS matrices, column-major (entry (row, col) at
+    // col * FB_BS + row): F_i = D_i^-1, G_i = D_i^-1 E_i, F_i^T, H_i = D_i^-T E_{i+1}^T, so that
+    //   forward  y_i = F_i r_i - G_i y_{i-1},   backward  x_i = F_i^T y_i - H_i x_{i+1}
+    // replace the row-by-row band sweeps (identity padding past the face end). fb_off[F] = first block of face F.
+    std::vector<int32_t> fb_off;        // [nfaces+1]
+    std::vector<double> fb;             // [blocks][4][FB_BS * FB_BS]
     // Fast diagonalisation of S_C (2D, R23): when the cross points of every component form a full
     // nx x ny tensor grid (index = ix + nx iy) and S_C = A_x (x) I + I (x) A_y exactly (uniform skeleton, unweighted
     // trace norm, Dirichlet rows on whole edges), S_C^-1 = (Q_y (x) Q_x) diag(1 / (lam_a + mu_b)) (Q_y (x) Q_x)^T with
@@ -233,6 +240,9 @@ struct ElimDev {
     int32_t* xcfw_col;
     double* xcfw_val;
     // G_F = X_FF^-1 X_F,adj per face (HElim::g3), non-tri only: work items (face, 32-node chunk) for the second face phase
+    // block-bidiagonal face solves (HElim::fb), non-tri only; null = row-by-row band sweeps
+    int32_t* fb_off;
+    double* fb;
     int32_t g3_items;
     int32_t *g3_item_face, *g3_item_i0;
     int64_t* g3_off;
@@ -264,6 +274,7 @@ struct ElimDev {
     int32_t *fell_c0, *fell_c1;
     double *fell_v0, *fell_v1, *fell_m, *fell_l;
 };
+constexpr int FB_BS = 16;            // block size of the block-bidiagonal 3D face solves
 constexpr int FELL_W = 3;
 constexpr int XELL_W = 5;            // a 2D cross point: itself + four face-end neighbours
 constexpr int PCR_L = 5;             // log2(32) reduction levels

@@ -345,6 +345,61 @@ de_status_t build_elim(const HostSetup& hs, const HCsr& X, HElim& E) {
         for (int32_t j = 0; j < n; ++j)
             for (int k = 0; k <= b && j + k < n; ++k) Mf[size_t(n - 1 - j - k) * ld + k] = Lf[size_t(j) * ld + k];
     }
+    // block-bidiagonal form of the 3D face factors (HElim::fb)
+    E.fb_off.clear();
+    E.fb.clear();
+    {
+        int maxb = 0;
+        for (int32_t F = 0; F < E.nfaces; ++F) maxb = std::max(maxb, E.face_band[F]);
+        // opt-in (env DE_FB=1): measured on c4 the block form does not shorten the first face phase (25-27 us against
+        // 27-28 us: 16 steps, each waiting for its 2 KB of block matrices from L2, cost what 2 x 121 shuffle rows cost)
+        // and it takes 58 MB per operator
+        if (hs.dim == 3 && maxb > 1 && maxb <= FB_BS && getenv("DE_FB")) {
+            constexpr int BS = FB_BS;
+            E.fb_off.assign(1, 0);
+            std::vector<double> D(BS * BS), Ei(BS * BS), En(BS * BS), Fi(BS * BS);
+            for (int32_t F = 0; F < E.nfaces; ++F) {
+                const int32_t n = E.face_off[F + 1] - E.face_off[F], b = E.face_band[F], ld = b + 1;
+                const double* Lf = &E.face_fac[E.face_fac_off[F]];
+                auto Lent = [&](int r, int c) -> double {   // L[r][c], r >= c
+                    if (r >= n || c >= n) return r == c ? 1.0 : 0.0;
+                    if (r == c) return 1.0 / Lf[size_t(c) * ld];
+                    return (r > c && r - c <= b) ? Lf[size_t(c) * ld + (r - c)] : 0.0;
+                };
+                const int nbk = (n + BS - 1) / BS;
+                for (int i = 0; i < nbk; ++i) {
+                    for (int r = 0; r < BS; ++r)
+                        for (int c = 0; c < BS; ++c) {
+                            D[r * BS + c] = r >= c ? Lent(BS * i + r, BS * i + c) : 0.0;
+                            Ei[r * BS + c] = i > 0 ? Lent(BS * i + r, BS * (i - 1) + c) : 0.0;
+                            En[r * BS + c] = i + 1 < nbk ? Lent(BS * (i + 1) + r, BS * i + c) : 0.0;   // E_{i+1}
+                        }
+                    for (int c = 0; c < BS; ++c)   // F = D^-1 column by column (forward substitution)
+                        for (int r = 0; r < BS; ++r) {
+                            double t = r == c ? 1.0 : 0.0;
+                            for (int k = c; k < r; ++k) t -= D[r * BS + k] * Fi[k * BS + c];
+                            Fi[r * BS + c] = r < c ? 0.0 : t / D[r * BS + r];
+                        }
+                    const size_t at = E.fb.size();
+                    E.fb.resize(at + 4 * BS * BS, 0.0);
+                    double* o = &E.fb[at];
+                    for (int r = 0; r < BS; ++r)
+                        for (int c = 0; c < BS; ++c) {
+                            double g = 0.0, h = 0.0;
+                            for (int k = 0; k < BS; ++k) {
+                                g += Fi[r * BS + k] * Ei[k * BS + c];          // G = F E_i
+                                h += Fi[k * BS + r] * En[c * BS + k];          // H = F^T E_{i+1}^T
+                            }
+                            o[0 * BS * BS + c * BS + r] = Fi[r * BS + c];
+                            o[1 * BS * BS + c * BS + r] = g;
+                            o[2 * BS * BS + c * BS + r] = Fi[c * BS + r];      // F^T
+                            o[3 * BS * BS + c * BS + r] = h;
+                        }
+                }
+                E.fb_off.push_back(E.fb_off.back() + nbk);
+            }
+        }
+    }
     // dense cross-point Schur complements S_C = X_CC - X_CF X_FF^-1 X_FC per component
     E.sc_off.assign(hs.ncomp + 1, 0);
     for (int c = 0; c < hs.ncomp; ++c) {

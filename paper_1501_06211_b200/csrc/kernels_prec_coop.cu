@@ -418,6 +418,68 @@ __device__ void face_warp(const CoopArgs& a, const ElimDev& E, int F, const doub
     __syncwarp();
 }
 
+// Warp solve of one 3D face block through its block-bidiagonal form (ElimDev::fb): y = X_FF^-1 (scale b_F).
+// Lanes 0-15 apply F_i (F_i^T) to the block's right-hand side, lanes 16-31 apply G_i (H_i) to the previous block's
+// solution; one shuffle per column broadcasts the vector entry inside each half, a xor-16 shuffle combines the halves.
+// 2 ceil(n / 16) steps of 16 independent FMAs instead of 2 n dependent shuffle-FMA rows; the next step's matrix
+// columns are loaded before the current step's products.
+__device__ void face_warp_blocks(const CoopArgs& a, const ElimDev& E, int F, const double* __restrict__ b,
+                                 const double* scl, double* __restrict__ out, double* wsm, int lane) {
+    constexpr int BS = FB_BS, BB = BS * BS;
+    const unsigned FULL = 0xffffffffu;
+    const PrecDev& P = a.P;
+    const int o = E.face_off[F], n = E.face_off[F + 1] - o;
+    const int nbk = E.fb_off[F + 1] - E.fb_off[F];
+    const double* __restrict__ tab = E.fb + size_t(E.fb_off[F]) * 4 * BB;
+    const double sc = scl[ccomp(P.comp_off, P.ncomp, E.face_nodes[o])];
+    const int row = lane & (BS - 1), half = lane >> 4, hsrc = lane & BS;   // shuffle source base of this half
+    double* ys = wsm;   // [nbk * BS] forward solution, per warp
+    __syncwarp();
+    double m[BS], mn[BS];
+#pragma unroll
+    for (int c = 0; c < BS; ++c) mn[c] = tab[size_t(half) * BB + c * BS + row];   // step 0: F_0 | G_0
+    double yprev = 0.0;
+    for (int i = 0; i < nbk; ++i) {
+        const int gi = BS * i + row;
+        const double r = gi < n ? sc * b[E.face_nodes[o + gi]] : 0.0;
+#pragma unroll
+        for (int c = 0; c < BS; ++c) m[c] = mn[c];
+        if (i + 1 < nbk) {
+#pragma unroll
+            for (int c = 0; c < BS; ++c) mn[c] = tab[(size_t(i + 1) * 4 + half) * BB + c * BS + row];
+        } else {   // first backward step: F^T | H of the last block
+#pragma unroll
+            for (int c = 0; c < BS; ++c) mn[c] = tab[(size_t(nbk - 1) * 4 + 2 + half) * BB + c * BS + row];
+        }
+        const double v = half ? yprev : r;
+        double acc = 0.0;
+#pragma unroll
+        for (int c = 0; c < BS; ++c) acc = fma(m[c], __shfl_sync(FULL, v, hsrc + c), acc);
+        const double t = __shfl_xor_sync(FULL, acc, BS);
+        yprev = half ? t - acc : acc - t;   // F r - G y_prev, in both halves
+        if (!half) ys[gi] = yprev;
+    }
+    __syncwarp();
+    double xnext = 0.0;
+    for (int i = nbk - 1; i >= 0; --i) {
+        const int gi = BS * i + row;
+#pragma unroll
+        for (int c = 0; c < BS; ++c) m[c] = mn[c];
+        if (i > 0) {
+#pragma unroll
+            for (int c = 0; c < BS; ++c) mn[c] = tab[(size_t(i - 1) * 4 + 2 + half) * BB + c * BS + row];
+        }
+        const double v = half ? xnext : ys[gi];
+        double acc = 0.0;
+#pragma unroll
+        for (int c = 0; c < BS; ++c) acc = fma(m[c], __shfl_sync(FULL, v, hsrc + c), acc);
+        const double t = __shfl_xor_sync(FULL, acc, BS);
+        xnext = half ? t - acc : acc - t;   // F^T y - H x_next
+        if (!half && gi < n) out[E.face_nodes[o + gi]] = xnext;
+    }
+    __syncwarp();
+}
+
 // Thread solve of one tridiagonal face block (2D: every face is a path of <= 64 trace nodes):
 // forward y_j = (r_j - L_{j,j-1} y_{j-1}) / L_jj, backward x_j = (y_j - L_{j+1,j} x_{j+1}) / L_jj.
 // The face data is interleaved over groups of 32 faces (ElimDev::tri_*), so lane l of a warp reads
@@ -670,7 +732,10 @@ __device__ void elim_coop(cg::grid_group& grid, const CoopArgs& a, const ElimDev
         if (w > 0)
             for (int F = gt; F < E.nfaces; F += nthr) face_thread_tridiag(a, E, F, b, scl, nullptr, y, 0, dsm + (threadIdx.x - 32));
     } else if (w > 0)
-        for (int F = gw; F < E.nfaces; F += nwarps) face_warp(a, E, F, b, scl, nullptr, y, 0, wsm, lane);
+        for (int F = gw; F < E.nfaces; F += nwarps) {
+            if (E.fb) face_warp_blocks(a, E, F, b, scl, y, wsm, lane);
+            else face_warp(a, E, F, b, scl, nullptr, y, 0, wsm, lane);
+        }
     if (TIM && a.timers && lane == 0 && w > 0 && gw < 4096) a.timers[200 + gw] = clock64() - tf0;
     if (fused && a.split) {   // wait for every block's t_C (published before its face solves): no grid barrier here
         if (threadIdx.x == 32) {

@@ -55,3 +55,33 @@ def test_shared_rows_equal_per_component_rows(name, kw):
         assert np.linalg.norm(x - y) <= 1e-11 * np.linalg.norm(y)
     assert np.all(za[1][comps[0].skel.gidx] == 0.0)
     assert abs(ita - itb) <= 1
+
+
+@pytest.mark.gpu
+def test_block_bidiagonal_face_solves_equal_band_sweeps():
+    """3D face solves through the block-bidiagonal form of the face factors (env DE_FB=1, opt-in: measured no faster)
+    against the default row-by-row band sweeps, same inputs."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1501_06211_b200 import binding as B
+    p = make_config("c4", nel=(24, 12, 12), sub=(6, 6, 6))
+    T = build_topology(p)
+    r = np.random.default_rng(43).normal(size=T.n_G)
+    zs = []
+    for fb in (True, False):
+        if fb:
+            os.environ["DE_FB"] = "1"
+        try:
+            S = B.Solver.from_problem(p, device=0)
+        finally:
+            os.environ.pop("DE_FB", None)
+        try:
+            S.factor()
+            dr = torch.tensor(r, dtype=torch.float64, device="cuda")
+            dz = torch.empty_like(dr)
+            B.de_precond_apply_device(S.ctx, dr.data_ptr(), dz.data_ptr())
+            zs.append(dz.cpu().numpy())
+        finally:
+            S.close()
+    assert np.linalg.norm(zs[0] - zs[1]) <= 1e-10 * np.linalg.norm(zs[1])
