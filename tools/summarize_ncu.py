@@ -62,12 +62,17 @@ if __name__ == '__main__':
         launches(f'{go}/launches_bench_c4.csv', f'profiles/{rnd}_launches_bench_c4.md',
                  f'{rnd} launch list: `bench.py --config c4 --steps 1 --warmup 2 --no-e2e --no-cpu-baseline` (config c4)')
     tr = {}
+    try:   # keep the figures of kernels that were not captured again
+        tr = json.load(open('profiles/traffic.json'))['dram_bytes_per_launch']
+    except Exception:
+        pass
     tr['k_prec_coop'] = full(f'{go}/r2_k_prec_coop.ncu-rep', f'profiles/{rnd}_prec_coop_c5.md',
                              f'{rnd}: k_prec_coop (C5 preconditioner, one cooperative launch), config c5',
                              algo_bytes=algo.get('k_prec_coop'))
-    tr['k_schur_explicit'] = full(f'{go}/r2_k_schur_explicit.ncu-rep', f'profiles/{rnd}_schur_explicit_c5.md',
-                                  f'{rnd}: k_schur_explicit (C2 explicit local Schur apply), config c5',
-                                  algo_bytes=algo.get('k_schur_explicit'))
+    if os.path.exists(f'{go}/r2_k_schur_explicit.ncu-rep'):
+        tr['k_schur_explicit'] = full(f'{go}/r2_k_schur_explicit.ncu-rep', f'profiles/{rnd}_schur_explicit_c5.md',
+                                      f'{rnd}: k_schur_explicit (C2 explicit local Schur apply), config c5',
+                                      algo_bytes=algo.get('k_schur_explicit'))
     json.dump({"config": "c5", "n_gpus": 1, "dram_bytes_per_launch": tr,
                "source": [f"profiles/{rnd}_prec_coop_c5.md", f"profiles/{rnd}_schur_explicit_c5.md"]},
               open('profiles/traffic.json', 'w'), indent=1)
