@@ -444,7 +444,8 @@ void prec_prepare(const PrecDev& P);   // one-time kernel attributes (outside gr
 struct CoopBuffers {
     int nb = 0, nsm = 148;
     size_t smem = 0;
-    int stage = 0, per_warp = 0, mf = 0, ncmax = 0, nbc_max = 0, tridiag = 0, gram_cgs2 = 1, fold = 0, split = 1, shr = 0;
+    int stage = 0, per_warp = 0, mf = 0, ncmax = 0, nbc_max = 0, tridiag = 0, gram_cgs2 = 1, fold = 0, split = 1, shr = 0, sc_persist = 0;
+    size_t sc_persist_bytes = 0;
     double* redf = nullptr;      // fold sums of the shared-row cross-point solve: [2][MAXC][NRED][nb]
     double* ucross = nullptr;   // fold: [KMAX][ncross of eK]
     unsigned int* arrive = nullptr;   // split-phase arrival counter of the fused eliminations (zero between launches)

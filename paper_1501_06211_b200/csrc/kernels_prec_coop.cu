@@ -54,6 +54,7 @@ struct CoopArgs {
     int smem_doubles;   // dynamic shared memory of the launch in doubles (fast-diagonalisation tables fit test)
     int shr;            // 1: a shared S_C^-1 (HElim::sc_shared) is applied for ALL components by the block that loads a row
     double* redf;       // [2][MAXC][NRED][nb] fold sums when shr (every block contributes to every component)
+    int sc_persist;     // 1: eK's S_C^-1 sits in the persisting L2 set-aside (access-policy window of the launch): plain loads
     int split;          // 1: fused eliminations wait on the arrival counter between t_C and the cross-point solve (no grid barrier)
     double* ucross;     // [KMAX][ncross of eK]: u_t = G^T (M W_t)_F, the face part of M W_t folded onto cross points
     unsigned int* arrive;   // split-phase arrival counter of the fused eliminations (t_C published -> cross-point solve)
@@ -612,6 +613,48 @@ __device__ __forceinline__ void face_warp_pcr(const PrecDev& P, const ElimDev& E
     }
 }
 
+// Rows [rlo, rhi) of x_C = S_C^-1 t_C: warp w takes the column slice [c0, c1) of all of them, RB rows x NA loads per
+// lane in flight; warp partials into part[w][row]. STREAM: evict-first loads (the matrix is streamed once per
+// elimination); false: plain loads for a matrix held in the persisting L2 set-aside (CoopArgs::sc_persist).
+template <bool STREAM>
+__device__ __forceinline__ void sc_rows(const double* __restrict__ S, int ncc, int rlo, int rhi, int nr, int c0, int c1,
+                                        int w, int lane, const double* tC, double* part) {
+    constexpr int NA = 8, RB = 4;
+    for (int r = rlo; r < rhi; r += RB) {
+        const double* __restrict__ row[RB];
+        double sr[RB];
+#pragma unroll
+        for (int u = 0; u < RB; ++u) {
+            row[u] = S + size_t(r + u < rhi ? r + u : r) * ncc;
+            sr[u] = 0.0;
+        }
+        for (int j = c0 + lane; j < c1; j += 32 * NA) {
+            double v[RB][NA], t[NA];
+#pragma unroll
+            for (int q = 0; q < NA; ++q) {
+                const int jj = j + 32 * q;
+                const bool ok = jj < c1;
+                // streamed once per step (evict-first); a shared S_C^-1 (HElim::sc_shared) is read by the blocks of
+                // every component at about the same time, and evict-first lines still serve the partner (measured
+                // again in round 2 with the lighter consumer: cached loads 0.615 vs 0.578 ms)
+#pragma unroll
+                for (int u = 0; u < RB; ++u)
+                    v[u][q] = (ok && r + u < rhi) ? (STREAM ? __ldcs(row[u] + jj) : __ldg(row[u] + jj)) : 0.0;
+                t[q] = ok ? tC[jj] : 0.0;
+            }
+#pragma unroll
+            for (int q = 0; q < NA; ++q)
+#pragma unroll
+                for (int u = 0; u < RB; ++u) sr[u] += v[u][q] * t[q];
+        }
+#pragma unroll
+        for (int u = 0; u < RB; ++u) {
+            const double su = warp_sum(sr[u]);
+            if (lane == 0 && r + u < rhi) part[w * nr + (r + u - rlo)] = su;
+        }
+    }
+}
+
 // which cross-point solve an elimination uses in block component c (the same answer in elim_coop and in the caller)
 __device__ __forceinline__ bool use_fd(const CoopArgs& a, const ElimDev& E, int c) {
     const int ncc = E.cross_comp_off[c + 1] - E.cross_comp_off[c];
@@ -1063,39 +1106,8 @@ __device__ void elim_coop(cg::grid_group& grid, const CoopArgs& a, const ElimDev
                 // ~13 rows (c5) take 4 dependent batches instead of 7); warp partials are summed in fixed order
                 const int cw = ((ncc + CW * 32 - 1) / (CW * 32)) * 32;
                 const int c0 = w * cw, c1 = min(ncc, c0 + cw);
-                constexpr int NA = 8, RB = 4;
-                for (int r = rlo; r < rhi; r += RB) {
-                    const double* __restrict__ row[RB];
-                    double sr[RB];
-#pragma unroll
-                    for (int u = 0; u < RB; ++u) {
-                        row[u] = S + size_t(r + u < rhi ? r + u : r) * ncc;
-                        sr[u] = 0.0;
-                    }
-                    for (int j = c0 + lane; j < c1; j += 32 * NA) {
-                        double v[RB][NA], t[NA];
-#pragma unroll
-                        for (int q = 0; q < NA; ++q) {
-                            const int jj = j + 32 * q;
-                            const bool ok = jj < c1;
-                            // streamed once per step (evict-first); a shared S_C^-1 (HElim::sc_shared) is read by the
-                            // blocks of every component at about the same time, and evict-first lines still serve the
-                            // partner (measured again in round 2 with the lighter consumer: cached loads 0.615 vs 0.578 ms)
-#pragma unroll
-                            for (int u = 0; u < RB; ++u) v[u][q] = (ok && r + u < rhi) ? __ldcs(row[u] + jj) : 0.0;
-                            t[q] = ok ? tC[jj] : 0.0;
-                        }
-#pragma unroll
-                        for (int q = 0; q < NA; ++q)
-#pragma unroll
-                            for (int u = 0; u < RB; ++u) sr[u] += v[u][q] * t[q];
-                    }
-#pragma unroll
-                    for (int u = 0; u < RB; ++u) {
-                        const double su = warp_sum(sr[u]);
-                        if (lane == 0 && r + u < rhi) part[w * nr + (r + u - rlo)] = su;
-                    }
-                }
+                if (a.sc_persist && &E == &a.P.eK) sc_rows<false>(S, ncc, rlo, rhi, nr, c0, c1, w, lane, tC, part);
+                else sc_rows<true>(S, ncc, rlo, rhi, nr, c0, c1, w, lane, tC, part);
             }
             if (dbg2) a.timers[182] = gtimer();
             __syncthreads();
@@ -2144,6 +2156,23 @@ bool prec_coop_prepare(const PrecDev& P, int device, CoopBuffers& B) {
         // L2 anyway); three (3D wirebasket): c4 cross-point phase 34 -> 31.8 us
         B.shr = ((P.ncomp > 2 || getenv("DE_SHR")) && need <= B.smem && !getenv("DE_NO_SHR")) ? 1 : 0;
     }
+    B.sc_persist = 0;
+    B.sc_persist_bytes = 0;
+    if (getenv("DE_SC_PERSIST") && !P.eK.fd) {   // opt-in A/B: persisting-L2 window over eK's S_C^-1 (<= 40 MB)
+        size_t bytes = 0;
+        for (int c = 0; c < (P.eK.sc_shared ? 1 : P.ncomp); ++c) {
+            const size_t n = size_t(P.eK.cross_comp_off[c + 1] - P.eK.cross_comp_off[c]);
+            bytes += n * n * 8;
+        }
+        int maxp = 0;
+        cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, device);
+        if (bytes > 0 && bytes <= size_t(40) << 20 && bytes <= size_t(maxp)) {
+            cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, bytes);
+            B.sc_persist = 1;
+            B.sc_persist_bytes = bytes;
+        }
+        if (getenv("DE_VERBOSE")) fprintf(stderr, "[de] S_C^-1 persisting window: %zu bytes (max %d) -> %d\n", bytes, maxp, B.sc_persist);
+    }
     B.split = getenv("DE_NO_SPLIT") ? 0 : 1;   // A/B switch: a grid barrier between t_C and the cross-point solve
     if (getenv("DE_VERBOSE")) fprintf(stderr, "[de] k_prec_coop: fold %d (R22) split %d\n", B.fold, B.split);
     return true;
@@ -2176,6 +2205,7 @@ int prec_apply_coop(const PrecDev& P, const CoopBuffers& B, const double* r, dou
     a.ucross = B.ucross;
     a.arrive = B.arrive;
     a.split = B.split;
+    a.sc_persist = B.sc_persist;
     a.shr = B.shr;
     a.redf = B.redf;
     a.smem_doubles = int(B.smem / sizeof(double));
@@ -2185,11 +2215,20 @@ int prec_apply_coop(const PrecDev& P, const CoopBuffers& B, const double* r, dou
     cfg.blockDim = dim3(CT);
     cfg.dynamicSmemBytes = B.smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeCooperative;
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    if (B.sc_persist) {   // eK's S_C^-1 (re-read by every K-elimination) held in the persisting L2 set-aside
+        attr[1].id = cudaLaunchAttributeAccessPolicyWindow;
+        attr[1].val.accessPolicyWindow.base_ptr = const_cast<double*>(P.eK.Sinv);
+        attr[1].val.accessPolicyWindow.num_bytes = B.sc_persist_bytes;
+        attr[1].val.accessPolicyWindow.hitRatio = 1.0f;
+        attr[1].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        attr[1].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        cfg.numAttrs = 2;
+    }
     cudaError_t e = cudaLaunchKernelEx(&cfg, reinterpret_cast<void (*)(CoopArgs)>(const_cast<void*>(B.kfn)), a);
     if (e != cudaSuccess) return -1;
     const size_t rsm = size_t(4 * KMAX * (KMAX + 1) + 6 * KMAX) * sizeof(double);
