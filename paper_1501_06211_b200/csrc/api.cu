@@ -123,7 +123,7 @@ struct de_ctx {
             *d_ig_db = nullptr, *d_ig_sub = nullptr, *d_gxp = nullptr, *d_gx_col = nullptr, *d_gx_da = nullptr,
             *d_gx_db = nullptr, *d_gx_sub = nullptr;
     double* d_dinv = nullptr;   // inverse diagonal blocks of the factors (wide bands, k_schur_blk)
-    int dinv_np = 0;
+    int dinv_np = 0, dinv_bs = 16;
     double *d_ig_val = nullptr, *d_gx_val = nullptr, *d_band = nullptr, *d_scratch = nullptr, *d_qloc = nullptr;
     int64_t n_ig = 0, n_gx = 0;
     int32_t *d_gptr = nullptr, *d_gsrc = nullptr, *d_gamma_dofs = nullptr;
@@ -249,6 +249,7 @@ SchurArgs schur_args(de_ctx* c, int mode, const double* xin, const double* f, do
     a.band = c->d_band;
     a.dinv = c->d_dinv;
     a.dinv_np = c->dinv_np;
+    a.dinv_bs = c->dinv_bs;
     a.ld = c->hs.ld;
     a.band_w = c->hs.band;
     a.idofs = c->d_idofs;
@@ -1198,8 +1199,9 @@ de_status_t setup_impl(const de_mesh_t* mesh, const double* density, double E0, 
     TRY(dalloc(c, &c->d_gx_val, size_t(c->n_gx)));
     TRY(dalloc(c, &c->d_band, 2 * size_t(c->n_local_I) * hs.ld));
     if ((hs.band + 1 + 31) / 32 > 4 && !getenv("DE_NO_DINV")) {   // wide bands (3D): k_schur_blk applies inverse diagonal blocks
-        c->dinv_np = (c->max_nI + BLK_D - 1) / BLK_D;
-        TRY(dalloc(c, &c->d_dinv, size_t(c->nsl) * c->dinv_np * BLK_D * BLK_D));
+        c->dinv_bs = schur_blk_panel_width(hs.ld, c->max_nI, c->max_nG);
+        c->dinv_np = (c->max_nI + c->dinv_bs - 1) / c->dinv_bs;
+        TRY(dalloc(c, &c->d_dinv, size_t(c->nsl) * c->dinv_np * c->dinv_bs * c->dinv_bs));
     }
     {   // explicit local Schur complements: decide, then allocate S_s and a column batch
         const double fac_one_pass = double(c->n_local_I) * (hs.band + 1);
@@ -1335,7 +1337,7 @@ de_status_t factor_impl(de_ctx* c) {
     launch_assemble_pairs(c->md, c->d_gx_da, c->d_gx_db, c->d_gx_sub, c->d_Ee, c->d_gx_val, c->n_gx, c->st);
     DE_CUDA(cudaMemsetAsync(c->d_fail, 0, sizeof(int), c->st));
     launch_band_cholesky(c->d_sd, c->nsl, c->d_band, hs.ld, hs.band, c->d_fail, c->st);
-    if (c->d_dinv) launch_blk_diag_inv(c->d_sd, c->nsl, c->d_band, hs.ld, c->d_dinv, c->dinv_np, c->st);
+    if (c->d_dinv) launch_blk_diag_inv(c->d_sd, c->nsl, c->d_band, hs.ld, c->d_dinv, c->dinv_np, c->dinv_bs, c->st);
     if (c->explicit_schur)   // S_s e_t for every local Gamma dof t, through the same interior solves
         for (int s0 = 0; s0 < c->nsl; s0 += c->col_batch) {
             SchurArgs a = schur_args(c, SCHUR_COLUMNS, nullptr, nullptr, nullptr, nullptr);

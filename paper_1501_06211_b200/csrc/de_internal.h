@@ -361,13 +361,14 @@ struct SchurArgs {
     double* colscratch;     // nsl*maxG*max_nI doubles
     int col_s0, max_nI;
     int max_ig;             // max A_IG entries of one subdomain (shared-memory staging in the formation)
-    // wide bands (k_schur_blk): inverses of the BLK_D x BLK_D diagonal blocks of L, [local subdomain][dinv_np][BLK_D][BLK_D]
+    // wide bands (k_schur_blk): inverses of the bs x bs diagonal blocks of L, [local subdomain][dinv_np][bs][bs]
     // row-major lower triangular (identity padding), formed after the factorisation; null = substitution chain
     const double* dinv;
-    int dinv_np;
+    int dinv_np, dinv_bs;   // blocks per subdomain, block size (= panel width of the k_schur_blk variant in use)
 };
-constexpr int BLK_D = 16;   // = panel width of the default k_schur_blk variant
-void launch_blk_diag_inv(const SubDesc* sd, int nsl, const double* band, int ld, double* dinv, int dinv_np, cudaStream_t st);
+int schur_blk_panel_width(int ld, int max_nI, int maxG);
+void launch_blk_diag_inv(const SubDesc* sd, int nsl, const double* band, int ld, double* dinv, int dinv_np, int bs,
+                         cudaStream_t st);
 int launch_schur_local(const SchurArgs& a, cudaStream_t st);
 // q_s = S_s x_s with the explicit column-major S_s (one CTA per subdomain, coalesced over rows)
 void launch_schur_explicit(const SubDesc* sd, int nsl, const double* sexp, const int32_t* Rg, const double* xin,

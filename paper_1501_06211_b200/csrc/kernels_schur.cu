@@ -581,6 +581,7 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 // Inverses of the BLK_D x BLK_D diagonal blocks of every local factor (one warp per block, lane c = column c of the
 // inverse by forward substitution): the blocked sweeps below apply them as small dense products, so no 16-step
 // shuffle chain sits between a panel's arrival and its trailing update.
+template <int BLK_D>
 __global__ void __launch_bounds__(256) k_blk_diag_inv(const SubDesc* sd, int nsl, const double* __restrict__ band, int ld,
                                                       double* __restrict__ dinv, int np_max) {
     const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
@@ -617,10 +618,15 @@ __global__ void __launch_bounds__(256) k_blk_diag_inv(const SubDesc* sd, int nsl
     for (int i = 0; i < BLK_D; ++i) out[i * BLK_D + c] = x[i];
 }
 
-void launch_blk_diag_inv(const SubDesc* sd, int nsl, const double* band, int ld, double* dinv, int dinv_np, cudaStream_t st) {
+void launch_blk_diag_inv(const SubDesc* sd, int nsl, const double* band, int ld, double* dinv, int dinv_np, int bs,
+                         cudaStream_t st) {
     const long long warps = (long long)nsl * dinv_np;
     if (warps <= 0) return;
-    k_blk_diag_inv<<<unsigned((warps + 7) / 8), 256, 0, st>>>(sd, nsl, band, ld, dinv, dinv_np);
+    const unsigned grid = unsigned((warps + 7) / 8);
+    if (bs == 16) k_blk_diag_inv<16><<<grid, 256, 0, st>>>(sd, nsl, band, ld, dinv, dinv_np);
+    else if (bs == 12) k_blk_diag_inv<12><<<grid, 256, 0, st>>>(sd, nsl, band, ld, dinv, dinv_np);
+    else if (bs == 8) k_blk_diag_inv<8><<<grid, 256, 0, st>>>(sd, nsl, band, ld, dinv, dinv_np);
+    else k_blk_diag_inv<4><<<grid, 256, 0, st>>>(sd, nsl, band, ld, dinv, dinv_np);
 }
 
 constexpr int BK_T = 256;   // threads; BK_P panel columns, BK_S ring stages (template: tuned per band width)
@@ -634,27 +640,30 @@ __global__ void __launch_bounds__(BK_T, 1) k_schur_blk(SchurArgs a) {
     const int mode = a.mode;
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
     double* pan = reinterpret_cast<double*>(smem + 128);   // [BK_S][BK_P][ld]
-    double* dblk = pan + BK_S * BK_P * ld;                 // [BK_S][BLK_D][BLK_D] inverse diagonal blocks (use_dinv)
-    double* v = dblk + BK_S * BLK_D * BLK_D;               // [n]: rhs, then y, then x
-    const bool use_dinv = BK_P == BLK_D && a.dinv != nullptr;
-    const double* dsrc = use_dinv ? a.dinv + size_t(blockIdx.x) * a.dinv_np * BLK_D * BLK_D : nullptr;
-    double* xl = v + a.max_nI;                             // [nG]
+    double* dblk = pan + BK_S * BK_P * ld;                 // [BK_S][BK_P][BK_P] inverse diagonal blocks (use_dinv)
+    double* v = dblk + BK_S * BK_P * BK_P;               // [n]: rhs, then y, then x
+    const bool use_dinv = a.dinv != nullptr && a.dinv_bs == BK_P;
+    const double* dsrc = use_dinv ? a.dinv + size_t(blockIdx.x) * a.dinv_np * BK_P * BK_P : nullptr;
+    // [nG] gathered interface values: behind v, or (ring of three or more stages: no room for both) in the LAST ring
+    // stage, which the prologue and the epilogue use while no panel lives there
+    constexpr bool XL_IN_RING = BK_S >= 3;
+    double* xl = XL_IN_RING ? pan + size_t(BK_S - 1) * BK_P * ld : v + a.max_nI;
     const double* Lb = a.band + d.band_off;
     const int np = (n + BK_P - 1) / BK_P;
     auto panel_of = [&](int q) { return q < np ? q : 2 * np - 1 - q; };   // forward ascending, backward descending
     auto issue = [&](int q) {
         const int p = panel_of(q), c0 = p * BK_P, nc = min(BK_P, n - c0);
         const uint32_t bytes = uint32_t(nc) * uint32_t(ld) * 8u;
-        const uint32_t dbytes = use_dinv ? uint32_t(BLK_D * BLK_D * 8) : 0u;
+        const uint32_t dbytes = use_dinv ? uint32_t(BK_P * BK_P * 8) : 0u;
         mbar_expect_tx(bar + (q % BK_S), bytes + dbytes);
         tma_load_1d(pan + size_t(q % BK_S) * BK_P * ld, Lb + size_t(c0) * ld, bytes, bar + (q % BK_S));
         if (use_dinv)
-            tma_load_1d(dblk + size_t(q % BK_S) * BLK_D * BLK_D, dsrc + size_t(p) * BLK_D * BLK_D, dbytes, bar + (q % BK_S));
+            tma_load_1d(dblk + size_t(q % BK_S) * BK_P * BK_P, dsrc + size_t(p) * BK_P * BK_P, dbytes, bar + (q % BK_S));
     };
     if (tid == 0) {
         for (int i = 0; i < BK_S; ++i) mbar_init(bar + i, 1);
         fence_mbar_init();
-        for (int q = 0; q < min(BK_S, 2 * np); ++q) issue(q);
+        for (int q = 0; q < min(BK_S - (XL_IN_RING ? 1 : 0), 2 * np); ++q) issue(q);
     }
     if (mode != SCHUR_CONDENSE)
         for (int l = tid; l < nG; l += BK_T) xl[l] = a.xin[a.Rg[d.goff + l]];
@@ -671,18 +680,19 @@ __global__ void __launch_bounds__(BK_T, 1) k_schur_blk(SchurArgs a) {
         v[r] = val;
     }
     __syncthreads();
+    if (XL_IN_RING && tid == 0 && BK_S - 1 < 2 * np) issue(BK_S - 1);   // the last stage is free of xl now
     for (int q = 0; q < 2 * np; ++q) {
         mbar_wait(bar + (q % BK_S), uint32_t((q / BK_S) & 1));
         const double* P = pan + size_t(q % BK_S) * BK_P * ld;
         const int p = panel_of(q), j0 = p * BK_P, nc = min(BK_P, n - j0);
         if (q < np) {   // forward: diagonal block, then the rows below
             if (wid == 0 && use_dinv) {   // y_blk = L_jj^-1 v_blk: 16 independent row products, no chain
-                const double* D = dblk + size_t(q % BK_S) * BLK_D * BLK_D;
+                const double* D = dblk + size_t(q % BK_S) * BK_P * BK_P;
                 double acc = 0.0;
                 if (lane < nc) {
 #pragma unroll
-                    for (int jj = 0; jj < BLK_D; ++jj)
-                        if (jj <= lane) acc = fma(D[lane * BLK_D + jj], v[j0 + jj], acc);
+                    for (int jj = 0; jj < BK_P; ++jj)
+                        if (jj <= lane) acc = fma(D[lane * BK_P + jj], v[j0 + jj], acc);
                 }
                 __syncwarp();
                 if (lane < nc) v[j0 + lane] = acc;
@@ -722,12 +732,12 @@ __global__ void __launch_bounds__(BK_T, 1) k_schur_blk(SchurArgs a) {
             }
             __syncthreads();
             if (wid == 0 && use_dinv) {   // x_blk = L_jj^-T t_blk
-                const double* D = dblk + size_t(q % BK_S) * BLK_D * BLK_D;
+                const double* D = dblk + size_t(q % BK_S) * BK_P * BK_P;
                 double acc = 0.0;
                 if (lane < nc) {
 #pragma unroll
-                    for (int jj = 0; jj < BLK_D; ++jj)
-                        if (jj >= lane && jj < nc) acc = fma(D[jj * BLK_D + lane], v[j0 + jj], acc);
+                    for (int jj = 0; jj < BK_P; ++jj)
+                        if (jj >= lane && jj < nc) acc = fma(D[jj * BK_P + lane], v[j0 + jj], acc);
                 }
                 __syncwarp();
                 if (lane < nc) v[j0 + lane] = acc;
@@ -754,6 +764,10 @@ __global__ void __launch_bounds__(BK_T, 1) k_schur_blk(SchurArgs a) {
         for (int i = tid; i < n; i += BK_T) a.u[idofs[i]] = v[i];
         return;
     }
+    if (XL_IN_RING && mode == SCHUR_APPLY) {   // every panel is consumed: the ring holds xl again for A_GG x
+        for (int l = tid; l < nG; l += BK_T) xl[l] = a.xin[a.Rg[d.goff + l]];
+        __syncthreads();
+    }
     const int32_t* gxp = a.gxp + d.gxp_off;
     for (int l = tid; l < nG; l += BK_T) {
         double qv = 0.0;
@@ -776,18 +790,25 @@ typedef void (*blk_fn)(SchurArgs);
 struct BlkVariant {
     blk_fn fn;
     size_t smem;
+    int panel;
 };
 static BlkVariant blk_variant(int ld, int max_nI, int maxG, bool set_attr) {
-    static const int PS[5][2] = {{16, 2}, {8, 4}, {12, 3}, {8, 5}, {4, 8}};
-    static const blk_fn FN[5] = {k_schur_blk<16, 2>, k_schur_blk<8, 4>, k_schur_blk<12, 3>, k_schur_blk<8, 5>, k_schur_blk<4, 8>};
+    static const int PS[6][2] = {{16, 2}, {8, 4}, {12, 3}, {8, 5}, {4, 8}, {16, 3}};
+    static const blk_fn FN[6] = {k_schur_blk<16, 2>, k_schur_blk<8, 4>, k_schur_blk<12, 3>, k_schur_blk<8, 5>, k_schur_blk<4, 8>,
+                                 k_schur_blk<16, 3>};
     int v = 0;
-    if (const char* e = getenv("DE_BLK_VARIANT")) v = std::max(0, std::min(4, atoi(e)));
-    auto need = [&](int k) { return 128 + sizeof(double) * (size_t(PS[k][1]) * (PS[k][0] * ld + BLK_D * BLK_D) + max_nI + maxG); };
-    if (need(v) > 227 * 1024) v = 0;
-    BlkVariant r{FN[v], need(v)};
+    if (const char* e = getenv("DE_BLK_VARIANT")) v = std::max(0, std::min(5, atoi(e)));
+    auto need = [&](int k) {   // rings of >= 3 stages keep xl in their last stage (no maxG term)
+        return 128 + sizeof(double) * (size_t(PS[k][1]) * (PS[k][0] * ld + PS[k][0] * PS[k][0]) + max_nI + (PS[k][1] >= 3 ? 0 : maxG));
+    };
+    if (need(v) > 227 * 1024 || (PS[v][1] >= 3 && maxG > PS[v][0] * ld)) v = 0;
+    BlkVariant r{FN[v], need(v), PS[v][0]};
     if (set_attr) raise_dyn_smem(reinterpret_cast<const void*>(r.fn), r.smem);
     return r;
 }
+
+// panel width of the variant in use (= block size of the inverse diagonal blocks)
+int schur_blk_panel_width(int ld, int max_nI, int maxG) { return blk_variant(ld, max_nI, maxG, false).panel; }
 
 // once per context, outside any graph capture
 void prepare_schur_blk(int ld, int band_w, int max_nI, int maxG) {
