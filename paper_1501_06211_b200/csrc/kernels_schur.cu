@@ -630,7 +630,9 @@ void launch_blk_diag_inv(const SubDesc* sd, int nsl, const double* band, int ld,
 }
 
 constexpr int BK_T = 256;   // threads; BK_P panel columns, BK_S ring stages (template: tuned per band width)
-template <int BK_P, int BK_S>
+// BK_TH: the last BK_TH columns of every panel are loaded by the CTA's threads (16-byte cp.async, completion tracked by the
+// panel's mbarrier) beside the bulk copy of the first BK_P - BK_TH: a second stream per SM.
+template <int BK_P, int BK_S, int BK_TH = 0>
 __global__ void __launch_bounds__(BK_T, 1) k_schur_blk(SchurArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     if (a.state != nullptr && a.state->done) return;
@@ -651,8 +653,8 @@ __global__ void __launch_bounds__(BK_T, 1) k_schur_blk(SchurArgs a) {
     const double* Lb = a.band + d.band_off;
     const int np = (n + BK_P - 1) / BK_P;
     auto panel_of = [&](int q) { return q < np ? q : 2 * np - 1 - q; };   // forward ascending, backward descending
-    auto issue = [&](int q) {
-        const int p = panel_of(q), c0 = p * BK_P, nc = min(BK_P, n - c0);
+    auto issue = [&](int q) {   // thread 0: the bulk copies of panel q (its first BK_P - BK_TH columns) and of its diagonal block
+        const int p = panel_of(q), c0 = p * BK_P, nc = min(BK_P - BK_TH, n - c0);
         const uint32_t bytes = uint32_t(nc) * uint32_t(ld) * 8u;
         const uint32_t dbytes = use_dinv ? uint32_t(BK_P * BK_P * 8) : 0u;
         mbar_expect_tx(bar + (q % BK_S), bytes + dbytes);
@@ -660,10 +662,27 @@ __global__ void __launch_bounds__(BK_T, 1) k_schur_blk(SchurArgs a) {
         if (use_dinv)
             tma_load_1d(dblk + size_t(q % BK_S) * BK_P * BK_P, dsrc + size_t(p) * BK_P * BK_P, dbytes, bar + (q % BK_S));
     };
+    auto issue_threads = [&](int q) {   // every thread: its share of the panel's last BK_TH columns, then one arrival
+        if constexpr (BK_TH > 0) {
+            const int p = panel_of(q), c0 = p * BK_P + (BK_P - BK_TH), nc = max(0, min(BK_TH, n - c0));
+            const int chunks = nc * ld / 2;   // 16-byte chunks (ld is even)
+            const double* src = Lb + size_t(c0) * ld;
+            double* dst = pan + size_t(q % BK_S) * BK_P * ld + size_t(BK_P - BK_TH) * ld;
+            for (int i = tid; i < chunks; i += BK_T) {
+                const unsigned sa = smem_u32(dst + 2 * i);
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(src + 2 * i) : "memory");
+            }
+            asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar + (q % BK_S))) : "memory");
+        }
+    };
     if (tid == 0) {
-        for (int i = 0; i < BK_S; ++i) mbar_init(bar + i, 1);
+        for (int i = 0; i < BK_S; ++i) mbar_init(bar + i, 1 + (BK_TH > 0 ? BK_T : 0));
         fence_mbar_init();
-        for (int q = 0; q < min(BK_S - (XL_IN_RING ? 1 : 0), 2 * np); ++q) issue(q);
+    }
+    if (BK_TH > 0) __syncthreads();   // the barriers exist before any thread arrives on them
+    for (int q = 0; q < min(BK_S - (XL_IN_RING ? 1 : 0), 2 * np); ++q) {
+        if (tid == 0) issue(q);
+        issue_threads(q);
     }
     if (mode != SCHUR_CONDENSE)
         for (int l = tid; l < nG; l += BK_T) xl[l] = a.xin[a.Rg[d.goff + l]];
@@ -680,7 +699,10 @@ __global__ void __launch_bounds__(BK_T, 1) k_schur_blk(SchurArgs a) {
         v[r] = val;
     }
     __syncthreads();
-    if (XL_IN_RING && tid == 0 && BK_S - 1 < 2 * np) issue(BK_S - 1);   // the last stage is free of xl now
+    if (XL_IN_RING && BK_S - 1 < 2 * np) {   // the last stage is free of xl now
+        if (tid == 0) issue(BK_S - 1);
+        issue_threads(BK_S - 1);
+    }
     for (int q = 0; q < 2 * np; ++q) {
         mbar_wait(bar + (q % BK_S), uint32_t((q / BK_S) & 1));
         const double* P = pan + size_t(q % BK_S) * BK_P * ld;
@@ -758,7 +780,10 @@ __global__ void __launch_bounds__(BK_T, 1) k_schur_blk(SchurArgs a) {
             }
         }
         __syncthreads();
-        if (tid == 0 && q + BK_S < 2 * np) issue(q + BK_S);   // every reader is past this panel
+        if (q + BK_S < 2 * np) {   // every reader is past this panel
+            if (tid == 0) issue(q + BK_S);
+            issue_threads(q + BK_S);
+        }
     }
     if (mode == SCHUR_BACKSUB) {
         for (int i = tid; i < n; i += BK_T) a.u[idofs[i]] = v[i];
@@ -793,11 +818,11 @@ struct BlkVariant {
     int panel;
 };
 static BlkVariant blk_variant(int ld, int max_nI, int maxG, bool set_attr) {
-    static const int PS[6][2] = {{16, 2}, {8, 4}, {12, 3}, {8, 5}, {4, 8}, {16, 3}};
-    static const blk_fn FN[6] = {k_schur_blk<16, 2>, k_schur_blk<8, 4>, k_schur_blk<12, 3>, k_schur_blk<8, 5>, k_schur_blk<4, 8>,
-                                 k_schur_blk<16, 3>};
+    static const int PS[8][2] = {{16, 2}, {8, 4}, {12, 3}, {8, 5}, {4, 8}, {16, 3}, {16, 2}, {16, 3}};
+    static const blk_fn FN[8] = {k_schur_blk<16, 2>, k_schur_blk<8, 4>, k_schur_blk<12, 3>, k_schur_blk<8, 5>, k_schur_blk<4, 8>,
+                                 k_schur_blk<16, 3>, k_schur_blk<16, 2, 8>, k_schur_blk<16, 3, 8>};   // 6, 7: half of every panel by cp.async
     int v = 0;
-    if (const char* e = getenv("DE_BLK_VARIANT")) v = std::max(0, std::min(5, atoi(e)));
+    if (const char* e = getenv("DE_BLK_VARIANT")) v = std::max(0, std::min(7, atoi(e)));
     auto need = [&](int k) {   // rings of >= 3 stages keep xl in their last stage (no maxG term)
         return 128 + sizeof(double) * (size_t(PS[k][1]) * (PS[k][0] * ld + PS[k][0] * PS[k][0]) + max_nI + (PS[k][1] >= 3 ? 0 : maxG));
     };
