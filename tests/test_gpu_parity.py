@@ -105,6 +105,7 @@ def test_schur_apply_matches_oracle(name, kw):
                 B.de_schur_apply_device(S.ctx, dx.data_ptr(), dq.data_ptr())
                 q = dq.cpu().numpy()
                 assert np.linalg.norm(q - ref) <= 1e-11 * np.linalg.norm(ref), mode
+                assert np.abs(q - ref).max() <= 1e-11 * np.abs(ref).max(), mode          # element-wise
         finally:
             S.close()
 
@@ -134,6 +135,10 @@ def _check_precond(p, T, comps, impl):
             B.de_precond_apply_device(S.ctx, dr.data_ptr(), dz.data_ptr())
             z = dz.cpu().numpy()
             assert np.linalg.norm(z - ref) <= 1e-9 * np.linalg.norm(ref), (impl, np.linalg.norm(z - ref) / np.linalg.norm(ref))
+            for cd in comps:                                   # element-wise, per component (the norm is componentwise)
+                g = cd.skel.gidx
+                if np.abs(ref[g]).max() > 0:
+                    assert np.abs(z[g] - ref[g]).max() <= 1e-9 * np.abs(ref[g]).max(), impl
             if trial == 1:
                 assert np.all(z[comps[0].skel.gidx] == 0.0)
     finally:
