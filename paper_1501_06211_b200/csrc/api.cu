@@ -591,6 +591,7 @@ de_status_t upload_prec_impl(de_ctx* c) {
         }
         // face-interleaved tridiagonal copy (2D faces are paths): coalesced thread-per-face solves
         D.pat_id = nullptr;
+        D.td_start = D.td_len = nullptr;
         D.tri = 1;
         for (int F = 0; F < E.nfaces && D.tri; ++F) {
             const int o = E.face_off[F], n = E.face_off[F + 1] - o;
@@ -910,6 +911,31 @@ de_status_t upload_prec_impl(de_ctx* c) {
                     for (auto& q : rows[ci]) {
                         gcol.push_back(q.first);
                         gval.push_back(q.second);
+                    }
+                }
+                D.td_start = D.td_len = nullptr;
+                if (!getenv("DE_NO_TD")) {   // face descriptors of the same rows
+                    std::vector<int32_t> ts(size_t(XCF_W) * E.ncross, 0), tl(size_t(XCF_W) * E.ncross, 0), cnt(E.ncross, 0);
+                    bool ok = true;
+                    for (int F = 0; F < E.nfaces && ok; ++F) {
+                        const int o = E.face_off[F], n = E.face_off[F + 1] - o;
+                        for (int j = 0; j < n; ++j)
+                            if (E.face_nodes[o + j] != E.face_nodes[o] + j) ok = false;   // contiguous flat indices
+                        for (int k = 0; k < 2 && ok; ++k) {
+                            if (txj[2 * F + k] < 0) continue;
+                            const int ci = txc[2 * F + k];
+                            if (cnt[ci] >= XCF_W || n > 32) {
+                                ok = false;
+                                break;
+                            }
+                            ts[size_t(cnt[ci]) * E.ncross + ci] = E.face_nodes[o];
+                            tl[size_t(cnt[ci]) * E.ncross + ci] = n | (k << 8);
+                            ++cnt[ci];
+                        }
+                    }
+                    if (ok) {
+                        TRY(dupload(c, &D.td_start, ts));
+                        TRY(dupload(c, &D.td_len, tl));
                     }
                 }
                 TRY(dupload(c, &D.gt_ptr, gp));

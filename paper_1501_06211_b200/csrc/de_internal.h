@@ -259,6 +259,11 @@ struct ElimDev {
     // the right-hand side, so the first face phase forms it once per component (fuse only)
     int32_t *gt_ptr, *gt_col;
     double* gt_val;
+    // the same rows through face descriptors (faces are contiguous in the flat numbering): cross point ci couples to
+    // <= XCF_W faces f, td_start[f * ncross + ci] = flat index of the face's first node, td_len[..] = nodes | end << 8
+    // (end = which of the face's two couplings ci is: its G column is g_v0 / g_v1 over the face's nodes); 0 = none.
+    // One load level (the descriptors) before the coalesced g and b loads instead of ptr -> (val, col) -> b; null = CSR
+    int32_t *td_start, *td_len;
     // fold ELL (fuse only, eK): rows of M and L with <= FELL_W entries, every entry carrying its column's
     // elimination couplings, so the consumer's x = y - G x_C of each neighbour is two dependent load levels
     // instead of four (CSR ptr -> col -> g[col] -> xC[g]); [FELL_W][nflat] each; fell_col[0][i] = -1: CSR row

@@ -710,7 +710,45 @@ __device__ void elim_coop(cg::grid_group& grid, const CoopArgs& a, const ElimDev
         // t_C = scale (b_C - G^T b_F) once per cross point (needs only b), two cross points per warp in flight.
         // Formed FIRST and published through a split-phase arrival counter: the cross-point solve below waits for
         // every block's arrival instead of a grid barrier, and the face solves (which it does not need) run in between.
-        if (w > 0) {
+        if (w > 0 && E.td_start) {   // through the face descriptors: one level, then coalesced g and b loads
+            double* tCg = P.y + P.nflat + E.ncross;
+            for (int ci0 = gw; ci0 < E.ncross; ci0 += 2 * nwarps) {
+                int st[2][XCF_W], ln[2][XCF_W], cf[2];
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const int ci = ci0 + u * nwarps;
+                    const bool ok = ci < E.ncross;
+                    cf[u] = ok ? E.cross_flat[ci] : 0;
+#pragma unroll
+                    for (int f = 0; f < XCF_W; ++f) {
+                        st[u][f] = ok ? E.td_start[size_t(f) * E.ncross + ci] : 0;
+                        ln[u][f] = ok ? E.td_len[size_t(f) * E.ncross + ci] : 0;
+                    }
+                }
+                double gv[2][XCF_W], bv[2][XCF_W];
+#pragma unroll
+                for (int u = 0; u < 2; ++u)
+#pragma unroll
+                    for (int f = 0; f < XCF_W; ++f) {
+                        const int n = ln[u][f] & 0xff, i = st[u][f] + lane;
+                        const bool ok = lane < n;
+                        gv[u][f] = ok ? ((ln[u][f] >> 8) ? E.g_v1[i] : E.g_v0[i]) : 0.0;
+                        bv[u][f] = ok ? b[bmap ? bmap[i] : i] : 0.0;
+                    }
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const int ci = ci0 + u * nwarps;
+                    double acc = 0.0;
+#pragma unroll
+                    for (int f = 0; f < XCF_W; ++f) acc = fma(gv[u][f], bv[u][f], acc);
+                    const double sgt = warp_sum(acc);
+                    if (lane == 0 && ci < E.ncross) {
+                        tCg[ci] = scl[ccomp(P.comp_off, P.ncomp, cf[u])] * (b[bmap ? bmap[cf[u]] : cf[u]] - sgt);
+                        if (fold_j > 0) a.ucross[size_t(fold_j - 1) * E.ncross + ci] = sgt;
+                    }
+                }
+            }
+        } else if (w > 0) {
             double* tCg = P.y + P.nflat + E.ncross;
             for (int ci0 = gw; ci0 < E.ncross; ci0 += 2 * nwarps) {
                 double acc[2] = {0.0, 0.0};
