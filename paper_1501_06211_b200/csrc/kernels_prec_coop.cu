@@ -875,6 +875,10 @@ __device__ void elim_coop(cg::grid_group& grid, const CoopArgs& a, const ElimDev
             __syncthreads();
         }
         const bool shr = use_shr(a, E, c);
+        // fold: (MW_t[c_r] - u_t[r]) of this block's rows, loaded BEFORE the cross-point GEMV (they are complete once every
+        // block has arrived) so that the fold sums after it read shared memory only
+        double cmine = 0.0;
+        bool cpre = false;
         if (shr) {
             // Shared S_C^-1: every block owns rows [Rlo, Rhi) of the ONE matrix (split over the whole grid) and applies
             // them to the t_C of every component, so each row crosses L2 -> SM once instead of once per component
@@ -1144,6 +1148,12 @@ __device__ void elim_coop(cg::grid_group& grid, const CoopArgs& a, const ElimDev
                 // ~13 rows (c5) take 4 dependent batches instead of 7); warp partials are summed in fixed order
                 const int cw = ((ncc + CW * 32 - 1) / (CW * 32)) * 32;
                 const int c0 = w * cw, c1 = min(ncc, c0 + cw);
+                cpre = fold_j > 0 && kc * nr <= CT && ncc + (CW + KMAX) * nr <= a.smem_doubles;
+                if (cpre && int(threadIdx.x) < kc * nr) {
+                    const int t = threadIdx.x / nr, rr = threadIdx.x - t * nr;
+                    const int cfi = E.cross_flat[base + rlo + rr];
+                    cmine = P.MW[size_t(t) * P.nflat + cfi] - a.ucross[size_t(t) * E.ncross + base + rlo + rr];
+                }
                 if (a.sc_persist && &E == &a.P.eK) sc_rows<false>(S, ncc, rlo, rhi, nr, c0, c1, w, lane, tC, part);
                 else sc_rows<true>(S, ncc, rlo, rhi, nr, c0, c1, w, lane, tC, part);
             }
@@ -1165,9 +1175,17 @@ __device__ void elim_coop(cg::grid_group& grid, const CoopArgs& a, const ElimDev
             // the face part over the warps (summed per warp in the face phase)
             const int rlo = ncc > 0 ? int(int64_t(lb) * ncc / nbc) : 0, rhi = ncc > 0 ? int(int64_t(lb + 1) * ncc / nbc) : 0;
             const double* xr = (fd ? dsm : dsm + ncc);
+            const int nr = rhi - rlo;
+            double* prod = dsm + ncc + CW * nr;   // [kc][nr] behind the dense path's row sums
+            if (cpre) {
+                if (int(threadIdx.x) < kc * nr) prod[threadIdx.x] = cmine * xr[threadIdx.x % nr];
+                __syncthreads();
+            }
             for (int v = w; v <= kc; v += CW) {
                 double t_ = 0.0;
-                if (v > 0)
+                if (v > 0 && cpre) {
+                    for (int r = lane; r < nr; r += 32) t_ += prod[(v - 1) * nr + r];
+                } else if (v > 0)
                     for (int r = rlo + lane; r < rhi; r += 32) {
                         const int cf = E.cross_flat[base + r];
                         t_ += (P.MW[size_t(v - 1) * P.nflat + cf] - a.ucross[size_t(v - 1) * E.ncross + base + r]) * xr[r - rlo];
